@@ -1,0 +1,199 @@
+/*
+ * bppsa.h — C-ABI of libbppsa.so, a B200 (sm_100a) implementation of the hot
+ * path of BPPSA: back-propagation as a modified Blelloch exclusive scan
+ * (Wang, Bai & Pekhimenko, arXiv 1907.10134; "P:<n>" = line n of PAPER.md).
+ *
+ * Conventions (apply to every entry point)
+ *   - All tensor pointers are DEVICE pointers (caller-owned, e.g. torch
+ *     allocations) unless a comment says "host".  The library never frees or
+ *     keeps caller memory; the only library-owned objects are CSR plans
+ *     (create/destroy pair).
+ *   - fp32 everywhere (reading 11 in DESIGN.md); row-major C layouts.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *     asynchronous on `stream`, validates all arguments before launching and
+ *     returns a status; nothing crosses the ABI as an exception.  On error no
+ *     partial-output guarantee is made.  bppsa_last_error() returns a
+ *     thread-local detail string for the last failing call.
+ *   - Calls are re-entrant per stream and capturable into CUDA graphs (no
+ *     allocation, no synchronisation inside compute calls).
+ *   - Results are bitwise reproducible for fixed shapes/options/build.
+ *
+ * Notation: T steps, B batch, H hidden size (1 <= H <= 64), I input size.
+ * h_t = f_t(h_{t-1}); J_t = dh_t/dh_{t-1}; grad_h[t] = dl/dh_t.
+ * Scan array (eqn:scan_input), scan order:
+ *     a = [seed, J_{T-1}^T, ..., J_0^T],   A <> B = B A
+ * Exclusive scan (Alg. 1 "Ensure"): output at the slot holding J_t^T is
+ * grad_h[t]; the inclusive extra J_0^T grad_h[0] is dl/dh_init.
+ */
+#ifndef BPPSA_H_
+#define BPPSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BPPSA_MAX_H 64
+
+typedef enum {
+  BPPSA_OK = 0,
+  BPPSA_ERR_INVALID_ARGUMENT = 1, /* null/host pointer, T/B/H out of range      */
+  BPPSA_ERR_SHAPE = 2,            /* incompatible shapes                  */
+  BPPSA_ERR_PLAN = 3,             /* CSR plan does not match the data     */
+  BPPSA_ERR_WORKSPACE = 4,        /* workspace too small or misaligned           */
+  BPPSA_ERR_CUDA = 5,             /* a CUDA runtime error (detail in last_error) */
+  BPPSA_ERR_NCCL = 6,             /* reserved                                    */
+  BPPSA_ERR_NOT_SUPPORTED = 7     /* valid request outside what this build does */
+} bppsa_status;
+
+const char* bppsa_status_str(bppsa_status s);
+const char* bppsa_last_error(void);
+/* 10000*major + 100*minor + patch */
+int bppsa_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Leaf transposed Jacobians (the scan's elements).
+ * ------------------------------------------------------------------------- */
+typedef enum {
+  BPPSA_JAC_DENSE = 0,    /* explicit J_t^T                                   */
+  BPPSA_JAC_RNN_TANH = 1, /* J_t^T = W_hh^T diag(1 - h_t^2)  (eqn:rnn) */
+  BPPSA_JAC_GRU = 2       /* eqn:gru_jcb, transposed reading      */
+} bppsa_jac_kind;
+
+/* A description of the T transposed Jacobians of one (shard of a) sequence.
+ * Only pointers are stored; the tensors stay caller-owned.                  */
+typedef struct bppsa_jac {
+  int kind;             /* bppsa_jac_kind                                      */
+  int T, B, H;
+  const float* JT;      /* DENSE: [T][B][H][H], JT[t][b][i][k] = (J_t^T)[i][k]  */
+  const float* h;       /* RNN:   [T][B][H]  h_t (tanh outputs, time-major)      */
+  const float* W_hh;    /* RNN:   [H][H]     torch weight_hh_l0                  */
+  const float* h_prev;  /* GRU:   [T][B][H]  h_{t-1}                             */
+  const float* r;       /* GRU:   [T][B][H]  reset gate                          */
+  const float* z;       /* GRU:   [T][B][H]  update gate                         */
+  const float* n;       /* GRU:   [T][B][H]  candidate                           */
+  const float* M;       /* GRU:   [T][B][H]  W_hn h_{t-1} + b_hn (eqn:gru_rewrite)*/
+  const float* W_hh3;   /* GRU:   [3H][H]    torch weight_hh_l0, gates (r, z, n) */
+} bppsa_jac;
+
+/* Describe the tanh-RNN leaves J_t^T = W_hh^T diag(1-h_t^2).
+ * JT_out == NULL: fill *desc with a fused descriptor (J^T is rebuilt inside the
+ * scan kernels and never written to HBM).  JT_out != NULL ([T][B][H][H]):
+ * materialise the matrices there and return a DENSE descriptor of JT_out.   */
+bppsa_status bppsa_jacobians_rnn(int T, int B, int H, const float* h,
+                                 const float* W_hh, float* JT_out,
+                                 bppsa_jac* desc, void* stream);
+
+/* GRU leaves per eqn:gru_jcb from the saved tape:
+ * J^T = W_hr^T diag(r(1-r)M(1-n^2)(1-z)) + W_hn^T diag(r(1-n^2)(1-z))
+ *     + W_hz^T diag(z(1-z)(h_{t-1}-n)) + diag(z).   Fused (H <= 32) or
+ * materialised as for bppsa_jacobians_rnn.                                  */
+bppsa_status bppsa_jacobians_gru(int T, int B, int H, const float* h_prev,
+                                 const float* r, const float* z, const float* n,
+                                 const float* M, const float* W_hh3,
+                                 float* JT_out, bppsa_jac* desc, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * The scan (Alg. 1).
+ * ------------------------------------------------------------------------- */
+typedef enum {
+  /* Blelloch's p < n regime (S = Theta(n/p + log p)): blocks of
+   * `block0` leaf slots are folded serially (up-sweep) and walked serially
+   * (down-sweep, GEMV only); the block aggregates are scanned recursively by
+   * the same two-phase scheme in blocks of `block` slots.                     */
+  BPPSA_SCAN_BLOCKED = 0,
+  /* Alg. 1 executed literally, one launch per level, over a workspace copy of
+   * the materialised array (DENSE only; same association as the oracle's
+   * serial Alg. 1).                                                           */
+  BPPSA_SCAN_ALG1 = 1,
+  /* The linear scan = sequential BP on the GPU (S_Linear = Theta(n)):
+   * the comparator.                                                          */
+  BPPSA_SCAN_LINEAR = 2
+} bppsa_scan_mode;
+
+typedef struct bppsa_scan_opts {
+  int mode;    /* bppsa_scan_mode                                              */
+  int block0;  /* BLOCKED: leaf block length in slots (0 = default)            */
+  int block;   /* BLOCKED: block length of the upper levels (0 = default)      */
+  /* Optional instrumentation (all may be NULL/0): if `events` is non-NULL the
+   * library records events[2k] / events[2k+1] (cudaEvent_t, created by the
+   * caller) on `stream` immediately before / after its k-th kernel launch,
+   * k < n_events/2.  `launches` (host int*) receives the number of kernels
+   * the call launched.                                                        */
+  void** events;
+  int n_events;
+  int* launches;
+} bppsa_scan_opts;   /* NULL opts = all defaults */
+
+/* Workspace bytes needed by bppsa_scan / the shard calls for this
+ * description and options (256-byte alignment required).                    */
+bppsa_status bppsa_scan_workspace_size(const bppsa_jac* jac,
+                                       const bppsa_scan_opts* opts,
+                                       size_t* bytes);
+
+/* Single-GPU scan.  seed [B][H] = dl/dh_{T-1} (a0).  grad_h [T][B][H] out:
+ * grad_h[t] = dl/dh_t, grad_h[T-1] = seed.  grad_h_init [B][H] out, nullable:
+ * J_0^T grad_h[0] = dl/dh_init.  ws: device workspace of at least
+ * bppsa_scan_workspace_size() bytes (contents are scratch).                 */
+bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h,
+                        float* grad_h_init, void* ws, size_t ws_bytes,
+                        const bppsa_scan_opts* opts, void* stream);
+
+/* Multi-GPU: contiguous time shards, rank order = time order.
+ * `jac` describes this rank's T_local steps.  The rank holding t = T-1 (the
+ * last rank) passes its seed and is the "head" shard.
+ *
+ * shard_up: local leaf + up-sweep to one aggregate per sample, written to
+ *   aggregate [B][H][H] (column-major: element (i,k) at k*H+i), the product
+ *   J_lo^T ... J_hi^T of this shard; for the head shard the aggregate is the
+ *   vector grad_h[lo-1] in aggregate[b*H*H + 0..H-1].  `ws` must be preserved
+ *   until the matching shard_down.
+ * shard_down: gathered = all ranks' aggregates [world][B][H*H] (rank order);
+ *   computes this rank's carry grad_h[hi] = M_{r+1}...M_{G-2} V_{G-1} on the
+ *   device and runs the local down-sweep into grad_h [T_local][B][H];
+ *   grad_h_init (nullable) receives J_lo^T grad_h[lo] (= dl/dh_init on rank 0).
+ * Between the two calls the caller all-gathers `aggregate` (NCCL over
+ * NVLink via torch.distributed in the Python binding).                     */
+bppsa_status bppsa_scan_shard_up(const bppsa_jac* jac, const float* seed,
+                                 float* aggregate, void* ws, size_t ws_bytes,
+                                 const bppsa_scan_opts* opts, void* stream);
+bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed,
+                                   const float* gathered, int rank, int world,
+                                   float* grad_h, float* grad_h_init, void* ws,
+                                   size_t ws_bytes, const bppsa_scan_opts* opts,
+                                   void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Parameter gradients, eqn:update_param, tied weights summed over
+ * time.  Deterministic (fixed-order) reductions, no float atomics.
+ * ------------------------------------------------------------------------- */
+bppsa_status bppsa_weight_grads_workspace_size(int T, int B, int H, int I,
+                                               size_t* bytes);
+
+/* RNN: delta_t = (1-h_t^2) o grad_h[t]; dW_hh = sum delta_t h_{t-1}^T [H][H],
+ * dW_ih = sum delta_t x_t^T [H][I], db = sum delta_t [H] (= db_ih = db_hh).
+ * x [T][B][I]; h [T][B][H]; h_init [B][H] nullable (=> h_{-1} = 0).          */
+bppsa_status bppsa_weight_grads_rnn(int T, int B, int H, int I, const float* x,
+                                    const float* h, const float* h_init,
+                                    const float* grad_h, float* dW_ih,
+                                    float* dW_hh, float* db, void* ws,
+                                    size_t ws_bytes, void* stream);
+
+/* GRU (gates r,z,n order as torch): dN = g(1-z)(1-n^2), dZ = g(h_prev-n)z(1-z),
+ * dR = dN M r(1-r), dM = dN r;  dW_ih3 = [dR;dZ;dN] x^T [3H][I],
+ * dW_hh3 = [dR;dZ;dM] h_prev^T [3H][H], db_ih3 = sum [dR;dZ;dN],
+ * db_hh3 = sum [dR;dZ;dM] ([3H] each).                                       */
+bppsa_status bppsa_weight_grads_gru(int T, int B, int H, int I, const float* x,
+                                    const float* h_prev, const float* r,
+                                    const float* z, const float* n,
+                                    const float* M, const float* grad_h,
+                                    float* dW_ih3, float* dW_hh3, float* db_ih3,
+                                    float* db_hh3, void* ws, size_t ws_bytes,
+                                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BPPSA_H_ */

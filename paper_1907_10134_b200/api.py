@@ -1,0 +1,250 @@
+"""Thin Python binding of libbppsa.so (include/bppsa.h) — argument marshalling
+only.  Every arithmetic step of the path runs in the library's sm_100a
+kernels; torch supplies device memory, the current CUDA stream and (for the
+sharded scan) the NCCL process group.  There is no CPU fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbppsa.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"{_LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+_lib = C.CDLL(_LIB_PATH)
+
+# ----------------------------------------------------------------- ABI types
+OK = 0
+JAC_DENSE, JAC_RNN_TANH, JAC_GRU = 0, 1, 2
+SCAN_BLOCKED, SCAN_ALG1, SCAN_LINEAR = 0, 1, 2
+MODES = {"blocked": SCAN_BLOCKED, "alg1": SCAN_ALG1, "linear": SCAN_LINEAR}
+
+_vp, _i, _sz = C.c_void_p, C.c_int, C.c_size_t
+
+
+class _Jac(C.Structure):
+    _fields_ = [("kind", _i), ("T", _i), ("B", _i), ("H", _i), ("JT", _vp), ("h", _vp), ("W_hh", _vp),
+                ("h_prev", _vp), ("r", _vp), ("z", _vp), ("n", _vp), ("M", _vp), ("W_hh3", _vp)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("mode", _i), ("block0", _i), ("block", _i), ("events", C.POINTER(_vp)), ("n_events", _i),
+                ("launches", C.POINTER(_i))]
+
+
+EXPORTS = {
+    "bppsa_status_str": (C.c_char_p, [_i]),
+    "bppsa_last_error": (C.c_char_p, []),
+    "bppsa_version": (_i, []),
+    "bppsa_jacobians_rnn": (_i, [_i, _i, _i, _vp, _vp, _vp, C.POINTER(_Jac), _vp]),
+    "bppsa_jacobians_gru": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_Jac), _vp]),
+    "bppsa_scan_workspace_size": (_i, [C.POINTER(_Jac), C.POINTER(_Opts), C.POINTER(_sz)]),
+    "bppsa_scan": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_scan_shard_up": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_scan_shard_down": (_i, [C.POINTER(_Jac), _vp, _vp, _i, _i, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_weight_grads_workspace_size": (_i, [_i, _i, _i, _i, C.POINTER(_sz)]),
+    "bppsa_weight_grads_rnn": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "bppsa_weight_grads_gru": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _sz, _vp]),
+}
+for _name, (_res, _args) in EXPORTS.items():
+    _f = getattr(_lib, _name)
+    _f.restype, _f.argtypes = _res, _args
+
+
+class BppsaError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.bppsa_status_str(status).decode()
+        detail = _lib.bppsa_last_error().decode()
+        super().__init__(f"{where}: {msg}: {detail}")
+        self.status = status
+
+
+def _check(status: int, where: str) -> None:
+    if status != OK:
+        raise BppsaError(status, where)
+
+
+def _ptr(t: torch.Tensor | None, name: str = "tensor"):
+    if t is None:
+        return None
+    if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    return t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def version() -> int:
+    return _lib.bppsa_version()
+
+
+# ----------------------------------------------------------------- leaves
+class Jacobians:
+    """A bppsa_jac descriptor plus references that keep its tensors alive."""
+
+    def __init__(self, desc: _Jac, keep):
+        self.desc = desc
+        self._keep = keep
+
+    T = property(lambda self: self.desc.T)
+    B = property(lambda self: self.desc.B)
+    H = property(lambda self: self.desc.H)
+    kind = property(lambda self: self.desc.kind)
+
+
+def jacobians_rnn(h: torch.Tensor, W_hh: torch.Tensor, JT_out: torch.Tensor | None = None, stream=None):
+    """bppsa_jacobians_rnn: J_t^T = W_hh^T diag(1-h_t^2) (fused descriptor, or
+    materialised into JT_out [T,B,H,H])."""
+    T, B, H = h.shape
+    d = _Jac()
+    _check(_lib.bppsa_jacobians_rnn(T, B, H, _ptr(h, "h"), _ptr(W_hh, "W_hh"), _ptr(JT_out, "JT_out"),
+                                    C.byref(d), _stream(stream)), "bppsa_jacobians_rnn")
+    return Jacobians(d, (h, W_hh, JT_out))
+
+
+def jacobians_gru(h_prev, r, z, n, M, W_hh3, JT_out: torch.Tensor | None = None, stream=None):
+    """bppsa_jacobians_gru: eqn:gru_jcb leaves from the saved GRU tape."""
+    T, B, H = r.shape
+    d = _Jac()
+    _check(_lib.bppsa_jacobians_gru(T, B, H, _ptr(h_prev, "h_prev"), _ptr(r, "r"), _ptr(z, "z"), _ptr(n, "n"),
+                                    _ptr(M, "M"), _ptr(W_hh3, "W_hh3"), _ptr(JT_out, "JT_out"), C.byref(d),
+                                    _stream(stream)), "bppsa_jacobians_gru")
+    return Jacobians(d, (h_prev, r, z, n, M, W_hh3, JT_out))
+
+
+def jacobians_dense(JT: torch.Tensor) -> Jacobians:
+    """A DENSE descriptor over caller-provided J_t^T [T,B,H,H] (row-major)."""
+    T, B, H, H2 = JT.shape
+    assert H == H2
+    d = _Jac()
+    d.kind, d.T, d.B, d.H, d.JT = JAC_DENSE, T, B, H, _ptr(JT, "JT")
+    return Jacobians(d, (JT,))
+
+
+# ----------------------------------------------------------------- scan
+def _opts(mode="blocked", block0=0, block=0, trace=None) -> _Opts:
+    o = _Opts(MODES[mode] if isinstance(mode, str) else int(mode), int(block0), int(block))
+    if trace is not None:
+        o.events, o.n_events, o.launches = trace._arr, len(trace.events), C.pointer(trace._count)
+    return o
+
+
+class LaunchTrace:
+    """Per-launch CUDA events for bppsa_scan_opts.events (instrumentation):
+    events[2k] / events[2k+1] bracket the library's k-th kernel launch."""
+
+    def __init__(self, max_launches: int = 64):
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * max_launches)]
+        for e in self.events:          # materialise the cudaEvent_t handles
+            e.record()
+        torch.cuda.synchronize()
+        self._arr = (_vp * len(self.events))(*[e.cuda_event for e in self.events])
+        self._count = _i(0)
+
+    @property
+    def launches(self) -> int:
+        return self._count.value
+
+    def kernel_ms(self, k: int) -> float:
+        return self.events[2 * k].elapsed_time(self.events[2 * k + 1])
+
+
+def scan_workspace_size(jac: Jacobians, mode="blocked", block0=0, block=0) -> int:
+    n = _sz()
+    o = _opts(mode, block0, block)
+    _check(_lib.bppsa_scan_workspace_size(C.byref(jac.desc), C.byref(o), C.byref(n)), "bppsa_scan_workspace_size")
+    return n.value
+
+
+def workspace(nbytes: int, device=None) -> torch.Tensor:
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device or "cuda")
+
+
+def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
+         grad_h_init: torch.Tensor | bool | None = None, ws: torch.Tensor | None = None,
+         mode="blocked", block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None):
+    """bppsa_scan: all grad_h[t] = dl/dh_t at once (and dl/dh_init if asked)."""
+    T, B, H = jac.T, jac.B, jac.H
+    dev = seed.device
+    if grad_h is None:
+        grad_h = torch.empty((T, B, H), dtype=torch.float32, device=dev)
+    if grad_h_init is True:
+        grad_h_init = torch.empty((B, H), dtype=torch.float32, device=dev)
+    elif grad_h_init is False:
+        grad_h_init = None
+    o = _opts(mode, block0, block, trace)
+    if ws is None:
+        ws = workspace(scan_workspace_size(jac, mode, block0, block), dev)
+    _check(_lib.bppsa_scan(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(grad_h, "grad_h"),
+                           _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
+                           _stream(stream)), "bppsa_scan")
+    return grad_h, grad_h_init
+
+
+def scan_shard_up(jac: Jacobians, seed: torch.Tensor | None, aggregate: torch.Tensor, ws: torch.Tensor,
+                  block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None):
+    o = _opts("blocked", block0, block, trace)
+    _check(_lib.bppsa_scan_shard_up(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(aggregate, "aggregate"),
+                                    ws.data_ptr(), ws.numel(), C.byref(o), _stream(stream)), "bppsa_scan_shard_up")
+    return aggregate
+
+
+def scan_shard_down(jac: Jacobians, seed: torch.Tensor | None, gathered: torch.Tensor | None, rank: int,
+                    world: int, grad_h: torch.Tensor, grad_h_init: torch.Tensor | None, ws: torch.Tensor,
+                    block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None):
+    o = _opts("blocked", block0, block, trace)
+    _check(_lib.bppsa_scan_shard_down(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(gathered, "gathered"), rank,
+                                      world, _ptr(grad_h, "grad_h"), _ptr(grad_h_init, "grad_h_init"),
+                                      ws.data_ptr(), ws.numel(), C.byref(o), _stream(stream)),
+           "bppsa_scan_shard_down")
+    return grad_h, grad_h_init
+
+
+# ----------------------------------------------------------------- weight grads
+def weight_grads_workspace_size(T, B, H, I) -> int:
+    n = _sz()
+    _check(_lib.bppsa_weight_grads_workspace_size(T, B, H, I, C.byref(n)), "bppsa_weight_grads_workspace_size")
+    return n.value
+
+
+def weight_grads_rnn(x, h, grad_h, h_init=None, ws=None, out=None, stream=None):
+    """bppsa_weight_grads_rnn -> (dW_ih [H,I], dW_hh [H,H], db [H])."""
+    T, B, H = h.shape
+    I = x.shape[2]
+    dev = h.device
+    if out is None:
+        out = (torch.empty((H, I), device=dev), torch.empty((H, H), device=dev), torch.empty((H,), device=dev))
+    if ws is None:
+        ws = workspace(weight_grads_workspace_size(T, B, H, I), dev)
+    dW_ih, dW_hh, db = out
+    _check(_lib.bppsa_weight_grads_rnn(T, B, H, I, _ptr(x, "x"), _ptr(h, "h"), _ptr(h_init, "h_init"),
+                                       _ptr(grad_h, "grad_h"), _ptr(dW_ih, "dW_ih"), _ptr(dW_hh, "dW_hh"),
+                                       _ptr(db, "db"), ws.data_ptr(), ws.numel(), _stream(stream)),
+           "bppsa_weight_grads_rnn")
+    return dW_ih, dW_hh, db
+
+
+def weight_grads_gru(x, tape: dict, grad_h, ws=None, out=None, stream=None):
+    """bppsa_weight_grads_gru -> (dW_ih3 [3H,I], dW_hh3 [3H,H], db_ih3 [3H], db_hh3 [3H])."""
+    T, B, H = tape["r"].shape
+    I = x.shape[2]
+    dev = grad_h.device
+    if out is None:
+        out = (torch.empty((3 * H, I), device=dev), torch.empty((3 * H, H), device=dev),
+               torch.empty((3 * H,), device=dev), torch.empty((3 * H,), device=dev))
+    if ws is None:
+        ws = workspace(weight_grads_workspace_size(T, B, H, I), dev)
+    a, b_, c, d = out
+    _check(_lib.bppsa_weight_grads_gru(T, B, H, I, _ptr(x, "x"), _ptr(tape["h_prev"], "h_prev"),
+                                       _ptr(tape["r"], "r"), _ptr(tape["z"], "z"), _ptr(tape["n"], "n"),
+                                       _ptr(tape["M"], "M"), _ptr(grad_h, "grad_h"), _ptr(a, "dW_ih3"),
+                                       _ptr(b_, "dW_hh3"), _ptr(c, "db_ih3"), _ptr(d, "db_hh3"), ws.data_ptr(),
+                                       ws.numel(), _stream(stream)), "bppsa_weight_grads_gru")
+    return out

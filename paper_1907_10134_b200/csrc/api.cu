@@ -1,0 +1,579 @@
+// api.cu — the C-ABI of libbppsa (include/bppsa.h): validation, workspace
+// planning and launch sequencing of the blocked Blelloch scan.
+//
+// Level structure (BPPSA_SCAN_BLOCKED).  Level 0 is the scan array itself
+// (n_0 = S = T + head slots, leaves implicit or DENSE).  Level l+1 holds the
+// aggregates of the blocks of C_l consecutive slots of level l
+// (n_{l+1} = ceil(n_l / C_l)).  The up-sweep folds blocks bottom-up; the
+// down-sweep walks every block from its exclusive prefix (the output of the
+// level above) — Blelloch's Theta(n/p + log p) schedule with every
+// matrix-matrix product in the up-sweep and only GEMVs in the down-sweep
+// (P:135).  Single-GPU: folding stops when a level fits one block; that level
+// is walked from the symbolic identity (root reset).  Shards fold to
+// one aggregate per sample, exchange, and walk from the received carry.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace bppsa {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+bppsa_status fail(bppsa_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+bppsa_status cuda_status(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return BPPSA_ERR_CUDA;
+}
+
+namespace {
+
+constexpr int kMaxLevels = 48;
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+#define REQUIRE_DEV(p, name)                                                               \
+  do {                                                                                     \
+    if (!is_device_ptr(p))                                                                 \
+      return fail(BPPSA_ERR_INVALID_ARGUMENT, std::string(name) + " must be a device pointer"); \
+  } while (0)
+
+// Per-call launch instrumentation (bppsa_scan_opts.events / launches).
+struct Tracer {
+  cudaEvent_t* ev = nullptr;
+  int n_ev = 0;
+  int k = 0;
+  void begin(cudaStream_t st) {
+    if (ev && 2 * k + 1 < n_ev) cudaEventRecord(ev[2 * k], st);
+  }
+  void end(cudaStream_t st) {
+    if (ev && 2 * k + 1 < n_ev) cudaEventRecord(ev[2 * k + 1], st);
+    ++k;
+  }
+};
+
+Tracer tracer_from(const bppsa_scan_opts* o) {
+  Tracer t;
+  if (o && o->events) {
+    t.ev = reinterpret_cast<cudaEvent_t*>(o->events);
+    t.n_ev = o->n_events;
+  }
+  return t;
+}
+
+void report_launches(const bppsa_scan_opts* o, const Tracer& t) {
+  if (o && o->launches) *o->launches = t.k;
+}
+
+struct Plan {
+  int L = 0;
+  long long n[kMaxLevels + 2] = {};
+  int C[kMaxLevels + 2] = {};
+  size_t agg_off[kMaxLevels + 2] = {}, out_off[kMaxLevels + 2] = {};
+  size_t dense_off = 0, carry_off = 0, total = 0;
+  bool has_dense = false;
+};
+
+int default_block0(const bppsa_jac& j) { return j.H <= 32 ? 16 : 64; }
+int default_block(const bppsa_jac& j) { return j.H <= 32 ? 16 : 32; }
+
+bppsa_status check_jac(const bppsa_jac* j, bool need_ptrs = true) {
+  if (!j) return fail(BPPSA_ERR_INVALID_ARGUMENT, "jac is NULL");
+  if (j->T < 1 || j->B < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "T and B must be >= 1 (reading 5)");
+  if (j->H < 1 || j->H > BPPSA_MAX_H) return fail(BPPSA_ERR_INVALID_ARGUMENT, "H must be in [1, 64]");
+  if (j->kind == BPPSA_JAC_DENSE) {
+    if (need_ptrs) REQUIRE_DEV(j->JT, "jac.JT");
+  } else if (j->kind == BPPSA_JAC_RNN_TANH) {
+    if (need_ptrs) {
+      REQUIRE_DEV(j->h, "jac.h");
+      REQUIRE_DEV(j->W_hh, "jac.W_hh");
+    }
+  } else if (j->kind == BPPSA_JAC_GRU) {
+    if (j->H > 32)
+      return fail(BPPSA_ERR_NOT_SUPPORTED, "fused GRU leaves need H <= 32; materialise (JT_out) for larger H");
+    if (need_ptrs) {
+      REQUIRE_DEV(j->h_prev, "jac.h_prev");
+      REQUIRE_DEV(j->r, "jac.r");
+      REQUIRE_DEV(j->z, "jac.z");
+      REQUIRE_DEV(j->n, "jac.n");
+      REQUIRE_DEV(j->M, "jac.M");
+      REQUIRE_DEV(j->W_hh3, "jac.W_hh3");
+    }
+  } else {
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "unknown jac.kind");
+  }
+  return BPPSA_OK;
+}
+
+bppsa_status get_opts(const bppsa_jac& j, const bppsa_scan_opts* o, int* mode, int* C0, int* C) {
+  *mode = o ? o->mode : BPPSA_SCAN_BLOCKED;
+  *C0 = (o && o->block0 > 0) ? o->block0 : default_block0(j);
+  *C = (o && o->block > 0) ? o->block : default_block(j);
+  if (*mode != BPPSA_SCAN_BLOCKED && *mode != BPPSA_SCAN_ALG1 && *mode != BPPSA_SCAN_LINEAR)
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "unknown scan mode");
+  if (*C0 < 2 || *C < 2) return fail(BPPSA_ERR_INVALID_ARGUMENT, "block lengths must be >= 2");
+  if (*mode == BPPSA_SCAN_ALG1 && j.kind != BPPSA_JAC_DENSE)
+    return fail(BPPSA_ERR_NOT_SUPPORTED, "ALG1 mode runs on materialised (DENSE) leaves");
+  return BPPSA_OK;
+}
+
+bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts, bool need_total, Plan* p) {
+  int mode, C0, C;
+  bppsa_status s = get_opts(j, opts, &mode, &C0, &C);
+  if (s != BPPSA_OK) return s;
+  const long long S = (long long)j.T + head;
+  const size_t HH = (size_t)j.H * j.H, B = (size_t)j.B;
+  size_t off = 0;
+  p->has_dense = (j.kind == BPPSA_JAC_DENSE) && mode != BPPSA_SCAN_ALG1;
+  if (p->has_dense) {
+    p->dense_off = off;
+    off = align_up(off + (size_t)j.T * B * HH * sizeof(float));
+  }
+  if (mode == BPPSA_SCAN_ALG1) {
+    p->L = 0;
+    p->dense_off = off;
+    off = align_up(off + (size_t)(j.T + 1) * B * HH * sizeof(float));
+    p->total = off;
+    return BPPSA_OK;
+  }
+  p->n[0] = S;
+  int l = 0;
+  if (mode == BPPSA_SCAN_LINEAR) {
+    p->C[0] = (int)std::min<long long>(S, 1ll << 30);
+  } else {
+    while (true) {
+      const int Cl = (l == 0) ? C0 : C;
+      p->C[l] = Cl;
+      if (!need_total && p->n[l] <= Cl) break;
+      if (need_total && l > 0 && p->n[l] == 1) break;
+      if (l >= kMaxLevels) return fail(BPPSA_ERR_INVALID_ARGUMENT, "too many levels");
+      p->n[l + 1] = (p->n[l] + Cl - 1) / Cl;
+      ++l;
+    }
+  }
+  p->L = l;
+  for (int k = 1; k <= p->L; ++k) {
+    p->agg_off[k] = off;
+    off = align_up(off + B * (size_t)p->n[k] * HH * sizeof(float));
+    p->out_off[k] = off;
+    off = align_up(off + B * (size_t)p->n[k] * j.H * sizeof(float));
+  }
+  p->carry_off = off;
+  off = align_up(off + B * j.H * sizeof(float));
+  p->total = off;
+  return BPPSA_OK;
+}
+
+LeafArgs leaf_args(const bppsa_jac& j, int head, const float* seed) {
+  LeafArgs a{};
+  a.seg = Seg{j.T, j.B, j.H, head};
+  a.kind = j.kind;
+  if (j.kind == BPPSA_JAC_RNN_TANH) {
+    a.h = j.h;
+    a.W = j.W_hh;
+  } else {
+    a.W = j.W_hh3;
+    a.hp = j.h_prev;
+    a.r = j.r;
+    a.z = j.z;
+    a.n = j.n;
+    a.M = j.M;
+  }
+  a.seed = seed;
+  return a;
+}
+
+// level-0 accessor over the transposed DENSE copy (column-major per matrix)
+MatAcc dense_acc(const bppsa_jac& j, int head, const float* JTc, const float* seed) {
+  const long long HH = (long long)j.H * j.H;
+  MatAcc A{};
+  const long long t0 = head ? j.T : (long long)j.T - 1;   // time of slot 0 (+ formally)
+  A.base = JTc + t0 * j.B * HH;
+  A.slot_stride = -(long long)j.B * HH;
+  A.batch_stride = HH;
+  A.head_vec = seed;
+  A.head_bstride = j.H;
+  return A;
+}
+
+MatAcc level_acc(const Plan& p, char* ws, int l, int H) {
+  const long long HH = (long long)H * H;
+  MatAcc A{};
+  A.base = reinterpret_cast<const float*>(ws + p.agg_off[l]);
+  A.slot_stride = HH;
+  A.batch_stride = p.n[l] * HH;
+  A.head_vec = A.base;
+  A.head_bstride = p.n[l] * HH;
+  return A;
+}
+
+float* level_out(const Plan& p, char* ws, int l) { return reinterpret_cast<float*>(ws + p.out_off[l]); }
+float* level_agg(const Plan& p, char* ws, int l) { return reinterpret_cast<float*>(ws + p.agg_off[l]); }
+
+// Up-sweep: levels 0 .. L-1 fold into levels 1 .. L.  `top_out` (nullable)
+// replaces the storage of level L (used by shard_up to write the aggregate
+// straight into the caller's buffer).
+bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan& p, char* ws, float* top_out,
+                    cudaStream_t st, Tracer& tr) {
+  const int H = j.H, B = j.B;
+  for (int l = 0; l < p.L; ++l) {
+    float* dst = (l + 1 == p.L && top_out) ? top_out : level_agg(p, ws, l + 1);
+    cudaError_t e;
+    tr.begin(st);
+    if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
+      e = launch_leaf_up(leaf_args(j, head, seed), p.C[0], dst, p.n[1], st);
+    } else {
+      const MatAcc A = (l == 0) ? dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed)
+                                : level_acc(p, ws, l, H);
+      e = launch_fold_up(A, H, B, p.n[l], p.C[l], head, dst, p.n[l + 1], st);
+    }
+    tr.end(st);
+    if (e != cudaSuccess) return cuda_status(e, "up-sweep launch");
+  }
+  return BPPSA_OK;
+}
+
+// Down-sweep from level `ltop` (whose single block's carry is `carry_top`, or
+// the symbolic identity for a head segment) to the leaves.
+bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Plan& p, char* ws, int ltop,
+                      long long ltop_C, const float* carry_top, float* grad_h, float* grad_init,
+                      cudaStream_t st, Tracer& tr) {
+  const int H = j.H, B = j.B;
+  const Seg seg{j.T, j.B, j.H, head};
+  for (int l = ltop; l >= 0; --l) {
+    const float* carry = (l == ltop) ? carry_top : level_out(p, ws, l + 1);
+    const long long nblk = (l == ltop) ? 1 : p.n[l + 1];
+    const int Cl = (l == ltop) ? (int)ltop_C : p.C[l];
+    cudaError_t e;
+    tr.begin(st);
+    if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
+      e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st);
+    } else if (l == 0) {
+      const MatAcc A = dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed);
+      e = launch_walk_down(A, H, B, p.n[0], Cl, head, carry, nblk, grad_h, 1, seg, grad_init, st);
+    } else {
+      e = launch_walk_down(level_acc(p, ws, l, H), H, B, p.n[l], Cl, head, carry, nblk, level_out(p, ws, l), 0,
+                           seg, nullptr, st);
+    }
+    tr.end(st);
+    if (e != cudaSuccess) return cuda_status(e, "down-sweep launch");
+  }
+  return BPPSA_OK;
+}
+
+bppsa_status check_ws(const Plan& p, void* ws, size_t ws_bytes) {
+  if (ws_bytes < p.total) return fail(BPPSA_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+  if (p.total > 0) {
+    if (!ws) return fail(BPPSA_ERR_WORKSPACE, "workspace is NULL");
+    if (reinterpret_cast<uintptr_t>(ws) % kAlign) return fail(BPPSA_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+    if (!is_device_ptr(ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace must be device memory");
+  }
+  return BPPSA_OK;
+}
+
+bppsa_status prepare_dense(const bppsa_jac& j, const Plan& p, char* ws, cudaStream_t st, Tracer& tr) {
+  if (!p.has_dense) return BPPSA_OK;
+  tr.begin(st);
+  cudaError_t e = launch_transpose_dense(j.JT, reinterpret_cast<float*>(ws + p.dense_off), (long long)j.T * j.B,
+                                         j.H, st);
+  tr.end(st);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "dense transpose launch");
+}
+
+}  // namespace
+}  // namespace bppsa
+
+using namespace bppsa;
+
+extern "C" {
+
+const char* bppsa_status_str(bppsa_status s) {
+  switch (s) {
+    case BPPSA_OK: return "BPPSA_OK";
+    case BPPSA_ERR_INVALID_ARGUMENT: return "BPPSA_ERR_INVALID_ARGUMENT";
+    case BPPSA_ERR_SHAPE: return "BPPSA_ERR_SHAPE";
+    case BPPSA_ERR_PLAN: return "BPPSA_ERR_PLAN";
+    case BPPSA_ERR_WORKSPACE: return "BPPSA_ERR_WORKSPACE";
+    case BPPSA_ERR_CUDA: return "BPPSA_ERR_CUDA";
+    case BPPSA_ERR_NCCL: return "BPPSA_ERR_NCCL";
+    case BPPSA_ERR_NOT_SUPPORTED: return "BPPSA_ERR_NOT_SUPPORTED";
+  }
+  return "BPPSA_UNKNOWN_STATUS";
+}
+
+const char* bppsa_last_error(void) { return g_last_error.c_str(); }
+
+int bppsa_version(void) { return 100; }
+
+bppsa_status bppsa_jacobians_rnn(int T, int B, int H, const float* h, const float* W_hh, float* JT_out,
+                                 bppsa_jac* desc, void* stream) {
+  if (!desc) return fail(BPPSA_ERR_INVALID_ARGUMENT, "desc is NULL");
+  bppsa_jac j{};
+  j.kind = BPPSA_JAC_RNN_TANH;
+  j.T = T; j.B = B; j.H = H; j.h = h; j.W_hh = W_hh;
+  bppsa_status s = check_jac(&j);
+  if (s != BPPSA_OK) return s;
+  if (JT_out) {
+    REQUIRE_DEV(JT_out, "JT_out");
+    cudaError_t e = launch_materialize_rnn(h, W_hh, JT_out, T, B, H, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "materialize rnn");
+    bppsa_jac d{};
+    d.kind = BPPSA_JAC_DENSE;
+    d.T = T; d.B = B; d.H = H; d.JT = JT_out;
+    *desc = d;
+    return BPPSA_OK;
+  }
+  *desc = j;
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_jacobians_gru(int T, int B, int H, const float* h_prev, const float* r, const float* z,
+                                 const float* n, const float* M, const float* W_hh3, float* JT_out,
+                                 bppsa_jac* desc, void* stream) {
+  if (!desc) return fail(BPPSA_ERR_INVALID_ARGUMENT, "desc is NULL");
+  bppsa_jac j{};
+  j.kind = BPPSA_JAC_GRU;
+  j.T = T; j.B = B; j.H = H;
+  j.h_prev = h_prev; j.r = r; j.z = z; j.n = n; j.M = M; j.W_hh3 = W_hh3;
+  if (JT_out) {
+    bppsa_jac chk = j;
+    chk.H = std::min(H, 32);           // pointer/shape checks; H limit only for the fused path
+    if (H < 1 || H > BPPSA_MAX_H) return fail(BPPSA_ERR_INVALID_ARGUMENT, "H must be in [1, 64]");
+    bppsa_status s = check_jac(&chk);
+    if (s != BPPSA_OK) return s;
+    REQUIRE_DEV(JT_out, "JT_out");
+    cudaError_t e = launch_materialize_gru(h_prev, r, z, n, M, W_hh3, JT_out, T, B, H, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "materialize gru");
+    bppsa_jac d{};
+    d.kind = BPPSA_JAC_DENSE;
+    d.T = T; d.B = B; d.H = H; d.JT = JT_out;
+    *desc = d;
+    return BPPSA_OK;
+  }
+  bppsa_status s = check_jac(&j);
+  if (s != BPPSA_OK) return s;
+  *desc = j;
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_scan_workspace_size(const bppsa_jac* jac, const bppsa_scan_opts* opts, size_t* bytes) {
+  if (!bytes) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  bppsa_status s = check_jac(jac, false);
+  if (s != BPPSA_OK) return s;
+  Plan p1, p2;
+  s = make_plan(*jac, 1, opts, false, &p1);
+  if (s != BPPSA_OK) return s;
+  // also large enough for shard use (head or not, aggregates to one)
+  int mode = opts ? opts->mode : BPPSA_SCAN_BLOCKED;
+  if (mode == BPPSA_SCAN_BLOCKED) {
+    s = make_plan(*jac, 0, opts, true, &p2);
+    if (s != BPPSA_OK) return s;
+    Plan p3;
+    s = make_plan(*jac, 1, opts, true, &p3);
+    if (s != BPPSA_OK) return s;
+    *bytes = std::max(p1.total, std::max(p2.total, p3.total));
+  } else {
+    *bytes = p1.total;
+  }
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h, float* grad_h_init, void* ws,
+                        size_t ws_bytes, const bppsa_scan_opts* opts, void* stream) {
+  bppsa_status s = check_jac(jac);
+  if (s != BPPSA_OK) return s;
+  REQUIRE_DEV(seed, "seed");
+  REQUIRE_DEV(grad_h, "grad_h");
+  if (grad_h_init) REQUIRE_DEV(grad_h_init, "grad_h_init");
+  const bppsa_jac& j = *jac;
+  Plan p;
+  s = make_plan(j, 1, opts, false, &p);
+  if (s != BPPSA_OK) return s;
+  s = check_ws(p, ws, ws_bytes);
+  if (s != BPPSA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  const int mode = opts ? opts->mode : BPPSA_SCAN_BLOCKED;
+  Tracer tr = tracer_from(opts);
+  if (mode == BPPSA_SCAN_ALG1) {
+    float* X = reinterpret_cast<float*>(w + p.dense_off);
+    const long long n = j.T;
+    const int L = (int)(64 - __builtin_clzll((unsigned long long)n));   // ceil(log2(n+1))
+    tr.begin(st);
+    cudaError_t e = launch_alg1_init(j.JT, seed, X, j.T, j.B, j.H, st);
+    tr.end(st);
+    if (e != cudaSuccess) return cuda_status(e, "alg1 init");
+    for (int d = 0; d <= L - 2; ++d) {
+      tr.begin(st);
+      e = launch_alg1_up(X, j.B, j.H, n, d, st);
+      tr.end(st);
+      if (e != cudaSuccess) return cuda_status(e, "alg1 up-sweep level");
+    }
+    for (int d = L - 1; d >= 0; --d) {   // a[n] <- I is symbolic (pair i = 0 rule)
+      tr.begin(st);
+      e = launch_alg1_down(X, j.B, j.H, n, d, st);
+      tr.end(st);
+      if (e != cudaSuccess) return cuda_status(e, "alg1 down-sweep level");
+    }
+    tr.begin(st);
+    e = launch_alg1_extract(X, j.JT, grad_h, grad_h_init, j.T, j.B, j.H, st);
+    tr.end(st);
+    if (e != cudaSuccess) return cuda_status(e, "alg1 extract");
+    report_launches(opts, tr);
+    return BPPSA_OK;
+  }
+  s = prepare_dense(j, p, w, st, tr);
+  if (s != BPPSA_OK) return s;
+  s = run_up(j, 1, seed, p, w, nullptr, st, tr);
+  if (s != BPPSA_OK) return s;
+  // top level: one block walked from the symbolic identity (head segment)
+  s = run_down(j, 1, seed, p, w, p.L, p.n[p.L], nullptr, grad_h, grad_h_init, st, tr);
+  report_launches(opts, tr);
+  return s;
+}
+
+bppsa_status bppsa_scan_shard_up(const bppsa_jac* jac, const float* seed, float* aggregate, void* ws,
+                                 size_t ws_bytes, const bppsa_scan_opts* opts, void* stream) {
+  bppsa_status s = check_jac(jac);
+  if (s != BPPSA_OK) return s;
+  REQUIRE_DEV(aggregate, "aggregate");
+  const int head = seed ? 1 : 0;
+  if (seed) REQUIRE_DEV(seed, "seed");
+  if (opts && opts->mode != BPPSA_SCAN_BLOCKED) return fail(BPPSA_ERR_NOT_SUPPORTED, "shards use the BLOCKED mode");
+  Plan p;
+  s = make_plan(*jac, head, opts, true, &p);
+  if (s != BPPSA_OK) return s;
+  s = check_ws(p, ws, ws_bytes);
+  if (s != BPPSA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  Tracer tr = tracer_from(opts);
+  s = prepare_dense(*jac, p, w, st, tr);
+  if (s != BPPSA_OK) return s;
+  if (p.L == 0) return fail(BPPSA_ERR_INVALID_ARGUMENT, "internal: empty shard plan");
+  // the top level (one aggregate per sample) goes straight into `aggregate`
+  s = run_up(*jac, head, seed, p, w, aggregate, st, tr);
+  report_launches(opts, tr);
+  return s;
+}
+
+bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed, const float* gathered, int rank,
+                                   int world, float* grad_h, float* grad_h_init, void* ws, size_t ws_bytes,
+                                   const bppsa_scan_opts* opts, void* stream) {
+  bppsa_status s = check_jac(jac);
+  if (s != BPPSA_OK) return s;
+  if (world < 1 || rank < 0 || rank >= world) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad rank/world");
+  const int head = (rank == world - 1) ? 1 : 0;
+  if (head && !seed) return fail(BPPSA_ERR_INVALID_ARGUMENT, "the last rank (holding t = T-1) needs the seed");
+  if (!head && seed) return fail(BPPSA_ERR_INVALID_ARGUMENT, "only the last rank passes the seed");
+  if (seed) REQUIRE_DEV(seed, "seed");
+  if (!head) REQUIRE_DEV(gathered, "gathered");
+  REQUIRE_DEV(grad_h, "grad_h");
+  if (grad_h_init) REQUIRE_DEV(grad_h_init, "grad_h_init");
+  if (opts && opts->mode != BPPSA_SCAN_BLOCKED) return fail(BPPSA_ERR_NOT_SUPPORTED, "shards use the BLOCKED mode");
+  Plan p;
+  s = make_plan(*jac, head, opts, true, &p);
+  if (s != BPPSA_OK) return s;
+  s = check_ws(p, ws, ws_bytes);
+  if (s != BPPSA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  float* carry = reinterpret_cast<float*>(w + p.carry_off);
+  Tracer tr = tracer_from(opts);
+  if (!head) {
+    tr.begin(st);
+    cudaError_t e = launch_carry_combine(gathered, rank, world, jac->B, jac->H, carry, st);
+    tr.end(st);
+    if (e != cudaSuccess) return cuda_status(e, "carry combine");
+  }
+  // level L holds one slot; level L-1 is one block walked from the carry
+  s = run_down(*jac, head, seed, p, w, p.L - 1, p.C[p.L - 1], head ? nullptr : carry, grad_h, grad_h_init, st, tr);
+  report_launches(opts, tr);
+  return s;
+}
+
+static long long wgrad_parts(long long rows) {
+  long long p = (rows + 1023) / 1024;
+  return std::max(1ll, std::min(p, 1184ll));
+}
+
+bppsa_status bppsa_weight_grads_workspace_size(int T, int B, int H, int I, size_t* bytes) {
+  if (!bytes) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  if (T < 1 || B < 1 || H < 1 || H > BPPSA_MAX_H || I < 0) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad shape");
+  const long long P = wgrad_parts((long long)T * B);
+  *bytes = align_up((size_t)P * 4 * H * (H + I + 1) * sizeof(float));   // GRU needs NA = 4H
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_weight_grads_rnn(int T, int B, int H, int I, const float* x, const float* h,
+                                    const float* h_init, const float* grad_h, float* dW_ih, float* dW_hh, float* db,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  size_t need;
+  bppsa_status s = bppsa_weight_grads_workspace_size(T, B, H, I, &need);
+  if (s != BPPSA_OK) return s;
+  if (I > 0) {
+    REQUIRE_DEV(x, "x");
+    REQUIRE_DEV(dW_ih, "dW_ih");
+  }
+  REQUIRE_DEV(h, "h");
+  REQUIRE_DEV(grad_h, "grad_h");
+  REQUIRE_DEV(dW_hh, "dW_hh");
+  REQUIRE_DEV(db, "db");
+  if (h_init) REQUIRE_DEV(h_init, "h_init");
+  if (ws_bytes < need || !is_device_ptr(ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace too small or not device memory");
+  const long long P = wgrad_parts((long long)T * B);
+  cudaError_t e = launch_wgrad_rnn(T, B, H, I, x, h, h_init, grad_h, dW_ih, dW_hh, db, static_cast<float*>(ws), P,
+                                   (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "weight grads rnn");
+}
+
+bppsa_status bppsa_weight_grads_gru(int T, int B, int H, int I, const float* x, const float* h_prev,
+                                    const float* r, const float* z, const float* n, const float* M,
+                                    const float* grad_h, float* dW_ih3, float* dW_hh3, float* db_ih3,
+                                    float* db_hh3, void* ws, size_t ws_bytes, void* stream) {
+  size_t need;
+  bppsa_status s = bppsa_weight_grads_workspace_size(T, B, H, I, &need);
+  if (s != BPPSA_OK) return s;
+  if (I > 0) {
+    REQUIRE_DEV(x, "x");
+    REQUIRE_DEV(dW_ih3, "dW_ih3");
+  }
+  REQUIRE_DEV(h_prev, "h_prev");
+  REQUIRE_DEV(r, "r");
+  REQUIRE_DEV(z, "z");
+  REQUIRE_DEV(n, "n");
+  REQUIRE_DEV(M, "M");
+  REQUIRE_DEV(grad_h, "grad_h");
+  REQUIRE_DEV(dW_hh3, "dW_hh3");
+  REQUIRE_DEV(db_ih3, "db_ih3");
+  REQUIRE_DEV(db_hh3, "db_hh3");
+  if (ws_bytes < need || !is_device_ptr(ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace too small or not device memory");
+  const long long P = wgrad_parts((long long)T * B);
+  cudaError_t e = launch_wgrad_gru(T, B, H, I, x, h_prev, r, z, n, M, grad_h, dW_ih3, dW_hh3, db_ih3, db_hh3,
+                                   static_cast<float*>(ws), P, (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "weight grads gru");
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// common.cuh — shared device/host definitions of libbppsa (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/bppsa.h"
+
+namespace bppsa {
+
+// ---------------------------------------------------------------------------
+// Error plumbing (thread-local detail string, status codes; no exceptions
+// cross the C-ABI).
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+bppsa_status fail(bppsa_status s, const std::string& msg);
+bppsa_status cuda_status(cudaError_t e, const char* where);
+
+#define BPPSA_CHECK_LAUNCH(where)                                         \
+  do {                                                                    \
+    cudaError_t _e = cudaGetLastError();                                  \
+    if (_e != cudaSuccess) return ::bppsa::cuda_status(_e, where);        \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// A segment of the scan array (one sequence, or one contiguous time shard).
+// Slots in scan order: head segments have slot 0 = seed and slot s >= 1
+// holding J_{T-s}^T; non-head shards have slot s holding J_{T-1-s}^T.
+// The exclusive output at the slot holding J_t^T is grad_h[t] (DESIGN r.3).
+// ---------------------------------------------------------------------------
+struct Seg {
+  int T, B, H;
+  int head;
+  __host__ __device__ __forceinline__ long long S() const { return (long long)T + head; }
+  __host__ __device__ __forceinline__ int time_of(long long s) const {
+    return head ? (T - (int)s) : (T - 1 - (int)s);
+  }
+};
+
+// Explicit H x H matrices of one level, column-major (element (i,k) at k*H+i),
+// addressed by (sample b, slot s).  A head level keeps the vector of slot 0 at
+// head_vec + b*head_bstride.
+struct MatAcc {
+  const float* base;
+  long long slot_stride;
+  long long batch_stride;
+  const float* head_vec;
+  long long head_bstride;
+  __device__ __forceinline__ const float* mat(int b, long long s) const {
+    return base + s * slot_stride + (long long)b * batch_stride;
+  }
+  __device__ __forceinline__ const float* vec(int b) const {
+    return head_vec + (long long)b * head_bstride;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (defined in the .cu files).
+// ---------------------------------------------------------------------------
+struct LeafArgs {            // implicit leaves (RNN / GRU)
+  Seg seg;
+  int kind;                  // BPPSA_JAC_RNN_TANH or BPPSA_JAC_GRU
+  const float* h;            // RNN
+  const float* W;            // RNN W_hh [H][H] | GRU W_hh3 [3H][H]
+  const float *hp, *r, *z, *n, *M;   // GRU
+  const float* seed;         // head only
+};
+
+// level-0 fold: blocks of C slots -> agg_out [B][n_out][H*H] (column-major)
+cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out,
+                           cudaStream_t st);
+// level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable
+cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry,
+                             long long nblk, float* grad_h, float* grad_init,
+                             cudaStream_t st);
+
+// explicit level fold / walk
+cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, int head,
+                           float* agg_out, long long n_out, cudaStream_t st);
+// out_mode 0: out[b][s][H] (carry array with n slots); 1: grad_h via seg time map
+cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, int head,
+                             const float* carry_in, long long nblk, float* out,
+                             int out_mode, const Seg& seg, float* total_out,
+                             cudaStream_t st);
+
+// DENSE helpers
+cudaError_t launch_transpose_dense(const float* JT, float* JTc, long long mats, int H,
+                                   cudaStream_t st);
+cudaError_t launch_materialize_rnn(const float* h, const float* W, float* JT, int T, int B,
+                                   int H, cudaStream_t st);
+cudaError_t launch_materialize_gru(const float* hp, const float* r, const float* z,
+                                   const float* n, const float* M, const float* W3,
+                                   float* JT, int T, int B, int H, cudaStream_t st);
+
+// Alg. 1 literal levels over X [(n+1)][B][H*H]
+cudaError_t launch_alg1_init(const float* JT, const float* seed, float* X, int T, int B,
+                             int H, cudaStream_t st);
+cudaError_t launch_alg1_up(float* X, int B, int H, long long n, int d, cudaStream_t st);
+cudaError_t launch_alg1_down(float* X, int B, int H, long long n, int d, cudaStream_t st);
+cudaError_t launch_alg1_extract(const float* X, const float* JT, float* grad_h,
+                                float* grad_init, int T, int B, int H, cudaStream_t st);
+
+// shards: carry = M_{r+1} ... M_{G-2} V_{G-1}
+cudaError_t launch_carry_combine(const float* gathered, int rank, int world, int B, int H,
+                                 float* carry_out, cudaStream_t st);
+cudaError_t launch_copy_aggregate(const float* agg_top, int B, int H, int head,
+                                  float* out, cudaStream_t st);
+
+// weight gradients
+cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const float* h,
+                             const float* h_init, const float* grad_h, float* dW_ih,
+                             float* dW_hh, float* db, float* ws, long long nparts,
+                             cudaStream_t st);
+cudaError_t launch_wgrad_gru(int T, int B, int H, int I, const float* x, const float* hp,
+                             const float* r, const float* z, const float* n,
+                             const float* M, const float* grad_h, float* dW_ih3,
+                             float* dW_hh3, float* db_ih3, float* db_hh3, float* ws,
+                             long long nparts, cudaStream_t st);
+
+}  // namespace bppsa

@@ -1,0 +1,360 @@
+// leaf.cu — level 0 of the blocked Blelloch scan with the leaf transposed
+// Jacobians built on the fly (never written to HBM).
+//
+// Up-sweep of one block of slots [s0, s1) (Alg. 1 lines 1-5 in Blelloch's
+// p < n regime): the block aggregate a[s1-1] ... a[s0] is folded in scan
+// order, agg <- a[s] agg.  Column j of agg therefore evolves as the BP chain
+//     c_j <- J_t^T c_j,   c_j(start) = e_j        (matrix blocks)
+//     v   <- J_t^T v,     v(start)   = seed       (the head block, a vector)
+// and every step of every chain multiplies by the SAME W_hh^T (the leaf is
+// J_t^T = W_hh^T diag(1-h_t^2), eqn:rnn P:315; GRU: eqn:gru_jcb P:836-857):
+//     (J_t^T c)_i = sum_k W[k][i] d_k c_k          (RNN)
+// A warp owns NC chains of one block; lane l owns rows i = l + 32m and keeps
+// W[:, i] in registers; the scaled vector x = d o c is exchanged through
+// shared memory (broadcast reads), one __syncwarp per step.
+//
+// Down-sweep of a block (Alg. 1 lines 7-13 with the operand reversal of line
+// 13): from the block's exclusive prefix (carry) v, out[s] = v,
+// v <- a[s] v = J_t^T v — a GEMV chain; out at the slot of J_t^T is grad_h[t].
+#include "common.cuh"
+
+namespace bppsa {
+namespace {
+
+template <int CELL>
+struct NX { static constexpr int v = (CELL == BPPSA_JAC_GRU) ? 3 : 1; };
+
+// Per-row step coefficients of J_t^T at (t, b, row i).
+//  RNN: c0 = 1 - h^2
+//  GRU: c0 = r(1-r) M (1-n^2)(1-z)  (multiplies W_hr^T)
+//       c1 = r (1-n^2)(1-z)          (multiplies W_hn^T)
+//       c2 = z(1-z)(h_prev - n)      (multiplies W_hz^T)
+//       c3 = z                       (diagonal J11)
+template <int CELL>
+struct Coef {
+  float c[4];
+};
+
+template <int CELL>
+__device__ __forceinline__ Coef<CELL> load_coef(const LeafArgs& a, long long off, bool valid) {
+  Coef<CELL> k;
+  k.c[0] = k.c[1] = k.c[2] = k.c[3] = 0.f;
+  if (!valid) return k;
+  if (CELL == BPPSA_JAC_RNN_TANH) {
+    float hv = __ldg(a.h + off);
+    k.c[0] = 1.f - hv * hv;
+  } else {
+    float r = __ldg(a.r + off), z = __ldg(a.z + off), n = __ldg(a.n + off);
+    float M = __ldg(a.M + off), hp = __ldg(a.hp + off);
+    float omn2 = 1.f - n * n, omz = 1.f - z;
+    k.c[0] = r * (1.f - r) * M * omn2 * omz;
+    k.c[1] = r * omn2 * omz;
+    k.c[2] = z * (1.f - z) * (hp - n);
+    k.c[3] = z;
+  }
+  return k;
+}
+
+// W[v][k] for row i: RNN W[k][i]; GRU v=0: W_hr[k][i], v=1: W_hn[k][i], v=2: W_hz[k][i]
+template <int CELL, int HT, int NR>
+__device__ __forceinline__ void load_w(const LeafArgs& a, int H, int lane,
+                                       float (&w)[NX<CELL>::v][NR][HT]) {
+#pragma unroll
+  for (int m = 0; m < NR; ++m) {
+    const int i = lane + 32 * m;
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+      const bool ok = (i < H) && (k < H);
+      if (CELL == BPPSA_JAC_RNN_TANH) {
+        w[0][m][k] = ok ? __ldg(a.W + (long long)k * H + i) : 0.f;
+      } else {
+        w[0][m][k] = ok ? __ldg(a.W + (long long)(0 * H + k) * H + i) : 0.f;  // W_hr
+        w[1][m][k] = ok ? __ldg(a.W + (long long)(2 * H + k) * H + i) : 0.f;  // W_hn
+        w[2][m][k] = ok ? __ldg(a.W + (long long)(1 * H + k) * H + i) : 0.f;  // W_hz
+      }
+    }
+  }
+}
+
+// acc_m = sum_v sum_k w[v][m][k] * xs[v*HT + k]   (xs broadcast, 16-byte reads)
+template <int CELL, int HT, int NR, int NP>
+__device__ __forceinline__ void matvec(const float (&w)[NX<CELL>::v][NR][HT],
+                                       const float* __restrict__ xs, float (&acc)[NR]) {
+  float part[NR][NP];
+#pragma unroll
+  for (int m = 0; m < NR; ++m)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) part[m][p] = 0.f;
+#pragma unroll
+  for (int v = 0; v < NX<CELL>::v; ++v) {
+#pragma unroll
+    for (int k4 = 0; k4 < HT / 4; ++k4) {
+      const float4 x4 = *reinterpret_cast<const float4*>(xs + v * HT + 4 * k4);
+      const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * k4 + kk;
+#pragma unroll
+        for (int m = 0; m < NR; ++m) part[m][k % NP] = fmaf(w[v][m][k], xv[kk], part[m][k % NP]);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < NR; ++m) {
+    float s = part[m][0];
+#pragma unroll
+    for (int p = 1; p < NP; ++p) s += part[m][p];
+    acc[m] = s;
+  }
+}
+
+template <int CELL, int HT, int NC>
+__global__ void __launch_bounds__(128) leaf_up_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                      long long n_out) {
+  constexpr int NR = (HT + 31) / 32;
+  constexpr int NV = NX<CELL>::v;
+  constexpr int XW = NC * NV * HT;       // floats per x buffer
+  extern __shared__ __align__(16) float smem[];
+  const int H = a.seg.H, B = a.seg.B;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* xs = smem + wib * 2 * XW;
+  const int G = (H + NC - 1) / NC;
+  const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (task >= (long long)B * n_out * G) return;
+  const int cg = (int)(task % G);
+  const long long rest = task / G;
+  const long long q = rest % n_out;
+  const int b = (int)(rest / n_out);
+  const long long S = a.seg.S();
+  const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+  const bool vec = a.seg.head && q == 0;
+  if (vec && cg > 0) return;
+  const int nc = vec ? 1 : min(NC, H - cg * NC);
+
+  float w[NV][NR][HT];
+  load_w<CELL, HT, NR>(a, H, lane, w);
+
+  float c[NC][NR];
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      if (vec)
+        c[j][m] = (j == 0 && i < H) ? __ldg(a.seed + (long long)b * H + i) : 0.f;
+      else
+        c[j][m] = (i == cg * NC + j) ? 1.f : 0.f;
+    }
+
+  long long s = vec ? 1 : s0;
+  const long long rowB = (long long)B * H;
+  Coef<CELL> nxt[NR];
+  if (s < s1) {
+    const long long t = a.seg.time_of(s);
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      nxt[m] = load_coef<CELL>(a, t * rowB + (long long)b * H + i, i < H);
+    }
+  }
+  int buf = 0;
+  for (; s < s1; ++s) {
+    Coef<CELL> cur[NR];
+#pragma unroll
+    for (int m = 0; m < NR; ++m) cur[m] = nxt[m];
+    if (s + 1 < s1) {                           // prefetch the next slot's coefficients
+      const long long t = a.seg.time_of(s + 1);
+#pragma unroll
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        nxt[m] = load_coef<CELL>(a, t * rowB + (long long)b * H + i, i < H);
+      }
+    }
+    float* xb = xs + buf * XW;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (j < nc) {
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+          const int i = lane + 32 * m;
+          if (i < HT) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) xb[(j * NV + v) * HT + i] = cur[m].c[v] * c[j][m];
+          }
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (j < nc) {
+        float acc[NR];
+        matvec<CELL, HT, NR, 1>(w, xb + j * NV * HT, acc);
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+          if (CELL == BPPSA_JAC_GRU) acc[m] = fmaf(cur[m].c[3], c[j][m], acc[m]);
+          c[j][m] = acc[m];
+        }
+      }
+    }
+    buf ^= 1;
+  }
+
+  float* dst = agg_out + ((long long)b * n_out + q) * H * H;
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    if (j < nc) {
+      const int col = vec ? 0 : cg * NC + j;
+#pragma unroll
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H) dst[(long long)col * H + i] = c[j][m];
+      }
+    }
+  }
+}
+
+template <int CELL, int HT>
+__global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const float* __restrict__ carry,
+                                                        long long nblk, float* __restrict__ grad_h,
+                                                        float* __restrict__ grad_init) {
+  constexpr int NR = (HT + 31) / 32;
+  constexpr int NV = NX<CELL>::v;
+  constexpr int XW = NV * HT;
+  extern __shared__ __align__(16) float smem[];
+  const int H = a.seg.H, B = a.seg.B;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float* xs = smem + wib * 2 * XW;
+  const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (task >= (long long)B * nblk) return;
+  const long long q = task % nblk;
+  const int b = (int)(task / nblk);
+  const long long S = a.seg.S();
+  const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+  const bool vec = a.seg.head && q == 0;
+
+  float w[NV][NR][HT];
+  load_w<CELL, HT, NR>(a, H, lane, w);
+
+  float v[NR];
+#pragma unroll
+  for (int m = 0; m < NR; ++m) {
+    const int i = lane + 32 * m;
+    v[m] = 0.f;
+    if (i < H) v[m] = vec ? __ldg(a.seed + (long long)b * H + i) : __ldg(carry + (q + (long long)b * nblk) * H + i);
+  }
+  const long long rowB = (long long)B * H;
+  long long s = vec ? 1 : s0;
+  Coef<CELL> nxt[NR];
+  if (s < s1) {
+    const long long t = a.seg.time_of(s);
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      nxt[m] = load_coef<CELL>(a, t * rowB + (long long)b * H + i, i < H);
+    }
+  }
+  int buf = 0;
+  for (; s < s1; ++s) {
+    const long long t = a.seg.time_of(s);
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      if (i < H) grad_h[t * rowB + (long long)b * H + i] = v[m];
+    }
+    const bool last = (s + 1 == s1);
+    const bool total = last && s1 == S && grad_init != nullptr;
+    if (last && !total) break;
+    Coef<CELL> cur[NR];
+#pragma unroll
+    for (int m = 0; m < NR; ++m) cur[m] = nxt[m];
+    if (!last) {
+      const long long tn = a.seg.time_of(s + 1);
+#pragma unroll
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        nxt[m] = load_coef<CELL>(a, tn * rowB + (long long)b * H + i, i < H);
+      }
+    }
+    float* xb = xs + buf * XW;
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      if (i < HT) {
+#pragma unroll
+        for (int vv = 0; vv < NV; ++vv) xb[vv * HT + i] = cur[m].c[vv] * v[m];
+      }
+    }
+    __syncwarp();
+    float acc[NR];
+    matvec<CELL, HT, NR, 4>(w, xb, acc);
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      if (CELL == BPPSA_JAC_GRU) acc[m] = fmaf(cur[m].c[3], v[m], acc[m]);
+      v[m] = acc[m];
+    }
+    buf ^= 1;
+    if (total) {
+#pragma unroll
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H) grad_init[(long long)b * H + i] = v[m];
+      }
+    }
+  }
+}
+
+constexpr int kWarpsPerCta = 4;
+
+template <int CELL, int HT, int NC>
+cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, cudaStream_t st) {
+  const int G = (a.seg.H + NC - 1) / NC;
+  const long long tasks = (long long)a.seg.B * n_out * G;
+  const long long grid = (tasks + kWarpsPerCta - 1) / kWarpsPerCta;
+  const size_t smem = (size_t)kWarpsPerCta * 2 * NC * NX<CELL>::v * HT * sizeof(float);
+  auto k = leaf_up_kernel<CELL, HT, NC>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(a, C, agg_out, n_out);
+  return cudaGetLastError();
+}
+
+template <int CELL, int HT>
+cudaError_t down_impl(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
+                      float* grad_init, cudaStream_t st) {
+  const long long tasks = (long long)a.seg.B * nblk;
+  const long long grid = (tasks + kWarpsPerCta - 1) / kWarpsPerCta;
+  const size_t smem = (size_t)kWarpsPerCta * 2 * NX<CELL>::v * HT * sizeof(float);
+  leaf_down_kernel<CELL, HT><<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(a, C, carry, nblk,
+                                                                           grad_h, grad_init);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, cudaStream_t st) {
+  const int H = a.seg.H;
+  if (a.kind == BPPSA_JAC_RNN_TANH) {
+    if (H == 20) return up_impl<BPPSA_JAC_RNN_TANH, 20, 20>(a, C, agg_out, n_out, st);
+    if (H <= 32) return up_impl<BPPSA_JAC_RNN_TANH, 32, 16>(a, C, agg_out, n_out, st);
+    return up_impl<BPPSA_JAC_RNN_TANH, 64, 8>(a, C, agg_out, n_out, st);
+  }
+  if (H == 20) return up_impl<BPPSA_JAC_GRU, 20, 10>(a, C, agg_out, n_out, st);
+  return up_impl<BPPSA_JAC_GRU, 32, 8>(a, C, agg_out, n_out, st);
+}
+
+cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk,
+                             float* grad_h, float* grad_init, cudaStream_t st) {
+  const int H = a.seg.H;
+  if (a.kind == BPPSA_JAC_RNN_TANH) {
+    if (H == 20) return down_impl<BPPSA_JAC_RNN_TANH, 20>(a, C, carry, nblk, grad_h, grad_init, st);
+    if (H <= 32) return down_impl<BPPSA_JAC_RNN_TANH, 32>(a, C, carry, nblk, grad_h, grad_init, st);
+    return down_impl<BPPSA_JAC_RNN_TANH, 64>(a, C, carry, nblk, grad_h, grad_init, st);
+  }
+  if (H == 20) return down_impl<BPPSA_JAC_GRU, 20>(a, C, carry, nblk, grad_h, grad_init, st);
+  return down_impl<BPPSA_JAC_GRU, 32>(a, C, carry, nblk, grad_h, grad_init, st);
+}
+
+}  // namespace bppsa

@@ -1,0 +1,194 @@
+// wgrad.cu — parameter gradients (eqn:update_param) for tied
+// recurrent weights summed over time:  dW = sum_{t,b} delta_{t,b} u_{t,b}^T.
+//
+// One contraction over K = T*B rows: out[a][c] = sum_rows A_row[a] * B_row[c]
+//   RNN: A = delta = (1-h^2) o grad_h              (H)
+//        B = [h_{t-1} | x_t | 1]                     (H + I + 1)
+//   GRU: A = [dR | dZ | dN | dM]                     (4H)
+//        B = [h_{t-1} | x_t | 1]
+// Rows are split into a fixed number of parts (a function of K only), each
+// CTA accumulates a 64 x 128 output tile of one part in registers (4 x 8
+// per thread, operands staged through shared memory), partial tiles go to
+// the workspace and a second kernel sums the parts in a fixed order —
+// deterministic, no float atomics.
+#include "common.cuh"
+
+namespace bppsa {
+namespace {
+
+constexpr int TA = 64, TB = 128, RR = 32, NT = 256;
+
+struct WArgs {
+  int T, B, H, I, kind;
+  const float *x, *h, *h_init, *g;              // RNN (h) / both (x, g)
+  const float *hp, *r, *z, *n, *M;              // GRU
+  long long rows, rows_per_part;
+  int NA, NB;
+};
+
+__device__ __forceinline__ float valA(const WArgs& w, long long row, int a) {
+  if (a >= w.NA) return 0.f;
+  if (w.kind == BPPSA_JAC_RNN_TANH) {
+    const long long o = row * w.H + a;
+    const float hv = w.h[o];
+    return (1.f - hv * hv) * w.g[o];
+  }
+  const int gate = a / w.H, i = a % w.H;
+  const long long o = row * w.H + i;
+  const float g = w.g[o], z = w.z[o], n = w.n[o];
+  const float dN = g * (1.f - z) * (1.f - n * n);
+  if (gate == 2) return dN;
+  if (gate == 1) return g * (w.hp[o] - n) * z * (1.f - z);
+  const float r = w.r[o];
+  if (gate == 0) return dN * w.M[o] * r * (1.f - r);
+  return dN * r;
+}
+
+__device__ __forceinline__ float valB(const WArgs& w, long long row, int c) {
+  if (c < w.H) {
+    if (w.kind == BPPSA_JAC_GRU) return w.hp[row * w.H + c];
+    if (row >= w.B) return w.h[(row - w.B) * w.H + c];             // h_{t-1}
+    return w.h_init ? w.h_init[row * w.H + c] : 0.f;                 // t = 0: row = b
+  }
+  if (c < w.H + w.I) return w.x[row * w.I + (c - w.H)];
+  if (c == w.H + w.I) return 1.f;
+  return 0.f;
+}
+
+__global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __restrict__ ws) {
+  __shared__ __align__(16) float As[RR][TA];
+  __shared__ __align__(16) float Bs[RR][TB];
+  const int part = blockIdx.x, ta = blockIdx.y, tb = blockIdx.z;
+  const long long r0 = (long long)part * w.rows_per_part;
+  const long long r1 = min(r0 + w.rows_per_part, w.rows);
+  const int tid = threadIdx.x, ti = tid % 16, tj = tid / 16;
+  float acc[4][8];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y] = 0.f;
+  for (long long rb = r0; rb < r1; rb += RR) {
+    for (int e = tid; e < RR * TA; e += NT) {
+      const int rr = e / TA, col = e % TA;
+      const long long row = rb + rr;
+      As[rr][col] = (row < r1) ? valA(w, row, ta * TA + col) : 0.f;
+    }
+    for (int e = tid; e < RR * TB; e += NT) {
+      const int rr = e / TB, col = e % TB;
+      const long long row = rb + rr;
+      Bs[rr][col] = (row < r1) ? valB(w, row, tb * TB + col) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < RR; ++rr) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[rr][ti * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[rr][tj * 8]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[rr][tj * 8 + 4]);
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y] = fmaf(av[x], bv[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+  float* dst = ws + (long long)part * w.NA * w.NB;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int a = ta * TA + ti * 4 + x;
+    if (a >= w.NA) continue;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const int c = tb * TB + tj * 8 + y;
+      if (c < w.NB) dst[(long long)a * w.NB + c] = acc[x][y];
+    }
+  }
+}
+
+// Sum the parts in order p = 0..P-1 for the requested (a, c) element.
+__device__ __forceinline__ float sum_parts(const float* ws, long long P, int NA, int NB, int a, int c) {
+  float s = 0.f;
+  const long long stride = (long long)NA * NB;
+  const float* p = ws + (long long)a * NB + c;
+  for (long long q = 0; q < P; ++q) s += p[q * stride];
+  return s;
+}
+
+__global__ void wgrad_reduce_rnn(const float* __restrict__ ws, long long P, int H, int I, float* dW_ih,
+                                 float* dW_hh, float* db) {
+  const int NB = H + I + 1;
+  const int total = H * NB;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int a = e / NB, c = e % NB;
+    const float s = sum_parts(ws, P, H, NB, a, c);
+    if (c < H) dW_hh[a * H + c] = s;
+    else if (c < H + I) dW_ih[a * I + (c - H)] = s;
+    else db[a] = s;
+  }
+}
+
+__global__ void wgrad_reduce_gru(const float* __restrict__ ws, long long P, int H, int I, float* dW_ih3,
+                                 float* dW_hh3, float* db_ih3, float* db_hh3) {
+  const int NA = 4 * H, NB = H + I + 1;
+  // outputs: dW_hh3 3H*H, dW_ih3 3H*I, db_ih3 3H, db_hh3 3H
+  const int n_hh = 3 * H * H, n_ih = 3 * H * I, total = n_hh + n_ih + 6 * H;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    if (e < n_hh) {
+      const int row = e / H, k = e % H, g = row / H, i = row % H;
+      const int a = (g == 2 ? 3 : g) * H + i;           // [dR; dZ; dM] h_prev^T
+      dW_hh3[e] = sum_parts(ws, P, NA, NB, a, k);
+    } else if (e < n_hh + n_ih) {
+      const int f = e - n_hh, row = f / I, j = f % I;
+      dW_ih3[f] = sum_parts(ws, P, NA, NB, row, H + j);  // [dR; dZ; dN] x^T
+    } else if (e < n_hh + n_ih + 3 * H) {
+      const int row = e - n_hh - n_ih;
+      db_ih3[row] = sum_parts(ws, P, NA, NB, row, H + I);
+    } else {
+      const int row = e - n_hh - n_ih - 3 * H, g = row / H, i = row % H;
+      db_hh3[row] = sum_parts(ws, P, NA, NB, (g == 2 ? 3 : g) * H + i, H + I);
+    }
+  }
+}
+
+cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream_t st) {
+  dim3 grid((unsigned)nparts, (unsigned)((w.NA + TA - 1) / TA), (unsigned)((w.NB + TB - 1) / TB));
+  wgrad_partial_kernel<<<grid, NT, 0, st>>>(w, ws);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const float* h, const float* h_init,
+                             const float* grad_h, float* dW_ih, float* dW_hh, float* db, float* ws,
+                             long long nparts, cudaStream_t st) {
+  WArgs w{};
+  w.T = T; w.B = B; w.H = H; w.I = I; w.kind = BPPSA_JAC_RNN_TANH;
+  w.x = x; w.h = h; w.h_init = h_init; w.g = grad_h;
+  w.rows = (long long)T * B;
+  w.rows_per_part = (w.rows + nparts - 1) / nparts;
+  w.NA = H; w.NB = H + I + 1;
+  cudaError_t e = run_partials(w, ws, nparts, st);
+  if (e != cudaSuccess) return e;
+  wgrad_reduce_rnn<<<(H * w.NB + 255) / 256, 256, 0, st>>>(ws, nparts, H, I, dW_ih, dW_hh, db);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wgrad_gru(int T, int B, int H, int I, const float* x, const float* hp, const float* r,
+                             const float* z, const float* n, const float* M, const float* grad_h, float* dW_ih3,
+                             float* dW_hh3, float* db_ih3, float* db_hh3, float* ws, long long nparts,
+                             cudaStream_t st) {
+  WArgs w{};
+  w.T = T; w.B = B; w.H = H; w.I = I; w.kind = BPPSA_JAC_GRU;
+  w.x = x; w.g = grad_h; w.hp = hp; w.r = r; w.z = z; w.n = n; w.M = M;
+  w.rows = (long long)T * B;
+  w.rows_per_part = (w.rows + nparts - 1) / nparts;
+  w.NA = 4 * H; w.NB = H + I + 1;
+  cudaError_t e = run_partials(w, ws, nparts, st);
+  if (e != cudaSuccess) return e;
+  const int total = 3 * H * H + 3 * H * I + 6 * H;
+  wgrad_reduce_gru<<<(total + 255) / 256, 256, 0, st>>>(ws, nparts, H, I, dW_ih3, dW_hh3, db_ih3, db_hh3);
+  return cudaGetLastError();
+}
+
+}  // namespace bppsa

@@ -1,0 +1,76 @@
+"""Multi-GPU BPPSA: contiguous time shards, one exchange.
+
+Rank order = time order; rank r owns t in [lo_r, hi_r) and the last rank holds
+t = T-1 and the seed (the "head" shard, first in scan order).  Protocol:
+
+  1. local leaf + up-sweep to one aggregate per sample        (bppsa_scan_shard_up)
+       rank < G-1:  M_r = J_lo^T ... J_{hi-1}^T   [B, H*H] column-major
+       rank = G-1:  V   = grad_h[lo-1]            [B, H] in the first H floats
+  2. all-gather of the aggregates over NCCL (torch.distributed; NVLink on the
+     8xB200 box) — the only data-path collective
+  3. carry for rank r: M_{r+1} ... M_{G-2} V and the local down-sweep on the
+     device                                                     (bppsa_scan_shard_down)
+  4. (caller) all-reduce of the weight gradients.
+
+The protocol is written against a small backend interface so the host logic
+can be exercised with the gloo backend on CPU (tests/test_dist_gloo.py plugs in
+an oracle-backed backend); the product backend is `CudaShardBackend`.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(T: int, G: int):
+    """Contiguous shards in time order, remainder spread over the first ranks."""
+    if T < G:
+        raise ValueError("need at least one step per rank")
+    base, rem = divmod(T, G)
+    out, lo = [], 0
+    for r in range(G):
+        sz = base + (1 if r < rem else 0)
+        out.append((lo, lo + sz))
+        lo += sz
+    return out
+
+
+class CudaShardBackend:
+    """bppsa_scan_shard_up / _down on this rank's GPU (workspace kept between)."""
+
+    def __init__(self, jac, block0: int = 0, block: int = 0):
+        from . import api
+        self.api, self.jac, self.block0, self.block = api, jac, block0, block
+        self.ws = api.workspace(api.scan_workspace_size(jac, "blocked", block0, block))
+
+    def up(self, seed):
+        B, H = self.jac.B, self.jac.H
+        agg = torch.empty((B, H * H), dtype=torch.float32, device="cuda")
+        self.api.scan_shard_up(self.jac, seed, agg, self.ws, self.block0, self.block)
+        return agg
+
+    def down(self, seed, gathered, rank, world, grad_h=None, want_init=False):
+        T, B, H = self.jac.T, self.jac.B, self.jac.H
+        if grad_h is None:
+            grad_h = torch.empty((T, B, H), dtype=torch.float32, device="cuda")
+        gi = torch.empty((B, H), dtype=torch.float32, device="cuda") if want_init else None
+        self.api.scan_shard_down(self.jac, seed, gathered, rank, world, grad_h, gi, self.ws,
+                                 self.block0, self.block)
+        return grad_h, gi
+
+
+def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None):
+    """Run the 3-step protocol on this rank.  `seed` must be given on the last
+    rank only (it holds t = T-1).  Returns (local grad_h, J_lo^T grad_h[lo])."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    head = rank == world - 1
+    if head != (seed is not None):
+        raise ValueError("exactly the last rank passes the seed")
+    agg = backend.up(seed)
+    if world > 1:
+        gathered = torch.empty((world,) + tuple(agg.shape), dtype=agg.dtype, device=agg.device)
+        dist.all_gather_into_tensor(gathered, agg.contiguous(), group=group)
+    else:
+        gathered = agg.unsqueeze(0)
+    return backend.down(seed, None if head else gathered, rank, world, grad_h=grad_h, want_init=want_init)

@@ -1,0 +1,313 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the
+same seeded inputs.  Gates: bit-exact on the integer families, <= 1e-4
+relative error in max-norm (north_star; DESIGN reading 12) on random fp32."""
+import numpy as np
+import pytest
+import torch
+
+import bppsa_workloads as W
+from oracle import bp, scan as S
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def rel(got, ref):
+    got = got.detach().cpu().numpy().astype(np.float64) if torch.is_tensor(got) else got
+    den = np.abs(ref).max()
+    return float(np.abs(got - ref).max() / (den if den > 0 else 1.0))
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_rnn(api, h, Wm, g, **kw):
+    jac = api.jacobians_rnn(cu(h), cu(Wm))
+    grad, gi = api.scan(jac, cu(g), grad_h_init=True, **kw)
+    torch.cuda.synchronize()
+    return grad, gi
+
+
+# ------------------------------------------------------------------ RNN, fused leaves
+@pytest.mark.parametrize("T", [1, 2, 3, 15, 16, 17, 100, 255, 256, 257, 1000])
+@pytest.mark.parametrize("H", [20, 64])
+def test_rnn_realistic_T_sweep(lib, T, H):
+    w = W.rnn_workload(T, 4, H, seed=T * 3 + H)
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    grad, gi = run_rnn(lib, w.h, w.W_hh, w.g)
+    assert rel(grad, ref) <= TOL and rel(gi, ref_init) <= TOL
+    assert np.array_equal(grad[T - 1].cpu().numpy(), w.g)          # grad_h[T-1] = seed exactly
+
+
+@pytest.mark.parametrize("H", [1, 5, 20, 31, 32, 33, 48, 64])
+@pytest.mark.parametrize("blocks", [(0, 0), (2, 2), (3, 5), (7, 4)])
+def test_rnn_H_and_block_sweep(lib, H, blocks):
+    T, B = 300, 3
+    f = W.norm_preserving_rnn(T, B, H, seed=H)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    grad, gi = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1])
+    assert rel(grad, ref) <= TOL and rel(gi, ref_init) <= TOL
+
+
+def test_rnn_config1(lib):
+    """C1: tanh RNN, H = 20, B = 16, T = 1000."""
+    w = W.rnn_workload(1000, 16, 20, seed=0)
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    for mode in ("blocked", "linear"):
+        grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, mode=mode)
+        assert rel(grad, ref) <= TOL and rel(gi, ref_init) <= TOL, mode
+
+
+@pytest.mark.parametrize("T", [10000, 30000])
+def test_rnn_config2(lib, T):
+    """C2: T in {10000, 30000}."""
+    w = W.rnn_workload(T, 16, 20, seed=T)
+    ref, _ = bp.bp_rnn(w.h, w.W_hh, w.g)
+    grad, _ = run_rnn(lib, w.h, w.W_hh, w.g)
+    assert rel(grad, ref) <= TOL
+
+
+@pytest.mark.parametrize("H,T", [(20, 65536), (64, 65536), (64, 4096)])
+def test_rnn_norm_preserving(lib, H, T):
+    """Reading 12 (ii): the norm-preserving family keeps every grad_h O(seed)
+    over the whole sequence, so the global max-norm constrains every step."""
+    f = W.norm_preserving_rnn(T, 4, H, seed=7)
+    ref, _ = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    grad, _ = run_rnn(lib, f["h"], f["W_hh"], f["g"])
+    e = rel(grad, ref)
+    print(f"norm-preserving H={H} T={T}: rel={e:.3e}")
+    assert e <= TOL
+
+
+@pytest.mark.parametrize("mode,blocks", [("blocked", (0, 0)), ("blocked", (2, 3)), ("blocked", (5, 2)),
+                                         ("linear", (0, 0))])
+@pytest.mark.parametrize("H", [20, 64])
+def test_rnn_integer_family_bit_exact(lib, mode, blocks, H):
+    f = W.int_rnn_family(2000, 3, H, seed=H)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    grad, gi = run_rnn(lib, f["h"], f["W_hh"], f["g"], mode=mode, block0=blocks[0], block=blocks[1])
+    assert np.array_equal(grad.cpu().numpy(), ref)
+    assert np.array_equal(gi.cpu().numpy(), ref_init)
+
+
+def test_rnn_closed_forms(lib):
+    """P4: W = 0 -> grad_h[t<T-1] = 0 exactly; h = 0 with an integer W -> powers of W^T."""
+    T, B, H = 50, 2, 20
+    rng = np.random.default_rng(0)
+    g = rng.integers(-3, 4, (B, H)).astype(np.float32)
+    grad, _ = run_rnn(lib, rng.uniform(-1, 1, (T, B, H)).astype(np.float32), np.zeros((H, H), np.float32), g)
+    assert not grad[:-1].any() and np.array_equal(grad[-1].cpu().numpy(), g)
+    f = W.int_rnn_family(T, B, H, seed=1, p_sat=0.0)     # h = 0: grad_h[t] = (W^T)^{T-1-t} g
+    grad, _ = run_rnn(lib, f["h"], f["W_hh"], f["g"])
+    Wm = f["W_hh"].astype(np.float64)
+    for t in (0, 17, T - 1):
+        assert np.array_equal(grad[t].cpu().numpy(), f["g"] @ np.linalg.matrix_power(Wm, T - 1 - t))
+
+
+def test_deterministic(lib):
+    w = W.rnn_workload(5000, 16, 64, seed=2)
+    a, _ = run_rnn(lib, w.h, w.W_hh, w.g)
+    b, _ = run_rnn(lib, w.h, w.W_hh, w.g)
+    assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ DENSE leaves, Alg. 1
+@pytest.mark.parametrize("mode", ["alg1", "blocked", "linear"])
+@pytest.mark.parametrize("T,H", [(1, 20), (2, 20), (7, 20), (300, 20), (129, 64), (1000, 32)])
+def test_dense_integer_bit_exact(lib, mode, T, H):
+    f = W.int_dense_family(T, 3, H, seed=T + H)
+    ref, ref_init = bp.bp_dense(f["JT"], f["g"])
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    grad, gi = lib.scan(jac, cu(f["g"]), grad_h_init=True, mode=mode)
+    torch.cuda.synchronize()
+    assert np.array_equal(grad.cpu().numpy(), ref)
+    assert np.array_equal(gi.cpu().numpy(), ref_init)
+
+
+@pytest.mark.parametrize("mode", ["alg1", "blocked"])
+@pytest.mark.parametrize("T,H", [(513, 20), (1000, 64), (257, 7)])
+def test_dense_random_vs_oracle(lib, mode, T, H):
+    f = W.random_dense_family(T, 4, H, seed=3, gain=1.0)
+    ref, ref_init = bp.bp_dense(f["JT"], f["g"])
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    grad, gi = lib.scan(jac, cu(f["g"]), grad_h_init=True, mode=mode)
+    torch.cuda.synchronize()
+    assert rel(grad, ref) <= TOL and rel(gi, ref_init) <= TOL
+
+
+def test_alg1_matches_oracle_alg1_tightly(lib):
+    """ALG1 mode has the association of the oracle's literal Alg. 1."""
+    T, B, H = 200, 2, 20
+    f = W.random_dense_family(T, B, H, seed=4)
+    tree = S.grads_from_scan(S.blelloch(S.scan_array(f["g"], f["JT"])))
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    grad, _ = lib.scan(jac, cu(f["g"]), mode="alg1")
+    assert rel(grad, tree) <= 1e-5
+
+
+def test_materialized_rnn_leaves(lib):
+    T, B, H = 40, 3, 20
+    w = W.rnn_workload(T, B, H, seed=9)
+    JT = torch.empty((T, B, H, H), device="cuda")
+    jac = lib.jacobians_rnn(cu(w.h), cu(w.W_hh), JT_out=JT)
+    torch.cuda.synchronize()
+    ref = np.stack([bp.rnn_jt(w.h[t], w.W_hh) for t in range(T)])
+    assert rel(JT, ref) <= 1e-6
+    grad, _ = lib.scan(jac, cu(w.g))
+    assert rel(grad, bp.bp_rnn(w.h, w.W_hh, w.g)[0]) <= TOL
+
+
+# ------------------------------------------------------------------ GRU
+def gru_tensors(tape):
+    return [cu(tape[k]) for k in ("h_prev", "r", "z", "n", "M")]
+
+
+@pytest.mark.parametrize("set_name,B", [("S", 16), ("M", 32), ("L", 64), ("L", 16)])
+def test_gru_config3(lib, set_name, B):
+    """C3: GRU H = 20 on IRMAS-shaped synthetic sequences (Table 3)."""
+    gw = W.gru_workload(set_name, B, seed=B)
+    ref, ref_init = bp.bp_gru(gw.tape, gw.params["W_hh3"], gw.g)
+    jac = lib.jacobians_gru(*gru_tensors(gw.tape), cu(gw.params["W_hh3"]))
+    grad, gi = lib.scan(jac, cu(gw.g), grad_h_init=True)
+    torch.cuda.synchronize()
+    assert rel(grad, ref) <= TOL and rel(gi, ref_init) <= TOL
+
+
+@pytest.mark.parametrize("fam", ["zero", "int"])
+def test_gru_exact_families(lib, fam):
+    T, B, H = (100, 3, 20) if fam == "zero" else (1000, 3, 20)
+    f = (W.gru_zero_family if fam == "zero" else W.gru_int_family)(T, B, H, seed=5)
+    ref, ref_init = bp.bp_gru(f["tape"], f["W_hh3"], f["g"])
+    jac = lib.jacobians_gru(*gru_tensors(f["tape"]), cu(f["W_hh3"]))
+    for mode in ("blocked", "linear"):
+        grad, gi = lib.scan(jac, cu(f["g"]), grad_h_init=True, mode=mode)
+        torch.cuda.synchronize()
+        assert np.array_equal(grad.cpu().numpy(), ref), mode
+        assert np.array_equal(gi.cpu().numpy(), ref_init), mode
+
+
+def test_gru_materialized_large_H(lib):
+    """H > 32 GRU goes through materialised (DENSE) leaves."""
+    T, B, H, I = 120, 2, 48, 5
+    p = W.gru_params(H, I, seed=3)
+    x = np.random.default_rng(1).standard_normal((T, B, I)).astype(np.float32)
+    tape = W.gru_forward(x, p)
+    g = np.random.default_rng(2).standard_normal((B, H)).astype(np.float32)
+    ref, _ = bp.bp_gru(tape, p["W_hh3"], g)
+    JT = torch.empty((T, B, H, H), device="cuda")
+    jac = lib.jacobians_gru(*gru_tensors(tape), cu(p["W_hh3"]), JT_out=JT)
+    torch.cuda.synchronize()
+    JTref = np.stack([bp.gru_jt(*(tape[k][t] for k in ("h_prev", "r", "z", "n", "M")), p["W_hh3"])
+                      for t in range(T)])
+    assert rel(JT, JTref) <= 1e-6
+    grad, _ = lib.scan(jac, cu(g))
+    assert rel(grad, ref) <= TOL
+
+
+# ------------------------------------------------------------------ weight gradients
+@pytest.mark.parametrize("T,B,H", [(1000, 16, 20), (3000, 16, 64), (1, 1, 5)])
+def test_weight_grads_rnn(lib, T, B, H):
+    w = W.rnn_workload(T, B, H, seed=1)
+    ref, _ = bp.bp_rnn(w.h, w.W_hh, w.g)
+    rng = np.random.default_rng(0)
+    h_init = rng.uniform(-1, 1, (B, H)).astype(np.float32)
+    grad = cu(ref.astype(np.float32))
+    for hi in (None, h_init):
+        dWih, dWhh, db = lib.weight_grads_rnn(cu(w.x), cu(w.h), grad, h_init=None if hi is None else cu(hi))
+        torch.cuda.synchronize()
+        r = bp.weight_grads_rnn(w.x, w.h, ref.astype(np.float32), h_init=hi)
+        assert rel(dWih, r[0]) <= TOL and rel(dWhh, r[1]) <= TOL and rel(db, r[2]) <= TOL
+
+
+@pytest.mark.parametrize("set_name,B", [("S", 16), ("L", 64)])
+def test_weight_grads_gru(lib, set_name, B):
+    gw = W.gru_workload(set_name, B, seed=3)
+    ref, _ = bp.bp_gru(gw.tape, gw.params["W_hh3"], gw.g)
+    tape = {k: cu(v) for k, v in gw.tape.items()}
+    out = lib.weight_grads_gru(cu(gw.x), tape, cu(ref.astype(np.float32)))
+    torch.cuda.synchronize()
+    r = bp.weight_grads_gru(gw.x, gw.tape, ref.astype(np.float32))
+    for got, want in zip(out, r):
+        assert rel(got, want) <= TOL
+
+
+# ------------------------------------------------------------------ shards (loopback on one GPU)
+@pytest.mark.parametrize("kind", ["rnn", "dense", "gru"])
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_shard_loopback(lib, kind, G):
+    """The multi-GPU protocol with the all-gather replaced by a device stack:
+    per-shard up, gather, carry combine, per-shard down == the oracle."""
+    T, B = 1000, 4
+    if kind == "rnn":
+        f = W.norm_preserving_rnn(T, B, 64, seed=G)
+        ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+        mk = lambda lo, hi: lib.jacobians_rnn(cu(f["h"][lo:hi]), cu(f["W_hh"]))
+        H, g = 64, f["g"]
+    elif kind == "dense":
+        f = W.int_dense_family(T, B, 20, seed=G)
+        ref, ref_init = bp.bp_dense(f["JT"], f["g"])
+        mk = lambda lo, hi: lib.jacobians_dense(cu(f["JT"][lo:hi]))
+        H, g = 20, f["g"]
+    else:
+        gw = W.gru_workload("L", B, seed=G)
+        T = gw.tape["r"].shape[0]
+        ref, ref_init = bp.bp_gru(gw.tape, gw.params["W_hh3"], gw.g)
+        mk = lambda lo, hi: lib.jacobians_gru(*(cu(gw.tape[k][lo:hi]) for k in ("h_prev", "r", "z", "n", "M")),
+                                              cu(gw.params["W_hh3"]))
+        H, g = 20, gw.g
+    from paper_1907_10134_b200.dist import shard_bounds
+    bounds = shard_bounds(T, G)
+    jacs = [mk(lo, hi) for lo, hi in bounds]
+    wss = [lib.workspace(lib.scan_workspace_size(j)) for j in jacs]
+    aggs = []
+    for r, (j, ws) in enumerate(zip(jacs, wss)):
+        agg = torch.empty((B, H * H), device="cuda")
+        lib.scan_shard_up(j, cu(g) if r == G - 1 else None, agg, ws)
+        aggs.append(agg)
+    gathered = torch.stack(aggs)
+    outs, init = [], None
+    for r, ((lo, hi), j, ws) in enumerate(zip(bounds, jacs, wss)):
+        gh = torch.empty((hi - lo, B, H), device="cuda")
+        gi = torch.empty((B, H), device="cuda") if r == 0 else None
+        lib.scan_shard_down(j, cu(g) if r == G - 1 else None, None if r == G - 1 else gathered, r, G, gh, gi, ws)
+        outs.append(gh)
+        if r == 0:
+            init = gi
+    torch.cuda.synchronize()
+    got = torch.cat(outs)
+    if kind == "dense":
+        assert np.array_equal(got.cpu().numpy(), ref) and np.array_equal(init.cpu().numpy(), ref_init)
+    else:
+        assert rel(got, ref) <= TOL and rel(init, ref_init) <= TOL
+
+
+# ------------------------------------------------------------------ boundary behaviour
+def test_errors(lib):
+    h = torch.zeros((4, 2, 20), device="cuda")
+    Wm = torch.zeros((20, 20), device="cuda")
+    with pytest.raises(lib.BppsaError, match="INVALID_ARGUMENT"):
+        lib.jacobians_rnn(torch.zeros((0, 2, 20), device="cuda"), Wm)
+    with pytest.raises(lib.BppsaError, match="INVALID_ARGUMENT"):
+        lib.jacobians_rnn(torch.zeros((4, 2, 65), device="cuda"), torch.zeros((65, 65), device="cuda"))
+    jac = lib.jacobians_rnn(h, Wm)
+    with pytest.raises(lib.BppsaError, match="WORKSPACE"):
+        lib.scan(jac, torch.zeros((2, 20), device="cuda"), ws=torch.empty(16, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(lib.BppsaError, match="NOT_SUPPORTED"):
+        lib.scan(jac, torch.zeros((2, 20), device="cuda"), mode="alg1")
+    z = torch.zeros((4, 2, 40), device="cuda")
+    with pytest.raises(lib.BppsaError, match="NOT_SUPPORTED"):
+        lib.jacobians_gru(z, z, z, z, z, torch.zeros((120, 40), device="cuda"))
+    with pytest.raises(ValueError):
+        lib.jacobians_rnn(torch.zeros((4, 2, 20)), torch.zeros((20, 20)))      # host tensors
+
+
+@pytest.mark.slow
+def test_rnn_config4_full_size(lib):
+    """C4 at full size in bench.py's configuration: H = 64, B = 16, T = 2^20,
+    realistic family (torch-default init, bitstreams), every output compared."""
+    import bench
+    w = bench.c4_inputs(seed=0)
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=bench.C4_BLOCK0, block=bench.C4_BLOCK)
+    assert rel(grad, ref) <= TOL and rel(gi, ref_init) <= TOL
