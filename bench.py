@@ -345,12 +345,19 @@ def sequential_baselines(api, w, args):
     e1.record()
     torch.cuda.synchronize()
     lin = e0.elapsed_time(e1)
-    Ts = 1 << 16
-    cud = cudnn_backward_ms(Ts, B, H, 1, reps=2) * (T / Ts)
     del h, grad, ws
     torch.cuda.empty_cache()
-    return {"gpu_linear_scan_ms": round(lin, 3), "cudnn_backward_ms": round(cud, 3),
-            "cudnn_note": "torch 2.11 nn.RNN backward (cuDNN, TF32 off) at T=65536, x16 (linear in T)",
+    cud, note = None, "cuDNN rejected every tried T"
+    for Ts in (1 << 16, 1 << 15, 1 << 14, 1 << 13, 1 << 12):
+        try:
+            cud = cudnn_backward_ms(Ts, B, H, 1, reps=2) * (T / Ts)
+            note = f"torch nn.RNN backward (cuDNN, TF32 off) at T={Ts}, x{T // Ts} (linear in T)"
+            break
+        except RuntimeError as ex:  # cuDNN refuses very long sequences
+            note = f"T={Ts}: {str(ex)[:80]}"
+            torch.cuda.empty_cache()
+    return {"gpu_linear_scan_ms": round(lin, 3), "cudnn_backward_ms": None if cud is None else round(cud, 3),
+            "cudnn_note": note,
             "gpu_linear_note": "bppsa_scan mode=LINEAR: sequential BP, one warp per sample, scan only"}
 
 
@@ -509,7 +516,7 @@ def main():
         line["e2e"] = r["e2e"]
         sb = r["sequential_bp"]
         sb["speedup_vs_gpu_linear"] = round(sb["gpu_linear_scan_ms"] / r["ms"], 2)
-        sb["speedup_vs_cudnn"] = round(sb["cudnn_backward_ms"] / r["ms"], 2)
+        sb["speedup_vs_cudnn"] = None if sb["cudnn_backward_ms"] is None else round(sb["cudnn_backward_ms"] / r["ms"], 2)
         line["sequential_bp"] = sb
         line["sweep"] = r["sweep"]
         line["cpu_baseline"] = oracle_sample()

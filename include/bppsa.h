@@ -117,6 +117,8 @@ typedef struct bppsa_scan_opts {
   int mode;    /* bppsa_scan_mode                                              */
   int block0;  /* BLOCKED: leaf block length in slots (0 = default)            */
   int block;   /* BLOCKED: block length of the upper levels (0 = default)      */
+  int leaf_impl; /* level-0 fold engine: 0 = auto (tensor cores where they apply:
+                  * RNN with H = 64), 1 = FFMA (CUDA cores), 2 = tensor cores   */
   /* Optional instrumentation (all may be NULL/0): if `events` is non-NULL the
    * library records events[2k] / events[2k+1] (cudaEvent_t, created by the
    * caller) on `stream` immediately before / after its k-th kernel launch,

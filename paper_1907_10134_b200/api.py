@@ -31,8 +31,8 @@ class _Jac(C.Structure):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("mode", _i), ("block0", _i), ("block", _i), ("events", C.POINTER(_vp)), ("n_events", _i),
-                ("launches", C.POINTER(_i))]
+    _fields_ = [("mode", _i), ("block0", _i), ("block", _i), ("leaf_impl", _i), ("events", C.POINTER(_vp)),
+                ("n_events", _i), ("launches", C.POINTER(_i))]
 
 
 EXPORTS = {
@@ -129,8 +129,12 @@ def jacobians_dense(JT: torch.Tensor) -> Jacobians:
 
 
 # ----------------------------------------------------------------- scan
-def _opts(mode="blocked", block0=0, block=0, trace=None) -> _Opts:
-    o = _Opts(MODES[mode] if isinstance(mode, str) else int(mode), int(block0), int(block))
+LEAF_IMPL = {"auto": 0, "ffma": 1, "tensor": 2}
+
+
+def _opts(mode="blocked", block0=0, block=0, trace=None, leaf_impl="auto") -> _Opts:
+    o = _Opts(MODES[mode] if isinstance(mode, str) else int(mode), int(block0), int(block),
+              LEAF_IMPL[leaf_impl] if isinstance(leaf_impl, str) else int(leaf_impl))
     if trace is not None:
         o.events, o.n_events, o.launches = trace._arr, len(trace.events), C.pointer(trace._count)
     return o
@@ -169,7 +173,8 @@ def workspace(nbytes: int, device=None) -> torch.Tensor:
 
 def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
          grad_h_init: torch.Tensor | bool | None = None, ws: torch.Tensor | None = None,
-         mode="blocked", block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None):
+         mode="blocked", block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None,
+         leaf_impl="auto"):
     """bppsa_scan: all grad_h[t] = dl/dh_t at once (and dl/dh_init if asked)."""
     T, B, H = jac.T, jac.B, jac.H
     dev = seed.device
@@ -179,7 +184,7 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
         grad_h_init = torch.empty((B, H), dtype=torch.float32, device=dev)
     elif grad_h_init is False:
         grad_h_init = None
-    o = _opts(mode, block0, block, trace)
+    o = _opts(mode, block0, block, trace, leaf_impl)
     if ws is None:
         ws = workspace(scan_workspace_size(jac, mode, block0, block), dev)
     _check(_lib.bppsa_scan(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(grad_h, "grad_h"),
@@ -189,8 +194,9 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
 
 
 def scan_shard_up(jac: Jacobians, seed: torch.Tensor | None, aggregate: torch.Tensor, ws: torch.Tensor,
-                  block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None):
-    o = _opts("blocked", block0, block, trace)
+                  block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None,
+                  leaf_impl="auto"):
+    o = _opts("blocked", block0, block, trace, leaf_impl)
     _check(_lib.bppsa_scan_shard_up(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(aggregate, "aggregate"),
                                     ws.data_ptr(), ws.numel(), C.byref(o), _stream(stream)), "bppsa_scan_shard_up")
     return aggregate

@@ -87,7 +87,25 @@ void report_launches(const bppsa_scan_opts* o, const Tracer& t) {
   if (o && o->launches) *o->launches = t.k;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// tcgen05 level-0 fold: tanh RNN with H = 64 (a dense 64-wide contraction per
+// step); everything else runs on the CUDA cores.
+bool use_tensor_leaf(const bppsa_jac& j, int leaf_impl) {
+  const bool ok = j.kind == BPPSA_JAC_RNN_TANH && j.H == 64;
+  return leaf_impl == 2 ? ok : (leaf_impl == 0 && ok);
+}
+
 struct Plan {
+  int leaf_impl = 0;
   int L = 0;
   long long n[kMaxLevels + 2] = {};
   int C[kMaxLevels + 2] = {};
@@ -146,6 +164,10 @@ bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts
   const long long S = (long long)j.T + head;
   const size_t HH = (size_t)j.H * j.H, B = (size_t)j.B;
   size_t off = 0;
+  p->leaf_impl = opts ? opts->leaf_impl : 0;
+  if (p->leaf_impl < 0 || p->leaf_impl > 2) return fail(BPPSA_ERR_INVALID_ARGUMENT, "leaf_impl must be 0, 1 or 2");
+  if (p->leaf_impl == 2 && !(j.kind == BPPSA_JAC_RNN_TANH && j.H == 64))
+    return fail(BPPSA_ERR_NOT_SUPPORTED, "tensor-core leaf fold is built for the tanh RNN with H = 64");
   p->has_dense = (j.kind == BPPSA_JAC_DENSE) && mode != BPPSA_SCAN_ALG1;
   if (p->has_dense) {
     p->dense_off = off;
@@ -243,7 +265,14 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
     cudaError_t e;
     tr.begin(st);
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
-      e = launch_leaf_up(leaf_args(j, head, seed), p.C[0], dst, p.n[1], st);
+      const LeafArgs la = leaf_args(j, head, seed);
+      if (use_tensor_leaf(j, p.leaf_impl)) {
+        // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
+        e = head ? launch_leaf_up(la, p.C[0], dst, p.n[1], 0, 1, st) : cudaSuccess;
+        if (e == cudaSuccess) e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], head, num_sms(), st);
+      } else {
+        e = launch_leaf_up(la, p.C[0], dst, p.n[1], 0, p.n[1], st);
+      }
     } else {
       const MatAcc A = (l == 0) ? dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed)
                                 : level_acc(p, ws, l, H);

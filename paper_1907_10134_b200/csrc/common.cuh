@@ -68,9 +68,12 @@ struct LeafArgs {            // implicit leaves (RNN / GRU)
   const float* seed;         // head only
 };
 
-// level-0 fold: blocks of C slots -> agg_out [B][n_out][H*H] (column-major)
-cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out,
-                           cudaStream_t st);
+// level-0 fold: blocks q in [q0, q0+nq) of C slots -> agg_out [B][n_out][H*H] (column-major)
+cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
+                           long long nq, cudaStream_t st);
+// same on the tensor cores (tcgen05, 3xTF32): RNN, H == 64, matrix blocks q in [q0, n_out)
+cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
+                              int num_sms, cudaStream_t st);
 // level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable
 cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry,
                              long long nblk, float* grad_h, float* grad_init,
@@ -105,8 +108,6 @@ cudaError_t launch_alg1_extract(const float* X, const float* JT, float* grad_h,
 // shards: carry = M_{r+1} ... M_{G-2} V_{G-1}
 cudaError_t launch_carry_combine(const float* gathered, int rank, int world, int B, int H,
                                  float* carry_out, cudaStream_t st);
-cudaError_t launch_copy_aggregate(const float* agg_top, int B, int H, int head,
-                                  float* out, cudaStream_t st);
 
 // weight gradients
 cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const float* h,

@@ -108,9 +108,44 @@ __device__ __forceinline__ void matvec(const float (&w)[NX<CELL>::v][NR][HT],
   }
 }
 
+// All NC chains at once: for every k the NC x NR accumulators are independent,
+// so consecutive FFMAs never wait on each other (x for 4 k's of every chain is
+// loaded first with 16-byte broadcast reads).
+template <int CELL, int HT, int NR, int NC>
+__device__ __forceinline__ void matvec_multi(const float (&w)[NX<CELL>::v][NR][HT],
+                                             const float* __restrict__ xb, float (&acc)[NC][NR]) {
+  constexpr int NV = NX<CELL>::v;
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+#pragma unroll
+    for (int m = 0; m < NR; ++m) acc[j][m] = 0.f;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+#pragma unroll
+    for (int k4 = 0; k4 < HT / 4; ++k4) {
+      float4 xv[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) xv[j] = *reinterpret_cast<const float4*>(xb + (j * NV + v) * HT + 4 * k4);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * k4 + kk;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const float xk = kk == 0 ? xv[j].x : kk == 1 ? xv[j].y : kk == 2 ? xv[j].z : xv[j].w;
+#pragma unroll
+          for (int m = 0; m < NR; ++m) acc[j][m] = fmaf(w[v][m][k], xk, acc[j][m]);
+        }
+      }
+    }
+  }
+}
+
 template <int CELL, int HT, int NC>
-__global__ void __launch_bounds__(128) leaf_up_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
-                                                      long long n_out) {
+struct UpBounds { static constexpr int minb = (CELL == BPPSA_JAC_RNN_TANH && HT == 64) ? 3 : 1; };
+
+template <int CELL, int HT, int NC>
+__global__ void __launch_bounds__(128, UpBounds<CELL, HT, NC>::minb) leaf_up_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                      long long n_out, long long q0, long long nq) {
   constexpr int NR = (HT + 31) / 32;
   constexpr int NV = NX<CELL>::v;
   constexpr int XW = NC * NV * HT;       // floats per x buffer
@@ -120,11 +155,11 @@ __global__ void __launch_bounds__(128) leaf_up_kernel(LeafArgs a, int C, float* 
   float* xs = smem + wib * 2 * XW;
   const int G = (H + NC - 1) / NC;
   const long long task = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
-  if (task >= (long long)B * n_out * G) return;
+  if (task >= (long long)B * nq * G) return;
   const int cg = (int)(task % G);
   const long long rest = task / G;
-  const long long q = rest % n_out;
-  const int b = (int)(rest / n_out);
+  const long long q = q0 + rest % nq;
+  const int b = (int)(rest / nq);
   const long long S = a.seg.S();
   const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
   const bool vec = a.seg.head && q == 0;
@@ -173,29 +208,26 @@ __global__ void __launch_bounds__(128) leaf_up_kernel(LeafArgs a, int C, float* 
     float* xb = xs + buf * XW;
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
-      if (j < nc) {
 #pragma unroll
-        for (int m = 0; m < NR; ++m) {
-          const int i = lane + 32 * m;
-          if (i < HT) {
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        if (i < HT) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) xb[(j * NV + v) * HT + i] = cur[m].c[v] * c[j][m];
-          }
+          for (int v = 0; v < NV; ++v) xb[(j * NV + v) * HT + i] = (j < nc) ? cur[m].c[v] * c[j][m] : 0.f;
         }
       }
     }
     __syncwarp();
+    {
+      float acc[NC][NR];
+      matvec_multi<CELL, HT, NR, NC>(w, xb, acc);    // chains j >= nc compute on zeros
 #pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      if (j < nc) {
-        float acc[NR];
-        matvec<CELL, HT, NR, 1>(w, xb + j * NV * HT, acc);
+      for (int j = 0; j < NC; ++j)
 #pragma unroll
         for (int m = 0; m < NR; ++m) {
-          if (CELL == BPPSA_JAC_GRU) acc[m] = fmaf(cur[m].c[3], c[j][m], acc[m]);
-          c[j][m] = acc[m];
+          if (CELL == BPPSA_JAC_GRU) acc[j][m] = fmaf(cur[m].c[3], c[j][m], acc[j][m]);
+          c[j][m] = acc[j][m];
         }
-      }
     }
     buf ^= 1;
   }
@@ -307,9 +339,11 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
 constexpr int kWarpsPerCta = 4;
 
 template <int CELL, int HT, int NC>
-cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, cudaStream_t st) {
+cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
+                    cudaStream_t st) {
   const int G = (a.seg.H + NC - 1) / NC;
-  const long long tasks = (long long)a.seg.B * n_out * G;
+  const long long tasks = (long long)a.seg.B * nq * G;
+  if (tasks == 0) return cudaSuccess;
   const long long grid = (tasks + kWarpsPerCta - 1) / kWarpsPerCta;
   const size_t smem = (size_t)kWarpsPerCta * 2 * NC * NX<CELL>::v * HT * sizeof(float);
   auto k = leaf_up_kernel<CELL, HT, NC>;
@@ -317,7 +351,7 @@ cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, c
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(a, C, agg_out, n_out);
+  k<<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(a, C, agg_out, n_out, q0, nq);
   return cudaGetLastError();
 }
 
@@ -334,15 +368,16 @@ cudaError_t down_impl(const LeafArgs& a, int C, const float* carry, long long nb
 
 }  // namespace
 
-cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, cudaStream_t st) {
+cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
+                           long long nq, cudaStream_t st) {
   const int H = a.seg.H;
   if (a.kind == BPPSA_JAC_RNN_TANH) {
-    if (H == 20) return up_impl<BPPSA_JAC_RNN_TANH, 20, 20>(a, C, agg_out, n_out, st);
-    if (H <= 32) return up_impl<BPPSA_JAC_RNN_TANH, 32, 16>(a, C, agg_out, n_out, st);
-    return up_impl<BPPSA_JAC_RNN_TANH, 64, 8>(a, C, agg_out, n_out, st);
+    if (H == 20) return up_impl<BPPSA_JAC_RNN_TANH, 20, 20>(a, C, agg_out, n_out, q0, nq, st);
+    if (H <= 32) return up_impl<BPPSA_JAC_RNN_TANH, 32, 16>(a, C, agg_out, n_out, q0, nq, st);
+    return up_impl<BPPSA_JAC_RNN_TANH, 64, 8>(a, C, agg_out, n_out, q0, nq, st);
   }
-  if (H == 20) return up_impl<BPPSA_JAC_GRU, 20, 10>(a, C, agg_out, n_out, st);
-  return up_impl<BPPSA_JAC_GRU, 32, 8>(a, C, agg_out, n_out, st);
+  if (H == 20) return up_impl<BPPSA_JAC_GRU, 20, 10>(a, C, agg_out, n_out, q0, nq, st);
+  return up_impl<BPPSA_JAC_GRU, 32, 8>(a, C, agg_out, n_out, q0, nq, st);
 }
 
 cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk,

@@ -1,0 +1,299 @@
+// tc_leaf.cu — level-0 up-sweep fold of the tanh-RNN leaves on the 5th-gen
+// tensor cores (tcgen05, TMEM accumulators), H = 64.
+//
+// Every step of every column chain of every block multiplies by the SAME
+// W_hh (leaf J_t^T = W^T diag(1-h_t^2), eqn:rnn P:315; see leaf.cu):
+//     c_new^T = (d_t o c)^T W      for all chains at once
+// i.e. one dense contraction D[128 x 64] = A[128 x 64] . B[64 x 64] per step
+// and tile, with A = X^T (one row per chain: x = d o c), B[n][k] = W[k][n].
+// fp32 accuracy from 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, x = x_hi +
+// x_lo, x_hi = tf32_rn(x), x_lo = tf32_rn(x - x_hi)).  lo is rounded to
+// nearest explicitly: left to the MMA's operand truncation it carries a
+// one-signed 2^-21 bias per product that grows linearly along a chain.
+//
+// A tile = 128 chains = the 64 column chains of block q of sample b and those
+// of sample b+1 (same slots, same length).  CTA = 2 epilogue warpgroups (one
+// tile each, thread = chain = TMEM lane) + 1 MMA-issuer warp; two tiles are
+// in flight so one tile's epilogue (TMEM -> regs, scale by d, split, st.shared)
+// overlaps the other tile's MMAs.  Persistent grid, one CTA per SM.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace bppsa {
+namespace {
+
+constexpr int TH = 64;                    // hidden size of this kernel
+constexpr int TM = 128;                   // chains per tile (UMMA M)
+constexpr int NSLOT = 2;                  // tiles in flight per CTA
+constexpr int NTHREADS = 32 * (4 * NSLOT + 1);
+constexpr int A_BYTES = TM * TH * 4;      // 32 KB
+constexpr int B_BYTES = TH * TH * 4;      // 16 KB
+constexpr int OFF_A = 0;                                  // [slot][hi,lo]
+constexpr int OFF_B = OFF_A + NSLOT * 2 * A_BYTES;        // [hi,lo]
+constexpr int OFF_BAR = OFF_B + 2 * B_BYTES;              // a_full[2], d_full[2], tmem
+constexpr int SMEM_BYTES = OFF_BAR + 64 + 1024;           // + 1024 B alignment slack
+constexpr uint32_t TMEM_COLS = 128;
+// instruction descriptor: D f32, A/B tf32, both K-major, N = 64, M = 128
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TH >> 3) << 17) |
+                           ((uint32_t)(TM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// element (row, k) of a K-major SWIZZLE_128B tile with `rows` rows and K = 64
+// fp32: two K-halves of rows x 128 B; 8-row atoms of 1024 B; the 16-byte
+// chunk index is XORed with (row % 8).
+__device__ __forceinline__ uint32_t sw_off(int row, int k, int rows) {
+  const int kk = k & 31;
+  return (uint32_t)((k >> 5) * rows * 128 + (row >> 3) * 1024 + (row & 7) * 128 + (((kk >> 2) ^ (row & 7)) << 4) +
+                    ((kk & 3) << 2));
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;           // LBO (16 B; unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32; // SBO: stride between 8-row groups
+  d |= (uint64_t)1 << 46;           // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;           // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
+               : "memory");
+}
+
+// 64 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
+      "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// x = d o c written as the chain's row of A_hi / A_lo (swizzled, 16-B stores)
+__device__ __forceinline__ void write_row(char* Ahi, char* Alo, int row, const float (&hrow)[64],
+                                         const float (&c)[64]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    float hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float hv = hrow[4 * q + e];
+      const float x = (1.f - hv * hv) * c[4 * q + e];
+      hi[e] = tf32_rn(x);
+      lo[e] = tf32_rn(x - hi[e]);     // RN, not the hardware's truncation: no bias
+    }
+    const uint32_t off = sw_off(row, 4 * q, TM);
+    *reinterpret_cast<float4*>(Ahi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<float4*>(Alo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+__device__ __forceinline__ void load_row(const float* __restrict__ p, bool ok, float (&v)[64]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float4 t = ok ? __ldg(reinterpret_cast<const float4*>(p) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[4 * q] = t.x;
+    v[4 * q + 1] = t.y;
+    v[4 * q + 2] = t.z;
+    v[4 * q + 3] = t.w;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                 long long n_out, long long q0) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* d_full = a_full + NSLOT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nq = n_out - q0;
+  const int nbp = (B + 1) / 2;
+  const long long ntiles = (long long)nbp * nq;
+
+  // ---- setup: B = W (hi / lo), barriers, TMEM
+  for (int e = threadIdx.x; e < TH * TH; e += NTHREADS) {
+    const int n = e / TH, k = e % TH;               // B[n][k] = W[k][n]
+    const float w = __ldg(a.W + (long long)k * TH + n);
+    const float hi = tf32_rn(w);
+    const uint32_t off = sw_off(n, k, TH);
+    *reinterpret_cast<float*>(smem + OFF_B + off) = hi;
+    *reinterpret_cast<float*>(smem + OFF_B + B_BYTES + off) = tf32_rn(w - hi);
+  }
+  if (warp == 4 * NSLOT) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) {
+        mbar_init(&a_full[s], 128);
+        mbar_init(&d_full[s], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4 * NSLOT) {
+    // ================= MMA issuer (one elected thread) =================
+    uint32_t ph[NSLOT] = {0, 0};
+    const uint32_t b_hi = su32(smem + OFF_B), b_lo = b_hi + B_BYTES;
+    for (long long pr = blockIdx.x; 2 * pr < ntiles; pr += gridDim.x) {
+      long long len[NSLOT];
+      for (int sl = 0; sl < NSLOT; ++sl) {
+        const long long tau = 2 * pr + sl;
+        const long long q = q0 + tau / nbp;
+        len[sl] = (tau < ntiles) ? (min(q * C + C, S) - q * C) : 0;
+      }
+      const long long steps = max(len[0], len[1]);
+      for (long long st = 0; st < steps; ++st) {
+        for (int sl = 0; sl < NSLOT; ++sl) {
+          if (st >= len[sl]) continue;
+          mbar_wait(&a_full[sl], ph[sl]);
+          ph[sl] ^= 1;
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_hi = su32(smem + OFF_A + sl * 2 * A_BYTES), a_lo = a_hi + A_BYTES;
+            // correction products first (hi*lo, lo*hi), then hi*hi: the tensor
+            // core truncates every accumulation, so adding the small terms while
+            // the accumulator is still small cuts the one-signed bias per step
+            // from ~13 to ~5 ulp (scripts/tc_unit.cu, profiles/tc_precision.md)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              const int pq = (i + 1) % 3;            // 1: hi*lo, 2: lo*hi, 0: hi*hi
+              const uint32_t aa = (pq == 2) ? a_lo : a_hi, bb = (pq == 1) ? b_lo : b_hi;
+#pragma unroll
+              for (int kk = 0; kk < TH / 8; ++kk) {
+                const uint32_t aoff = (uint32_t)((kk >> 2) * TM * 128 + (kk & 3) * 32);
+                const uint32_t boff = (uint32_t)((kk >> 2) * TH * 128 + (kk & 3) * 32);
+                mma_tf32(tmem + sl * TH, sdesc(aa + aoff), sdesc(bb + boff), (i | kk) != 0);
+              }
+            }
+            mma_commit(&d_full[sl]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ================= epilogue warpgroup `g`: one tile, thread = chain =====
+    const int g = warp >> 2;
+    const int row = (warp & 3) * 32 + lane;                 // TMEM lane / A row
+    char* Ahi = smem + OFF_A + g * 2 * A_BYTES;
+    char* Alo = Ahi + A_BYTES;
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + g * TH;
+    uint32_t ph = 0;
+    const long long rowB = (long long)B * TH;
+    for (long long pr = blockIdx.x; 2 * pr < ntiles; pr += gridDim.x) {
+      const long long tau = 2 * pr + g;
+      if (tau >= ntiles) continue;
+      const long long q = q0 + tau / nbp;
+      const int b = (int)(tau % nbp) * 2 + (row >> 6);
+      const int j = row & 63;
+      const bool ok = b < B;
+      const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+      float c[64], hrow[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) c[k] = (k == j && ok) ? 1.f : 0.f;
+      load_row(a.h + (long long)a.seg.time_of(s0) * rowB + (long long)b * TH, ok, hrow);
+      for (long long s = s0; s < s1; ++s) {
+        write_row(Ahi, Alo, row, hrow, c);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&a_full[g]);
+        if (s + 1 < s1) load_row(a.h + (long long)a.seg.time_of(s + 1) * rowB + (long long)b * TH, ok, hrow);
+        mbar_wait(&d_full[g], ph);
+        ph ^= 1;
+        tc_fence_after();
+        tmem_ld64(taddr, c);
+      }
+      if (ok) {
+        float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH);
+#pragma unroll
+        for (int k4 = 0; k4 < 16; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4 * NSLOT) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace
+
+// Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.
+cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
+                              int num_sms, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const long long ntiles = (long long)((a.seg.B + 1) / 2) * (n_out - q0);
+  const long long pairs = (ntiles + 1) / 2;
+  const int grid = (int)std::min<long long>(pairs, num_sms);
+  if (grid <= 0) return cudaSuccess;
+  tc_leaf_up_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+  return cudaGetLastError();
+}
+
+}  // namespace bppsa
