@@ -543,14 +543,17 @@ bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed, cons
   return s;
 }
 
+// A fixed function of the row count only (deterministic results): parts of
+// at least 64 rows, at most 16 CTAs per SM of partial tiles.
 static long long wgrad_parts(long long rows) {
-  long long p = (rows + 1023) / 1024;
-  return std::max(1ll, std::min(p, 1184ll));
+  long long p = (rows + 63) / 64;
+  return std::max(1ll, std::min(p, 2368ll));
 }
 
 bppsa_status bppsa_weight_grads_workspace_size(int T, int B, int H, int I, size_t* bytes) {
   if (!bytes) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bytes is NULL");
   if (T < 1 || B < 1 || H < 1 || H > BPPSA_MAX_H || I < 0) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad shape");
+  if (!wgrad_supported(H, I)) return fail(BPPSA_ERR_NOT_SUPPORTED, "weight gradients need I + 1 <= 64");
   const long long P = wgrad_parts((long long)T * B);
   *bytes = align_up((size_t)P * 4 * H * (H + I + 1) * sizeof(float));   // GRU needs NA = 4H
   return BPPSA_OK;

@@ -110,6 +110,7 @@ cudaError_t launch_carry_combine(const float* gathered, int rank, int world, int
                                  float* carry_out, cudaStream_t st);
 
 // weight gradients
+bool wgrad_supported(int H, int I);
 cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const float* h,
                              const float* h_init, const float* grad_h, float* dW_ih,
                              float* dW_hh, float* db, float* ws, long long nparts,

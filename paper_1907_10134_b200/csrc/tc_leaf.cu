@@ -12,10 +12,14 @@
 // one-signed 2^-21 bias per product that grows linearly along a chain.
 //
 // A tile = 128 chains = the 64 column chains of block q of sample b and those
-// of sample b+1 (same slots, same length).  CTA = 2 epilogue warpgroups (one
-// tile each, thread = chain = TMEM lane) + 1 MMA-issuer warp; two tiles are
-// in flight so one tile's epilogue (TMEM -> regs, scale by d, split, st.shared)
-// overlaps the other tile's MMAs.  Persistent grid, one CTA per SM.
+// of sample b+1 (same slots, same length).  A (hi and lo) lives in TMEM next to
+// the accumulator (the TS form of tcgen05.mma): with N = 64 an SS-mode MMA
+// would read 6 KB of operands from shared memory per 32 cycles, above the
+// 128 B/clk shared-memory bandwidth; in TS mode only B (2 KB) comes from
+// shared memory.  CTA = 2 x 8 epilogue warps (thread = chain row x K-half:
+// tcgen05.ld D -> scale by d -> tf32 split -> tcgen05.st A) + 1 MMA-issuer
+// warp; two tiles are in flight so one tile's epilogue overlaps the other
+// tile's MMAs.  Persistent grid, one CTA per SM.
 #include <algorithm>
 
 #include "common.cuh"
@@ -26,14 +30,19 @@ namespace {
 constexpr int TH = 64;                    // hidden size of this kernel
 constexpr int TM = 128;                   // chains per tile (UMMA M)
 constexpr int NSLOT = 2;                  // tiles in flight per CTA
-constexpr int NTHREADS = 32 * (4 * NSLOT + 1);
-constexpr int A_BYTES = TM * TH * 4;      // 32 KB
+constexpr int EPI_WARPS = 8;               // per tile: 4 lane quarters x 2 column halves
+constexpr int EPI_THREADS = 32 * EPI_WARPS;
+constexpr int NTHREADS = 32 * (EPI_WARPS * NSLOT + 1);
 constexpr int B_BYTES = TH * TH * 4;      // 16 KB
-constexpr int OFF_A = 0;                                  // [slot][hi,lo]
-constexpr int OFF_B = OFF_A + NSLOT * 2 * A_BYTES;        // [hi,lo]
-constexpr int OFF_BAR = OFF_B + 2 * B_BYTES;              // a_full[2], d_full[2], tmem
+constexpr int OFF_B = 0;                                  // [hi,lo]
+constexpr int HCH = 64;                                   // steps staged per chunk
+constexpr int H_BYTES = 2 * HCH * TH * 4;                 // one tile's h slices (2 blocks), 32 KB
+constexpr int OFF_H = OFF_B + 2 * B_BYTES;                // [slot]
+constexpr int OFF_BAR = OFF_H + NSLOT * H_BYTES;          // a_full[2], d_full[2], tmem
 constexpr int SMEM_BYTES = OFF_BAR + 64 + 1024;           // + 1024 B alignment slack
-constexpr uint32_t TMEM_COLS = 128;
+// TMEM columns: D of slot g at [64g, 64g+64); A_hi / A_lo of slot g at
+// 128 + 128g + {0, 64}
+constexpr uint32_t TMEM_COLS = 512;
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 64, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TH >> 3) << 17) |
                            ((uint32_t)(TM >> 4) << 24);
@@ -85,30 +94,43 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(IDESC), "r"(acc));
 }
+// A from TMEM (K-major: row = lane, K along 32-bit columns), B from shared memory
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(IDESC), "r"(acc));
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
                : "memory");
 }
 
-// 64 consecutive fp32 TMEM columns of this thread's lane
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
-  uint32_t r[64];
+// 32 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
-      "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
         "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
-        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
-        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
-        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
-        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
 }
 
 __device__ __forceinline__ float tf32_rn(float x) {
@@ -117,34 +139,35 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-// x = d o c written as the chain's row of A_hi / A_lo (swizzled, 16-B stores)
-__device__ __forceinline__ void write_row(char* Ahi, char* Alo, int row, const float (&hrow)[64],
-                                         const float (&c)[64]) {
+// x = d o c for the K-half `kh` (32 columns) of the chain's row, split into
+// tf32 hi / lo and stored to the A_hi / A_lo TMEM columns of this lane;
+// hrow = the block's staged h_t row (shared memory, broadcast reads)
+__device__ __forceinline__ void write_half_tmem(uint32_t t_ahi, uint32_t t_alo, int kh,
+                                               const float* __restrict__ hrow, const float (&c)[32]) {
+  uint32_t hi[32], lo[32];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    float hi[4], lo[4];
+  for (int q = 0; q < 8; ++q) {
+    const float4 h4 = *reinterpret_cast<const float4*>(hrow + 32 * kh + 4 * q);
+    const float hv4[4] = {h4.x, h4.y, h4.z, h4.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float hv = hrow[4 * q + e];
+      const float hv = hv4[e];
       const float x = (1.f - hv * hv) * c[4 * q + e];
-      hi[e] = tf32_rn(x);
-      lo[e] = tf32_rn(x - hi[e]);     // RN, not the hardware's truncation: no bias
+      const float h = tf32_rn(x);
+      hi[4 * q + e] = __float_as_uint(h);
+      lo[4 * q + e] = __float_as_uint(tf32_rn(x - h));   // RN, not the MMA's truncation: no bias
     }
-    const uint32_t off = sw_off(row, 4 * q, TM);
-    *reinterpret_cast<float4*>(Ahi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<float4*>(Alo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
   }
+  tmem_st32(t_ahi + 32 * kh, hi);
+  tmem_st32(t_alo + 32 * kh, lo);
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
-__device__ __forceinline__ void load_row(const float* __restrict__ p, bool ok, float (&v)[64]) {
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const float4 t = ok ? __ldg(reinterpret_cast<const float4*>(p) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-    v[4 * q] = t.x;
-    v[4 * q + 1] = t.y;
-    v[4 * q + 2] = t.z;
-    v[4 * q + 3] = t.w;
-  }
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
@@ -170,10 +193,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
     *reinterpret_cast<float*>(smem + OFF_B + off) = hi;
     *reinterpret_cast<float*>(smem + OFF_B + B_BYTES + off) = tf32_rn(w - hi);
   }
-  if (warp == 4 * NSLOT) {
+  if (warp == EPI_WARPS * NSLOT) {
     if (lane == 0) {
       for (int s = 0; s < NSLOT; ++s) {
-        mbar_init(&a_full[s], 128);
+        mbar_init(&a_full[s], EPI_THREADS);
         mbar_init(&d_full[s], 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -189,7 +212,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4 * NSLOT) {
+  if (warp == EPI_WARPS * NSLOT) {
     // ================= MMA issuer (one elected thread) =================
     uint32_t ph[NSLOT] = {0, 0};
     const uint32_t b_hi = su32(smem + OFF_B), b_lo = b_hi + B_BYTES;
@@ -208,7 +231,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
           ph[sl] ^= 1;
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a_hi = su32(smem + OFF_A + sl * 2 * A_BYTES), a_lo = a_hi + A_BYTES;
+            const uint32_t a_hi = tmem + 128 + 128 * sl, a_lo = a_hi + 64;
             // correction products first (hi*lo, lo*hi), then hi*hi: the tensor
             // core truncates every accumulation, so adding the small terms while
             // the accumulator is still small cuts the one-signed bias per step
@@ -219,9 +242,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
               const uint32_t aa = (pq == 2) ? a_lo : a_hi, bb = (pq == 1) ? b_lo : b_hi;
 #pragma unroll
               for (int kk = 0; kk < TH / 8; ++kk) {
-                const uint32_t aoff = (uint32_t)((kk >> 2) * TM * 128 + (kk & 3) * 32);
                 const uint32_t boff = (uint32_t)((kk >> 2) * TH * 128 + (kk & 3) * 32);
-                mma_tf32(tmem + sl * TH, sdesc(aa + aoff), sdesc(bb + boff), (i | kk) != 0);
+                mma_tf32_ts(tmem + sl * TH, aa + 8 * kk, sdesc(bb + boff), (i | kk) != 0);
               }
             }
             mma_commit(&d_full[sl]);
@@ -231,47 +253,65 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
       }
     }
   } else {
-    // ================= epilogue warpgroup `g`: one tile, thread = chain =====
-    const int g = warp >> 2;
-    const int row = (warp & 3) * 32 + lane;                 // TMEM lane / A row
-    char* Ahi = smem + OFF_A + g * 2 * A_BYTES;
-    char* Alo = Ahi + A_BYTES;
-    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + g * TH;
+    // ===== epilogue of tile slot g: 8 warps, thread = (chain row, K-half) =====
+    const int g = warp / EPI_WARPS, wl = warp % EPI_WARPS;
+    const int row = (wl & 3) * 32 + lane;                   // TMEM lane / A row (lane quarter = warp % 4)
+    const int kh = wl >> 2;                                 // column half of D / K-half of A
+    const int et = wl * 32 + lane;                          // 0 .. EPI_THREADS-1
+    const uint32_t lane_base = tmem + ((uint32_t)((wl & 3) * 32) << 16);
+    const uint32_t taddr = lane_base + g * TH + 32 * kh;             // D, this thread's 32 columns
+    const uint32_t t_ahi = lane_base + 128 + 128 * g, t_alo = t_ahi + 64;
+    float* hs = reinterpret_cast<float*>(smem + OFF_H + g * H_BYTES);   // [2 blocks][HCH][64]
     uint32_t ph = 0;
     const long long rowB = (long long)B * TH;
     for (long long pr = blockIdx.x; 2 * pr < ntiles; pr += gridDim.x) {
       const long long tau = 2 * pr + g;
       if (tau >= ntiles) continue;
       const long long q = q0 + tau / nbp;
-      const int b = (int)(tau % nbp) * 2 + (row >> 6);
+      const int bp = (int)(tau % nbp);
+      const int b = bp * 2 + (row >> 6);
       const int j = row & 63;
       const bool ok = b < B;
       const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
-      float c[64], hrow[64];
+      float c[32];
 #pragma unroll
-      for (int k = 0; k < 64; ++k) c[k] = (k == j && ok) ? 1.f : 0.f;
-      load_row(a.h + (long long)a.seg.time_of(s0) * rowB + (long long)b * TH, ok, hrow);
-      for (long long s = s0; s < s1; ++s) {
-        write_row(Ahi, Alo, row, hrow, c);
-        fence_async_smem();
-        tc_fence_before();
-        mbar_arrive(&a_full[g]);
-        if (s + 1 < s1) load_row(a.h + (long long)a.seg.time_of(s + 1) * rowB + (long long)b * TH, ok, hrow);
-        mbar_wait(&d_full[g], ph);
-        ph ^= 1;
-        tc_fence_after();
-        tmem_ld64(taddr, c);
+      for (int k = 0; k < 32; ++k) c[k] = (32 * kh + k == j && ok) ? 1.f : 0.f;
+      for (long long sc = s0; sc < s1; sc += HCH) {
+        const int n = (int)min((long long)HCH, s1 - sc);
+        // stage the h_t rows of this chunk for both blocks of the tile (cp.async)
+        named_bar(1 + g, EPI_THREADS);             // previous chunk fully consumed
+        for (int e = et; e < 2 * n * 16; e += EPI_THREADS) {
+          const int bb = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+          float* dst = hs + (bb * HCH + st) * TH + ch * 4;
+          const int bs = bp * 2 + bb;
+          if (bs < B)
+            cp_async16(dst, a.h + (long long)a.seg.time_of(sc + st) * rowB + (long long)bs * TH + ch * 4);
+          else
+            *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        named_bar(1 + g, EPI_THREADS);
+        const float* hb = hs + (row >> 6) * HCH * TH;
+        for (int st = 0; st < n; ++st) {
+          write_half_tmem(t_ahi, t_alo, kh, hb + st * TH, c);
+          tc_fence_before();
+          mbar_arrive(&a_full[g]);
+          mbar_wait(&d_full[g], ph);
+          ph ^= 1;
+          tc_fence_after();
+          tmem_ld32(taddr, c);
+        }
       }
       if (ok) {
-        float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH);
+        float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 32 * kh);
 #pragma unroll
-        for (int k4 = 0; k4 < 16; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+        for (int k4 = 0; k4 < 8; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4 * NSLOT) {
+  if (warp == EPI_WARPS * NSLOT) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
   }

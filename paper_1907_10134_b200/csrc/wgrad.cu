@@ -1,29 +1,32 @@
 // wgrad.cu — parameter gradients (eqn:update_param) for tied
 // recurrent weights summed over time:  dW = sum_{t,b} delta_{t,b} u_{t,b}^T.
 //
-// One contraction over K = T*B rows: out[a][c] = sum_rows A_row[a] * B_row[c]
-//   RNN: A = delta = (1-h^2) o grad_h              (H)
-//        B = [h_{t-1} | x_t | 1]                     (H + I + 1)
-//   GRU: A = [dR | dZ | dN | dM]                     (4H)
-//        B = [h_{t-1} | x_t | 1]
-// Rows are split into a fixed number of parts (a function of K only), each
-// CTA accumulates a 64 x 128 output tile of one part in registers (4 x 8
-// per thread, operands staged through shared memory), partial tiles go to
-// the workspace and a second kernel sums the parts in a fixed order —
-// deterministic, no float atomics.
+// One contraction over K = T*B rows: out[a][c] = sum_rows A_row[a] * U_row[c]
+//   RNN: A = delta = (1-h^2) o grad_h              (NA = H)
+//   GRU: A = [dR | dZ | dN | dM]                     (NA = 4H)
+//   U   = [h_{t-1} (H) | x_t (I) | 1]                (H + I + 1 columns)
+// Rows are split into a fixed number of parts (a function of K only).  A CTA
+// owns one part and a 64-row slice of A: the H x 64 "hidden" block sits in a
+// 4x4-per-thread register tile, the (I + 1) "extra" columns are spread over
+// the threads; row stages of 32 are double-buffered through shared memory
+// (the next stage's operands are loaded while the current one is consumed).
+// Partial tiles go to the workspace and a second kernel sums the parts in a
+// fixed order — deterministic, no float atomics, round-to-nearest FFMA.
 #include "common.cuh"
 
 namespace bppsa {
 namespace {
 
-constexpr int TA = 64, TB = 128, RR = 32, NT = 256;
+constexpr int TA = 64, RR = 32, NT = 256, MAXE = 64;
+constexpr int PER_A = RR * TA / NT;   // 8 elements of A per thread per stage
+constexpr int PER_U = RR * TA / NT;   // 8 elements of U (hidden part) per thread per stage
 
 struct WArgs {
   int T, B, H, I, kind;
   const float *x, *h, *h_init, *g;              // RNN (h) / both (x, g)
   const float *hp, *r, *z, *n, *M;              // GRU
   long long rows, rows_per_part;
-  int NA, NB;
+  int NA, E;                                    // E = I + 1 extra columns
 };
 
 __device__ __forceinline__ float valA(const WArgs& w, long long row, int a) {
@@ -33,7 +36,7 @@ __device__ __forceinline__ float valA(const WArgs& w, long long row, int a) {
     const float hv = w.h[o];
     return (1.f - hv * hv) * w.g[o];
   }
-  const int gate = a / w.H, i = a % w.H;
+  const int gate = a / w.H, i = a - gate * w.H;
   const long long o = row * w.H + i;
   const float g = w.g[o], z = w.z[o], n = w.n[o];
   const float dN = g * (1.f - z) * (1.f - n * n);
@@ -44,65 +47,112 @@ __device__ __forceinline__ float valA(const WArgs& w, long long row, int a) {
   return dN * r;
 }
 
-__device__ __forceinline__ float valB(const WArgs& w, long long row, int c) {
-  if (c < w.H) {
-    if (w.kind == BPPSA_JAC_GRU) return w.hp[row * w.H + c];
-    if (row >= w.B) return w.h[(row - w.B) * w.H + c];             // h_{t-1}
-    return w.h_init ? w.h_init[row * w.H + c] : 0.f;                 // t = 0: row = b
-  }
-  if (c < w.H + w.I) return w.x[row * w.I + (c - w.H)];
-  if (c == w.H + w.I) return 1.f;
-  return 0.f;
+__device__ __forceinline__ float valU(const WArgs& w, long long row, int c) {   // hidden part, c < H
+  if (c >= w.H) return 0.f;
+  if (w.kind == BPPSA_JAC_GRU) return w.hp[row * w.H + c];
+  if (row >= w.B) return w.h[(row - w.B) * w.H + c];             // h_{t-1}
+  return w.h_init ? w.h_init[row * w.H + c] : 0.f;                 // t = 0: row = b
+}
+
+__device__ __forceinline__ float valE(const WArgs& w, long long row, int c) {   // extra part
+  return (c < w.I) ? w.x[row * w.I + c] : 1.f;
 }
 
 __global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __restrict__ ws) {
-  __shared__ __align__(16) float As[RR][TA];
-  __shared__ __align__(16) float Bs[RR][TB];
-  const int part = blockIdx.x, ta = blockIdx.y, tb = blockIdx.z;
+  __shared__ __align__(16) float As[2][RR][TA];
+  __shared__ __align__(16) float Us[2][RR][TA];
+  __shared__ float Es[2][RR][MAXE];
+  const int part = blockIdx.x, ta = blockIdx.y;
   const long long r0 = (long long)part * w.rows_per_part;
   const long long r1 = min(r0 + w.rows_per_part, w.rows);
   const int tid = threadIdx.x, ti = tid % 16, tj = tid / 16;
-  float acc[4][8];
+  const int nE = TA * w.E;                          // extra outputs of this A slice
+  float acc[4][4];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 8; ++y) acc[x][y] = 0.f;
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+  float eacc[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) eacc[u] = 0.f;
+
+  float pa[PER_A], pu[PER_U], pe[MAXE * RR / NT];
+  auto fetch = [&](long long rb) {
+#pragma unroll
+    for (int u = 0; u < PER_A; ++u) {
+      const int e = tid + u * NT, rr = e / TA, col = e % TA;
+      const long long row = rb + rr;
+      pa[u] = (row < r1) ? valA(w, row, ta * TA + col) : 0.f;
+      pu[u] = (row < r1) ? valU(w, row, col) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < MAXE * RR / NT; ++u) {
+      const int e = tid + u * NT, rr = e / MAXE, col = e % MAXE;
+      const long long row = rb + rr;
+      pe[u] = (row < r1 && col < w.E) ? valE(w, row, col) : 0.f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PER_A; ++u) {
+      const int e = tid + u * NT, rr = e / TA, col = e % TA;
+      As[buf][rr][col] = pa[u];
+      Us[buf][rr][col] = pu[u];
+    }
+#pragma unroll
+    for (int u = 0; u < MAXE * RR / NT; ++u) {
+      const int e = tid + u * NT;
+      Es[buf][e / MAXE][e % MAXE] = pe[u];
+    }
+  };
+
+  fetch(r0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
   for (long long rb = r0; rb < r1; rb += RR) {
-    for (int e = tid; e < RR * TA; e += NT) {
-      const int rr = e / TA, col = e % TA;
-      const long long row = rb + rr;
-      As[rr][col] = (row < r1) ? valA(w, row, ta * TA + col) : 0.f;
-    }
-    for (int e = tid; e < RR * TB; e += NT) {
-      const int rr = e / TB, col = e % TB;
-      const long long row = rb + rr;
-      Bs[rr][col] = (row < r1) ? valB(w, row, tb * TB + col) : 0.f;
-    }
-    __syncthreads();
+    const bool more = rb + RR < r1;
+    if (more) fetch(rb + RR);                        // loads in flight during the FMAs
 #pragma unroll 4
     for (int rr = 0; rr < RR; ++rr) {
-      const float4 a4 = *reinterpret_cast<const float4*>(&As[rr][ti * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[rr][tj * 8]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[rr][tj * 8 + 4]);
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[buf][rr][ti * 4]);
+      const float4 u4 = *reinterpret_cast<const float4*>(&Us[buf][rr][tj * 4]);
       const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float uv[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 8; ++y) acc[x][y] = fmaf(av[x], bv[y], acc[x][y]);
+        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(av[x], uv[y], acc[x][y]);
     }
+    for (int u = 0; u < 16; ++u) {                    // extra columns: x_t and the bias
+      const int e = tid + u * NT;
+      if (e >= nE) break;
+      const int a = e / w.E, c = e % w.E;
+      float s = eacc[u];
+      for (int rr = 0; rr < RR; ++rr) s = fmaf(As[buf][rr][a], Es[buf][rr][c], s);
+      eacc[u] = s;
+    }
+    if (more) stash(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
-  float* dst = ws + (long long)part * w.NA * w.NB;
+  const int NB = w.H + w.E;
+  float* dst = ws + (long long)part * w.NA * NB;
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
     const int a = ta * TA + ti * 4 + x;
     if (a >= w.NA) continue;
 #pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      const int c = tb * TB + tj * 8 + y;
-      if (c < w.NB) dst[(long long)a * w.NB + c] = acc[x][y];
+    for (int y = 0; y < 4; ++y) {
+      const int c = tj * 4 + y;
+      if (c < w.H) dst[(long long)a * NB + c] = acc[x][y];
     }
+  }
+  for (int u = 0; u < 16; ++u) {
+    const int e = tid + u * NT;
+    if (e >= nE) break;
+    const int a = ta * TA + e / w.E, c = e % w.E;
+    if (a < w.NA) dst[(long long)a * NB + w.H + c] = eacc[u];
   }
 }
 
@@ -152,12 +202,14 @@ __global__ void wgrad_reduce_gru(const float* __restrict__ ws, long long P, int 
 }
 
 cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream_t st) {
-  dim3 grid((unsigned)nparts, (unsigned)((w.NA + TA - 1) / TA), (unsigned)((w.NB + TB - 1) / TB));
+  dim3 grid((unsigned)nparts, (unsigned)((w.NA + TA - 1) / TA));
   wgrad_partial_kernel<<<grid, NT, 0, st>>>(w, ws);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+bool wgrad_supported(int H, int I) { return H <= TA && I + 1 <= MAXE && TA * (I + 1) <= 16 * NT; }
 
 cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const float* h, const float* h_init,
                              const float* grad_h, float* dW_ih, float* dW_hh, float* db, float* ws,
@@ -167,10 +219,11 @@ cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const f
   w.x = x; w.h = h; w.h_init = h_init; w.g = grad_h;
   w.rows = (long long)T * B;
   w.rows_per_part = (w.rows + nparts - 1) / nparts;
-  w.NA = H; w.NB = H + I + 1;
+  w.NA = H; w.E = I + 1;
   cudaError_t e = run_partials(w, ws, nparts, st);
   if (e != cudaSuccess) return e;
-  wgrad_reduce_rnn<<<(H * w.NB + 255) / 256, 256, 0, st>>>(ws, nparts, H, I, dW_ih, dW_hh, db);
+  const int NB = H + I + 1;
+  wgrad_reduce_rnn<<<(H * NB + 255) / 256, 256, 0, st>>>(ws, nparts, H, I, dW_ih, dW_hh, db);
   return cudaGetLastError();
 }
 
@@ -183,7 +236,7 @@ cudaError_t launch_wgrad_gru(int T, int B, int H, int I, const float* x, const f
   w.x = x; w.g = grad_h; w.hp = hp; w.r = r; w.z = z; w.n = n; w.M = M;
   w.rows = (long long)T * B;
   w.rows_per_part = (w.rows + nparts - 1) / nparts;
-  w.NA = 4 * H; w.NB = H + I + 1;
+  w.NA = 4 * H; w.E = I + 1;
   cudaError_t e = run_partials(w, ws, nparts, st);
   if (e != cudaSuccess) return e;
   const int total = 3 * H * H + 3 * H * I + 6 * H;

@@ -69,8 +69,9 @@ def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None
         raise ValueError("exactly the last rank passes the seed")
     agg = backend.up(seed)
     if world > 1:
-        gathered = torch.empty((world,) + tuple(agg.shape), dtype=agg.dtype, device=agg.device)
-        dist.all_gather_into_tensor(gathered, agg.contiguous(), group=group)
+        flat = torch.empty((world * agg.shape[0],) + tuple(agg.shape[1:]), dtype=agg.dtype, device=agg.device)
+        dist.all_gather_into_tensor(flat, agg.contiguous(), group=group)    # concat form (NCCL and gloo)
+        gathered = flat.view((world,) + tuple(agg.shape))
     else:
         gathered = agg.unsqueeze(0)
     return backend.down(seed, None if head else gathered, rank, world, grad_h=grad_h, want_init=want_init)
