@@ -195,6 +195,88 @@ bppsa_status bppsa_weight_grads_gru(int T, int B, int H, int I, const float* x,
                                     float* db_hh3, void* ws, size_t ws_bytes,
                                     void* stream);
 
+/* ---------------------------------------------------------------------------
+ * CSR variant (P:182 sec:jcb_in_sparse_format): transposed
+ * Jacobians with architecture-fixed ("guaranteed zero") sparsity patterns; a
+ * symbolic product plan computed once ahead of time (output patterns and, for
+ * every output entry, its contribution pairs); numeric SpGEMM / SpMV on the
+ * device; the level-balanced hybrid schedule of P:472 (up-sweep levels
+ * d < u, a serial bridge over the 2^u-block aggregates, down-sweep levels
+ * d < dl, dl in {u, u+1}; DESIGN reading 19).
+ *
+ * Layouts: CSR in the SciPy convention, rows = the operator's INPUT space.
+ * Device data of a batched element is sample-minor, data[p * B + b] (one
+ * structural entry of all B samples is one contiguous 4B-vector, so every
+ * gather of the numeric SpGEMM reads B consecutive floats); a shared element
+ * (e.g. conv weights) is data[p].
+ * ------------------------------------------------------------------------- */
+typedef struct bppsa_csr_pattern {   /* HOST arrays                          */
+  int rows, cols;
+  long long nnz;
+  const long long* indptr;           /* [rows+1]                              */
+  const int* indices;                /* [nnz], strictly increasing per row    */
+} bppsa_csr_pattern;
+
+typedef struct bppsa_csr_plan bppsa_csr_plan;   /* opaque, immutable after create */
+
+/* chain[k] = pattern of J_{k+1}^T in time order (k = 0 is f_1, whose rows are
+ * the network input), n operators, chain compatibility cols(J_k^T) =
+ * rows(J_{k+1}^T).  Builds every symbolic product of the schedule on
+ * the host (may take seconds) and uploads the plan with cudaMemcpy
+ * (synchronous; not graph-capturable).  Errors: SHAPE for incompatible
+ * neighbours, INVALID_ARGUMENT for bad (u, dl), NOT_SUPPORTED when the
+ * schedule's products exceed `max_contributions` (0 = 2^31) pairs.         */
+bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n,
+                                   int up_levels, int down_levels,
+                                   long long max_contributions,
+                                   bppsa_csr_plan** plan);
+void bppsa_csr_plan_destroy(bppsa_csr_plan* plan);
+/* Workspace for batch B given which elements carry per-sample data.        */
+bppsa_status bppsa_csr_plan_workspace_size(const bppsa_csr_plan* plan, int B,
+                                           const int* batched, size_t* bytes);
+/* Static counts of the schedule (the FLOP analysis of fig:prune_symbolic,
+ * P:467): contribution pairs of all SpGEMMs, nnz touched by all SpMVs, and
+ * the number of numeric kernels one scan launches.                         */
+bppsa_status bppsa_csr_plan_info(const bppsa_csr_plan* plan,
+                                 long long* contributions, long long* spmv_nnz,
+                                 int* n_kernels);
+/* data[k]: device values of J_{k+1}^T (layout above; batched[k] != 0 for
+ * per-sample data).  seed: dl/dx_n [B][cols(J_n^T)].  grads[k], k = 0..n
+ * (n+1 pointers, NULL = not wanted): dl/dx_k [B][dim x_k]; grads[n] = seed;
+ * grads[0] = J_1^T dl/dx_1 is the inclusive extra.                          */
+bppsa_status bppsa_csr_scan(const bppsa_csr_plan* plan, int B,
+                            const float* const* data, const int* batched,
+                            const float* seed, float* const* grads, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* Analytical transposed-Jacobian builders (Algs. 2-10), device
+ * data + host patterns:
+ * conv 3x3 / pad 1 / stride 1, c_i -> c_o on h x w (generic stencil; reading
+ * 17).  Two-call pattern: pass NULL arrays to get *nnz.  weights_host
+ * [c_o][c_i][3][3] is only consulted when drop_zero != 0 (pruned taps leave
+ * the pattern).  tap[p] receives the weight index of entry p for
+ * bppsa_csr_conv_data.                                                      */
+bppsa_status bppsa_csr_conv3x3_pattern(int ci, int co, int h, int w,
+                                       const float* weights_host, int drop_zero,
+                                       long long* nnz, long long* indptr,
+                                       int* indices, int* tap);
+/* data[p] = weights[tap[p]] (device; shared across the batch)               */
+bppsa_status bppsa_csr_conv_data(long long nnz, const int* tap,
+                                 const float* weights, float* data,
+                                 void* stream);
+/* ReLU (Algs. 5-7): identity pattern of size d; data[i*B + b] = [x[b][i] > 0] */
+bppsa_status bppsa_csr_relu_data(long long d, int B, const float* x,
+                                 float* data, void* stream);
+/* 2x2/stride-2 max-pool window pattern (reading 18): row = input pixel
+ * (c, y, x), one entry in column (c, y/2, x/2).  Host pattern builder and
+ * device data: data[i*B + b] = 1 if pool_idx[b][c][y/2][x/2] (flat index in
+ * the c-th input plane, torch return_indices) selects pixel i, else 0.      */
+bppsa_status bppsa_csr_maxpool_pattern(int c, int h, int w, long long* indptr,
+                                       int* indices);
+bppsa_status bppsa_csr_maxpool_data(int c, int h, int w, int B,
+                                    const long long* pool_idx, float* data,
+                                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

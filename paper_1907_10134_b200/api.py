@@ -50,6 +50,24 @@ EXPORTS = {
     "bppsa_weight_grads_gru": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                     _vp, _sz, _vp]),
 }
+
+class _CsrPat(C.Structure):
+    _fields_ = [("rows", _i), ("cols", _i), ("nnz", C.c_longlong), ("indptr", _vp), ("indices", _vp)]
+
+
+_ll, _pp = C.c_longlong, C.POINTER(_vp)
+EXPORTS.update({
+    "bppsa_csr_plan_create": (_i, [C.POINTER(_CsrPat), _i, _i, _i, _ll, C.POINTER(_vp)]),
+    "bppsa_csr_plan_destroy": (None, [_vp]),
+    "bppsa_csr_plan_workspace_size": (_i, [_vp, _i, C.POINTER(_i), C.POINTER(_sz)]),
+    "bppsa_csr_plan_info": (_i, [_vp, C.POINTER(_ll), C.POINTER(_ll), C.POINTER(_i)]),
+    "bppsa_csr_scan": (_i, [_vp, _i, _pp, C.POINTER(_i), _vp, _pp, _vp, _sz, _vp]),
+    "bppsa_csr_conv3x3_pattern": (_i, [_i, _i, _i, _i, _vp, _i, C.POINTER(_ll), _vp, _vp, _vp]),
+    "bppsa_csr_conv_data": (_i, [_ll, _vp, _vp, _vp, _vp]),
+    "bppsa_csr_relu_data": (_i, [_ll, _i, _vp, _vp, _vp]),
+    "bppsa_csr_maxpool_pattern": (_i, [_i, _i, _i, _vp, _vp]),
+    "bppsa_csr_maxpool_data": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
+})
 for _name, (_res, _args) in EXPORTS.items():
     _f = getattr(_lib, _name)
     _f.restype, _f.argtypes = _res, _args
@@ -253,4 +271,116 @@ def weight_grads_gru(x, tape: dict, grad_h, ws=None, out=None, stream=None):
                                        _ptr(tape["M"], "M"), _ptr(grad_h, "grad_h"), _ptr(a, "dW_ih3"),
                                        _ptr(b_, "dW_hh3"), _ptr(c, "db_ih3"), _ptr(d, "db_hh3"), ws.data_ptr(),
                                        ws.numel(), _stream(stream)), "bppsa_weight_grads_gru")
+    return out
+
+
+# ----------------------------------------------------------------- CSR variant
+class CsrPlan:
+    """bppsa_csr_plan (library-owned; destroyed with this object)."""
+
+    def __init__(self, handle, n, dims):
+        self.h, self.n, self.dims = handle, n, dims      # dims[k] = dim x_k, k = 0..n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.bppsa_csr_plan_destroy(self.h)
+            self.h = None
+
+    def info(self):
+        c, s, k = C.c_longlong(), C.c_longlong(), _i()
+        _check(_lib.bppsa_csr_plan_info(self.h, C.byref(c), C.byref(s), C.byref(k)), "bppsa_csr_plan_info")
+        return {"contributions": c.value, "spmv_nnz": s.value, "kernels": k.value}
+
+    def workspace_size(self, B, batched):
+        arr = (_i * self.n)(*[int(b) for b in batched])
+        n = _sz()
+        _check(_lib.bppsa_csr_plan_workspace_size(self.h, B, arr, C.byref(n)), "bppsa_csr_plan_workspace_size")
+        return n.value
+
+
+def csr_plan_create(patterns, up_levels: int, down_levels: int, max_contributions: int = 0) -> CsrPlan:
+    """patterns: [(rows, cols, indptr int64 ndarray, indices int32 ndarray)] for
+    J_1^T .. J_n^T (time order)."""
+    import numpy as np
+    n = len(patterns)
+    keep = []
+    arr = (_CsrPat * n)()
+    for k, (rows, cols, ip, ix) in enumerate(patterns):
+        ip = np.ascontiguousarray(ip, dtype=np.int64)
+        ix = np.ascontiguousarray(ix, dtype=np.int32)
+        keep += [ip, ix]
+        arr[k] = _CsrPat(rows, cols, int(ip[-1]), ip.ctypes.data, ix.ctypes.data)
+    h = _vp()
+    _check(_lib.bppsa_csr_plan_create(arr, n, up_levels, down_levels, max_contributions, C.byref(h)),
+           "bppsa_csr_plan_create")
+    dims = [patterns[0][0]] + [p[1] for p in patterns]
+    return CsrPlan(h, n, dims)
+
+
+def csr_scan(plan: CsrPlan, data, batched, seed, grads=None, ws=None, stream=None):
+    """bppsa_csr_scan.  data[k]: device values of J_{k+1}^T ([nnz] shared or
+    [nnz, B] sample-minor); seed [B, dim x_n].  Returns grads[k] = dl/dx_k
+    ([B, dim x_k], k = 0..n)."""
+    B = seed.shape[0]
+    if grads is None:
+        grads = [torch.empty((B, d), dtype=torch.float32, device=seed.device) for d in plan.dims]
+    if ws is None:
+        ws = workspace(plan.workspace_size(B, batched), seed.device)
+    darr = (_vp * plan.n)(*[_ptr(d, f"data[{k}]") for k, d in enumerate(data)])
+    garr = (_vp * (plan.n + 1))(*[None if g is None else _ptr(g, "grad") for g in grads])
+    barr = (_i * plan.n)(*[int(b) for b in batched])
+    _check(_lib.bppsa_csr_scan(plan.h, B, darr, barr, _ptr(seed, "seed"), garr, ws.data_ptr(), ws.numel(),
+                               _stream(stream)), "bppsa_csr_scan")
+    return grads
+
+
+def csr_conv3x3_pattern(ci, co, h, w, weights=None, drop_zero=False):
+    """Host pattern of a 3x3/pad-1 conv J^T -> (indptr int64, indices int32, tap int32)."""
+    import numpy as np
+    wt = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+    wp = None if wt is None else wt.ctypes.data
+    nnz = C.c_longlong()
+    _check(_lib.bppsa_csr_conv3x3_pattern(ci, co, h, w, wp, int(drop_zero), C.byref(nnz), None, None, None),
+           "bppsa_csr_conv3x3_pattern")
+    ip = np.empty(ci * h * w + 1, np.int64)
+    ix = np.empty(nnz.value, np.int32)
+    tap = np.empty(nnz.value, np.int32)
+    _check(_lib.bppsa_csr_conv3x3_pattern(ci, co, h, w, wp, int(drop_zero), C.byref(nnz), ip.ctypes.data,
+                                          ix.ctypes.data, tap.ctypes.data), "bppsa_csr_conv3x3_pattern")
+    return ip, ix, tap
+
+
+def csr_conv_data(tap: torch.Tensor, weights: torch.Tensor, out=None, stream=None):
+    if out is None:
+        out = torch.empty(tap.numel(), dtype=torch.float32, device=tap.device)
+    _check(_lib.bppsa_csr_conv_data(tap.numel(), tap.data_ptr(), _ptr(weights, "weights"), _ptr(out, "data"),
+                                    _stream(stream)), "bppsa_csr_conv_data")
+    return out
+
+
+def csr_relu_data(x: torch.Tensor, out=None, stream=None):
+    """x [B, d] (ReLU inputs) -> data [d, B] in {0, 1} (Alg. 7)."""
+    B, d = x.shape[0], x[0].numel()
+    if out is None:
+        out = torch.empty((d, B), dtype=torch.float32, device=x.device)
+    _check(_lib.bppsa_csr_relu_data(d, B, _ptr(x, "x"), _ptr(out, "data"), _stream(stream)), "bppsa_csr_relu_data")
+    return out
+
+
+def csr_maxpool_pattern(c, h, w):
+    import numpy as np
+    ip = np.empty(c * h * w + 1, np.int64)
+    ix = np.empty(c * h * w, np.int32)
+    _check(_lib.bppsa_csr_maxpool_pattern(c, h, w, ip.ctypes.data, ix.ctypes.data), "bppsa_csr_maxpool_pattern")
+    return ip, ix
+
+
+def csr_maxpool_data(pool_idx: torch.Tensor, c, h, w, out=None, stream=None):
+    """pool_idx [B, c, h/2, w/2] int64 (torch return_indices) -> data [c*h*w, B]."""
+    B = pool_idx.shape[0]
+    if out is None:
+        out = torch.empty((c * h * w, B), dtype=torch.float32, device=pool_idx.device)
+    assert pool_idx.dtype == torch.int64 and pool_idx.is_contiguous()
+    _check(_lib.bppsa_csr_maxpool_data(c, h, w, B, pool_idx.data_ptr(), _ptr(out, "data"), _stream(stream)),
+           "bppsa_csr_maxpool_data")
     return out
