@@ -438,7 +438,38 @@ def sweep_small(api, args):
 
     out["c3"] = {"set": "L (1034 x 12)", "B": 64, "H": 20, "bppsa_ms_eager": round(_time(bwd_gru), 4),
                  "cudnn_backward_ms": round(cudnn_backward_ms(1034, 64, 20, 12, reps=5, x=gw.x, gru=True), 4)}
+    out["c5"] = sweep_csr(api)
     return out
+
+
+def sweep_csr(api):
+    """Config 5: 97 %-pruned VGG-11 conv stack, B = 16, CSR transposed
+    Jacobians.  Hybrid schedules (u, dl) vs the linear SpMV chain (0, 0)."""
+    import torch
+    import bppsa_workloads as W
+    from paper_1907_10134_b200.vgg import CsrChain
+    w = W.vgg11_workload(B=16, seed=0)
+    relu_in = [torch.from_numpy(r[1]).cuda() for r in w["recs"] if r[0] == "relu"]
+    pools = [torch.from_numpy(r[1]).cuda() for r in w["recs"] if r[0] == "pool"]
+    chain = CsrChain(W.VGG11_CFG, w["weights"], relu_in, pools)
+    seed = torch.from_numpy(w["g"]).cuda()
+    res = {"B": 16, "n": chain.n, "nnz_total": int(sum(int(p[2][-1]) for p in chain.patterns))}
+    for sched in ((0, 0), (1, 2), (2, 3)):
+        t0 = time.perf_counter()
+        plan = chain.plan(*sched)
+        t_plan = time.perf_counter() - t0
+        ws = api.workspace(plan.workspace_size(16, chain.batched))
+        grads = [torch.empty((16, d), device="cuda") for d in plan.dims]
+        ms = _time(lambda: api.csr_scan(plan, chain.data, chain.batched, seed, grads=grads, ws=ws), reps=10)
+        info = plan.info()
+        res[f"u{sched[0]}_dl{sched[1]}"] = {"scan_ms": round(ms, 4), "plan_build_s": round(t_plan, 2),
+                                            "contributions": info["contributions"], "spmv_nnz": info["spmv_nnz"],
+                                            "kernels": info["kernels"], "ws_GB": round(ws.numel() / 1e9, 3)}
+        del ws, plan
+        torch.cuda.empty_cache()
+    res["note"] = ("paper schedule (u, dl) = (3, 4) (P:472) needs 9.1e10 contribution pairs on this pruned "
+                   "VGG-11 (rejected by the plan's cap); (0, 0) is the linear scan = sequential BP with SpMVs")
+    return res
 
 
 # ----------------------------------------------------------------------------- reference arm

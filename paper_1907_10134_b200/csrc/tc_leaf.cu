@@ -12,11 +12,12 @@
 // one-signed 2^-21 bias per product that grows linearly along a chain.
 //
 // A tile = 128 chains = the 64 column chains of block q of sample b and those
-// of sample b+1 (same slots, same length).  A (hi and lo) lives in TMEM next to
-// the accumulator (the TS form of tcgen05.mma): with N = 64 an SS-mode MMA
-// would read 6 KB of operands from shared memory per 32 cycles, above the
-// 128 B/clk shared-memory bandwidth; in TS mode only B (2 KB) comes from
-// shared memory.  CTA = 2 x 8 epilogue warps (thread = chain row x K-half:
+// of sample b+1 (same slots, same length).  A tf32 MMA with M = 128 costs ~60
+// cycles at N = 64 but 64 at N = 128 (profiles/tc_precision.md), so B stacks
+// [W_hi | W_lo] along N and every MMA is a full-rate N = 128 one:
+// D = A_lo [W_hi | W_lo] + A_hi [W_hi | W_lo] (16 MMAs, A_hi / A_lo in TMEM —
+// the TS form, B from shared memory), D[:, :64] + D[:, 64:] summed
+// round-to-nearest in the epilogue (4 products incl. lo*lo, 2 TMEM reads).  CTA = 2 x 8 epilogue warps (thread = chain row x K-half:
 // tcgen05.ld D -> scale by d -> tf32 split -> tcgen05.st A) + 1 MMA-issuer
 // warp; two tiles are in flight so one tile's epilogue overlaps the other
 // tile's MMAs.  Persistent grid, one CTA per SM.
@@ -32,20 +33,24 @@ constexpr int TM = 128;                   // chains per tile (UMMA M)
 constexpr int NSLOT = 2;                  // tiles in flight per CTA
 constexpr int EPI_WARPS = 8;               // per tile: 4 lane quarters x 2 column halves
 constexpr int EPI_THREADS = 32 * EPI_WARPS;
-constexpr int NTHREADS = 32 * (EPI_WARPS * NSLOT + 1);
-constexpr int B_BYTES = TH * TH * 4;      // 16 KB
-constexpr int OFF_B = 0;                                  // [hi,lo]
-constexpr int HCH = 64;                                   // steps staged per chunk
-constexpr int H_BYTES = 2 * HCH * TH * 4;                 // one tile's h slices (2 blocks), 32 KB
-constexpr int OFF_H = OFF_B + 2 * B_BYTES;                // [slot]
+constexpr int NTHREADS = 32 * (EPI_WARPS * NSLOT + 1);   // + one MMA-issuer warp
+constexpr int B_ROWS = 2 * TH;            // B = [W_hi | W_lo] stacked along N
+constexpr int B_BYTES = B_ROWS * TH * 4;  // 32 KB
+constexpr int HCH = 64;                   // steps staged per chunk
+constexpr int H_BYTES = 2 * HCH * TH * 4; // one tile's h slices (2 blocks), 32 KB
+constexpr int OFF_B = 0;
+constexpr int OFF_H = OFF_B + B_BYTES;
 constexpr int OFF_BAR = OFF_H + NSLOT * H_BYTES;          // a_full[2], d_full[2], tmem
 constexpr int SMEM_BYTES = OFF_BAR + 64 + 1024;           // + 1024 B alignment slack
-// TMEM columns: D of slot g at [64g, 64g+64); A_hi / A_lo of slot g at
-// 128 + 128g + {0, 64}
+// TMEM columns of slot g (base 256 g): D = A [W_hi | W_lo] accumulated over
+// A = A_lo then A_hi at [0, 128) (cols 0..63: hh + lh, 64..127: hl + ll),
+// A_hi at [128, 192), A_lo at [192, 256)
 constexpr uint32_t TMEM_COLS = 512;
-// instruction descriptor: D f32, A/B tf32, both K-major, N = 64, M = 128
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TH >> 3) << 17) |
-                           ((uint32_t)(TM >> 4) << 24);
+// instruction descriptors: D f32, A/B tf32, both K-major, M = 128, N = 128 / 64
+constexpr uint32_t idesc(int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+constexpr uint32_t IDESC128 = idesc(128);
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -88,18 +93,19 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+      "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 // A from TMEM (K-major: row = lane, K along 32-bit columns), B from shared memory
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id,
+                                            uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(IDESC), "r"(acc));
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
@@ -140,32 +146,44 @@ __device__ __forceinline__ float tf32_rn(float x) {
 }
 
 // x = d o c for the K-half `kh` (32 columns) of the chain's row, split into
-// tf32 hi / lo and stored to the A_hi / A_lo TMEM columns of this lane;
-// hrow = the block's staged h_t row (shared memory, broadcast reads)
-__device__ __forceinline__ void write_half_tmem(uint32_t t_ahi, uint32_t t_alo, int kh,
-                                               const float* __restrict__ hrow, const float (&c)[32]) {
-  uint32_t hi[32], lo[32];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 h4 = *reinterpret_cast<const float4*>(hrow + 32 * kh + 4 * q);
-    const float hv4[4] = {h4.x, h4.y, h4.z, h4.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float hv = hv4[e];
-      const float x = (1.f - hv * hv) * c[4 * q + e];
-      const float h = tf32_rn(x);
-      hi[4 * q + e] = __float_as_uint(h);
-      lo[4 * q + e] = __float_as_uint(tf32_rn(x - h));   // RN, not the MMA's truncation: no bias
-    }
-  }
-  tmem_st32(t_ahi + 32 * kh, hi);
-  tmem_st32(t_alo + 32 * kh, lo);
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+// tf32 hi (-> this lane's A_hi TMEM columns) and lo (-> the swizzled A_lo tile
+// in shared memory); hrow = the block's staged h_t row (broadcast reads)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(sdst)), "l"(gsrc) : "memory");
 }
+// x = d o c for the K-half `kh` (32 columns) of the chain's row, split into
+// tf32 hi / lo and stored into this lane's A_hi / A_lo TMEM columns;
+// hrow = shared address of the block's staged h_t row (broadcast reads)
+__device__ __forceinline__ void write_half(uint32_t t_ahi, uint32_t t_alo, int kh, uint32_t hrow,
+                                          const float (&c)[32]) {
+  uint32_t v[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 h4 = lds128(hrow + 4u * (32 * kh + 4 * q));
+    const float hv4[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[4 * q + e] = __float_as_uint((1.f - hv4[e] * hv4[e]) * c[4 * q + e]);
+  }
+  uint32_t hi[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) hi[k] = __float_as_uint(tf32_rn(__uint_as_float(v[k])));
+  tmem_st32(t_ahi + 32 * kh, hi);
+#pragma unroll
+  for (int k = 0; k < 32; ++k)   // lo rounded to nearest (not the MMA's truncation: no bias)
+    v[k] = __float_as_uint(tf32_rn(__uint_as_float(v[k]) - __uint_as_float(hi[k])));
+  tmem_st32(t_alo + 32 * kh, v);
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
@@ -186,14 +204,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
 
   // ---- setup: B = W (hi / lo), barriers, TMEM
   for (int e = threadIdx.x; e < TH * TH; e += NTHREADS) {
-    const int n = e / TH, k = e % TH;               // B[n][k] = W[k][n]
+    const int n = e / TH, k = e % TH;               // B[n][k] = W[k][n]: rows 0..63 hi, 64..127 lo
     const float w = __ldg(a.W + (long long)k * TH + n);
     const float hi = tf32_rn(w);
-    const uint32_t off = sw_off(n, k, TH);
-    *reinterpret_cast<float*>(smem + OFF_B + off) = hi;
-    *reinterpret_cast<float*>(smem + OFF_B + B_BYTES + off) = tf32_rn(w - hi);
+    *reinterpret_cast<float*>(smem + OFF_B + sw_off(n, k, B_ROWS)) = hi;
+    *reinterpret_cast<float*>(smem + OFF_B + sw_off(TH + n, k, B_ROWS)) = tf32_rn(w - hi);
   }
-  if (warp == EPI_WARPS * NSLOT) {
+  const int mma_warp = EPI_WARPS * NSLOT;
+  if (warp == mma_warp) {
     if (lane == 0) {
       for (int s = 0; s < NSLOT; ++s) {
         mbar_init(&a_full[s], EPI_THREADS);
@@ -212,61 +230,58 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == EPI_WARPS * NSLOT) {
-    // ================= MMA issuer (one elected thread) =================
-    uint32_t ph[NSLOT] = {0, 0};
-    const uint32_t b_hi = su32(smem + OFF_B), b_lo = b_hi + B_BYTES;
-    for (long long pr = blockIdx.x; 2 * pr < ntiles; pr += gridDim.x) {
-      long long len[NSLOT];
+  if (warp == mma_warp) {
+    // ================= MMA issuer: both tile slots, 16 full-rate N = 128 MMAs per step =====
+    uint32_t pha[NSLOT] = {0, 0};
+    const uint32_t bb = su32(smem + OFF_B);
+    long long len[NSLOT] = {0, 0}, done[NSLOT] = {0, 0}, tau[NSLOT];
+    for (int sl = 0; sl < NSLOT; ++sl) tau[sl] = 2 * (long long)blockIdx.x + sl;
+    auto tile_len = [&](long long t) -> long long {
+      if (t >= ntiles) return 0;
+      const long long q = q0 + t / nbp;
+      return min(q * C + C, S) - q * C;
+    };
+    for (int sl = 0; sl < NSLOT; ++sl) len[sl] = tile_len(tau[sl]);
+    while (len[0] > 0 || len[1] > 0) {
       for (int sl = 0; sl < NSLOT; ++sl) {
-        const long long tau = 2 * pr + sl;
-        const long long q = q0 + tau / nbp;
-        len[sl] = (tau < ntiles) ? (min(q * C + C, S) - q * C) : 0;
-      }
-      const long long steps = max(len[0], len[1]);
-      for (long long st = 0; st < steps; ++st) {
-        for (int sl = 0; sl < NSLOT; ++sl) {
-          if (st >= len[sl]) continue;
-          mbar_wait(&a_full[sl], ph[sl]);
-          ph[sl] ^= 1;
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a_hi = tmem + 128 + 128 * sl, a_lo = a_hi + 64;
-            // correction products first (hi*lo, lo*hi), then hi*hi: the tensor
-            // core truncates every accumulation, so adding the small terms while
-            // the accumulator is still small cuts the one-signed bias per step
-            // from ~13 to ~5 ulp (scripts/tc_unit.cu, profiles/tc_precision.md)
+        if (len[sl] == 0) continue;
+        mbar_wait(&a_full[sl], pha[sl]);
+        pha[sl] ^= 1;
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t d = tmem + 256 * sl, a_hi = d + 128, a_lo = d + 192;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
-              const int pq = (i + 1) % 3;            // 1: hi*lo, 2: lo*hi, 0: hi*hi
-              const uint32_t aa = (pq == 2) ? a_lo : a_hi, bb = (pq == 1) ? b_lo : b_hi;
+          for (int pq = 0; pq < 2; ++pq) {              // A_lo first: small terms while D is small
+            const uint32_t aa = pq == 0 ? a_lo : a_hi;
 #pragma unroll
-              for (int kk = 0; kk < TH / 8; ++kk) {
-                const uint32_t boff = (uint32_t)((kk >> 2) * TH * 128 + (kk & 3) * 32);
-                mma_tf32_ts(tmem + sl * TH, aa + 8 * kk, sdesc(bb + boff), (i | kk) != 0);
-              }
+            for (int kk = 0; kk < TH / 8; ++kk) {
+              const uint32_t boff = (uint32_t)((kk >> 2) * B_ROWS * 128 + (kk & 3) * 32);
+              mma_tf32_ts(d, aa + 8 * kk, sdesc(bb + boff), IDESC128, (pq | kk) != 0);
             }
-            mma_commit(&d_full[sl]);
           }
-          __syncwarp();
+          mma_commit(&d_full[sl]);
+        }
+        __syncwarp();
+        if (++done[sl] == len[sl]) {
+          done[sl] = 0;
+          tau[sl] += 2 * (long long)gridDim.x;
+          len[sl] = tile_len(tau[sl]);
         }
       }
     }
   } else {
-    // ===== epilogue of tile slot g: 8 warps, thread = (chain row, K-half) =====
+    // ===== tile slot g: 8 warps, thread = (chain row, K-half) =====
     const int g = warp / EPI_WARPS, wl = warp % EPI_WARPS;
     const int row = (wl & 3) * 32 + lane;                   // TMEM lane / A row (lane quarter = warp % 4)
     const int kh = wl >> 2;                                 // column half of D / K-half of A
     const int et = wl * 32 + lane;                          // 0 .. EPI_THREADS-1
-    const uint32_t lane_base = tmem + ((uint32_t)((wl & 3) * 32) << 16);
-    const uint32_t taddr = lane_base + g * TH + 32 * kh;             // D, this thread's 32 columns
-    const uint32_t t_ahi = lane_base + 128 + 128 * g, t_alo = t_ahi + 64;
+    const uint32_t lane_base = tmem + ((uint32_t)((wl & 3) * 32) << 16) + 256 * g;
+    const uint32_t t_d = lane_base + 32 * kh, t_ahi = lane_base + 128, t_alo = lane_base + 192;
     float* hs = reinterpret_cast<float*>(smem + OFF_H + g * H_BYTES);   // [2 blocks][HCH][64]
+    const uint32_t hs_s = su32(hs);
     uint32_t ph = 0;
     const long long rowB = (long long)B * TH;
-    for (long long pr = blockIdx.x; 2 * pr < ntiles; pr += gridDim.x) {
-      const long long tau = 2 * pr + g;
-      if (tau >= ntiles) continue;
+    for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
       const long long q = q0 + tau / nbp;
       const int bp = (int)(tau % nbp);
       const int b = bp * 2 + (row >> 6);
@@ -281,25 +296,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
         // stage the h_t rows of this chunk for both blocks of the tile (cp.async)
         named_bar(1 + g, EPI_THREADS);             // previous chunk fully consumed
         for (int e = et; e < 2 * n * 16; e += EPI_THREADS) {
-          const int bb = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
-          float* dst = hs + (bb * HCH + st) * TH + ch * 4;
-          const int bs = bp * 2 + bb;
+          const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+          float* dst = hs + (bb2 * HCH + st) * TH + ch * 4;
+          const int bs = bp * 2 + bb2;
           if (bs < B)
             cp_async16(dst, a.h + (long long)a.seg.time_of(sc + st) * rowB + (long long)bs * TH + ch * 4);
           else
-            *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         named_bar(1 + g, EPI_THREADS);
-        const float* hb = hs + (row >> 6) * HCH * TH;
+        const uint32_t hb = hs_s + 4u * ((row >> 6) * HCH * TH);
         for (int st = 0; st < n; ++st) {
-          write_half_tmem(t_ahi, t_alo, kh, hb + st * TH, c);
+          write_half(t_ahi, t_alo, kh, hb + 4u * st * TH, c);
           tc_fence_before();
           mbar_arrive(&a_full[g]);
           mbar_wait(&d_full[g], ph);
           ph ^= 1;
           tc_fence_after();
-          tmem_ld32(taddr, c);
+          float t[32];                           // c = (hh + lh) + (hl + ll), round-to-nearest
+          tmem_ld32(t_d, c);
+          tmem_ld32(t_d + 64, t);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) c[k] += t[k];
         }
       }
       if (ok) {
