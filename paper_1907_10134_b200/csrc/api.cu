@@ -298,7 +298,12 @@ bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Pla
     cudaError_t e;
     tr.begin(st);
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
-      e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st);
+      // tcgen05 walk: many short chains (the linear scan's single long chain per
+      // sample stays on the CUDA cores; so do single-block segments)
+      if (use_tensor_leaf(j, p.leaf_impl) && nblk >= 2 && Cl >= 8)
+        e = launch_tc_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st);
+      else
+        e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st);
     } else if (l == 0) {
       const MatAcc A = dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed);
       e = launch_walk_down(A, H, B, p.n[0], Cl, head, carry, nblk, grad_h, 1, seg, grad_init, st);

@@ -74,6 +74,8 @@ cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n
 // same on the tensor cores (tcgen05, 3xTF32): RNN, H == 64, matrix blocks q in [q0, n_out)
 cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
                               int num_sms, cudaStream_t st);
+cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
+                                float* grad_init, int num_sms, cudaStream_t st);
 // level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable
 cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry,
                              long long nblk, float* grad_h, float* grad_init,

@@ -336,6 +336,190 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Level-0 DOWN-sweep on the tensor cores: every block (b, q) is a vector chain
+// walked from its carry (exclusive prefix; the seed for the head block):
+//     grad_h[t(s)] = v;  v <- J_{t(s)}^T v = W^T (d_t o v)
+// A tile = 128 chains of arbitrary (b, q) (each with its own time window), so
+// each thread streams its own h half-row: a private 2-stage cp.async ring, no
+// barriers.  Same MMA scheme as the up-sweep (16 N = 128 MMAs per step).
+// ---------------------------------------------------------------------------
+constexpr int OFF_RING = OFF_B + B_BYTES;                     // [slot][row][kh][2 stages][32 floats]
+constexpr int RING_BYTES = NSLOT * TM * 2 * 2 * 32 * 4;       // 128 KB
+constexpr int OFF_BAR_D = OFF_RING + RING_BYTES;
+constexpr int SMEM_BYTES_D = OFF_BAR_D + 64 + 1024;
+
+__global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_down_kernel(LeafArgs a, int C, const float* __restrict__ carry,
+                                                                   long long nblk, float* __restrict__ grad_h,
+                                                                   float* __restrict__ grad_init) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR_D);
+  uint64_t* d_full = a_full + NSLOT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nchains = (long long)B * nblk;
+  const long long ntiles = (nchains + TM - 1) / TM;
+
+  for (int e = threadIdx.x; e < TH * TH; e += NTHREADS) {
+    const int n = e / TH, k = e % TH;               // B[n][k] = W[k][n]: rows 0..63 hi, 64..127 lo
+    const float w = __ldg(a.W + (long long)k * TH + n);
+    const float hi = tf32_rn(w);
+    *reinterpret_cast<float*>(smem + OFF_B + sw_off(n, k, B_ROWS)) = hi;
+    *reinterpret_cast<float*>(smem + OFF_B + sw_off(TH + n, k, B_ROWS)) = tf32_rn(w - hi);
+  }
+  const int mma_warp = EPI_WARPS * NSLOT;
+  if (warp == mma_warp) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) {
+        mbar_init(&a_full[s], EPI_THREADS);
+        mbar_init(&d_full[s], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == mma_warp) {
+    uint32_t pha[NSLOT] = {0, 0};
+    const uint32_t bb = su32(smem + OFF_B);
+    long long done[NSLOT] = {0, 0}, tau[NSLOT];
+    bool live[NSLOT];
+    for (int sl = 0; sl < NSLOT; ++sl) {
+      tau[sl] = 2 * (long long)blockIdx.x + sl;
+      live[sl] = tau[sl] < ntiles;
+    }
+    while (live[0] || live[1]) {
+      for (int sl = 0; sl < NSLOT; ++sl) {
+        if (!live[sl]) continue;
+        mbar_wait(&a_full[sl], pha[sl]);
+        pha[sl] ^= 1;
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t d = tmem + 256 * sl, a_hi = d + 128, a_lo = d + 192;
+#pragma unroll
+          for (int pq = 0; pq < 2; ++pq) {
+            const uint32_t aa = pq == 0 ? a_lo : a_hi;
+#pragma unroll
+            for (int kk = 0; kk < TH / 8; ++kk) {
+              const uint32_t boff = (uint32_t)((kk >> 2) * B_ROWS * 128 + (kk & 3) * 32);
+              mma_tf32_ts(d, aa + 8 * kk, sdesc(bb + boff), IDESC128, (pq | kk) != 0);
+            }
+          }
+          mma_commit(&d_full[sl]);
+        }
+        __syncwarp();
+        if (++done[sl] == C) {
+          done[sl] = 0;
+          tau[sl] += 2 * (long long)gridDim.x;
+          live[sl] = tau[sl] < ntiles;
+        }
+      }
+    }
+  } else {
+    const int g = warp / EPI_WARPS, wl = warp % EPI_WARPS;
+    const int row = (wl & 3) * 32 + lane;
+    const int kh = wl >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)((wl & 3) * 32) << 16) + 256 * g;
+    const uint32_t t_d = lane_base + 32 * kh, t_ahi = lane_base + 128, t_alo = lane_base + 192;
+    float* ring = reinterpret_cast<float*>(smem + OFF_RING) + ((g * TM + row) * 2 + kh) * 2 * 32;
+    const uint32_t ring_s = su32(ring);
+    uint32_t ph = 0;
+    const long long rowB = (long long)B * TH;
+    for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+      const long long id = tau * TM + row;
+      const bool valid = id < nchains;
+      const int b = valid ? (int)(id / nblk) : 0;
+      const long long q = valid ? id % nblk : 0;
+      const bool head = a.seg.head && q == 0;
+      const long long s_start = head ? 1 : q * C, s1 = min(q * C + C, S);
+      const long long len = valid ? s1 - s_start : 0;
+      const bool total = valid && grad_init != nullptr && s1 == S;
+      float c[32];
+      const float* src0 = head ? a.seed + (long long)b * TH : carry + ((long long)b * nblk + q) * TH;
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(src0 + 32 * kh) + k4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        c[4 * k4] = v.x; c[4 * k4 + 1] = v.y; c[4 * k4 + 2] = v.z; c[4 * k4 + 3] = v.w;
+      }
+      auto prefetch = [&](long long st) {      // h row of step st into ring stage st & 1
+        if (st < len) {
+          const float* hp = a.h + (long long)a.seg.time_of(s_start + st) * rowB + (long long)b * TH + 32 * kh;
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) cp_async16(ring + (st & 1) * 32 + 4 * k4, hp + 4 * k4);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      prefetch(0);
+      for (long long st = 0; st < C; ++st) {
+        prefetch(st + 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        const bool active = st < len;
+        float dv[32];
+        if (active) {
+          float* gp = grad_h + (long long)a.seg.time_of(s_start + st) * rowB + (long long)b * TH + 32 * kh;
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4)
+            reinterpret_cast<float4*>(gp)[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) {
+            const float4 h4 = lds128(ring_s + 4u * ((st & 1) * 32 + 4 * k4));
+            dv[4 * k4] = 1.f - h4.x * h4.x; dv[4 * k4 + 1] = 1.f - h4.y * h4.y;
+            dv[4 * k4 + 2] = 1.f - h4.z * h4.z; dv[4 * k4 + 3] = 1.f - h4.w * h4.w;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) dv[k] = 0.f;
+        }
+        uint32_t v[32], hi[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float x = dv[k] * c[k];
+          const float h = tf32_rn(x);
+          hi[k] = __float_as_uint(h);
+          v[k] = __float_as_uint(tf32_rn(x - h));
+        }
+        tmem_st32(t_ahi + 32 * kh, hi);
+        tmem_st32(t_alo + 32 * kh, v);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&a_full[g]);
+        mbar_wait(&d_full[g], ph);
+        ph ^= 1;
+        tc_fence_after();
+        float t[32];
+        tmem_ld32(t_d, c);
+        tmem_ld32(t_d + 64, t);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) c[k] += t[k];
+        if (total && st == len - 1) {          // inclusive extra: J_{t(S-1)}^T grad_h[t(S-1)]
+          float4* dst = reinterpret_cast<float4*>(grad_init + (long long)b * TH + 32 * kh);
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+        }
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == EPI_WARPS * NSLOT) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
 }  // namespace
 
 // Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.
@@ -352,6 +536,21 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
   const int grid = (int)std::min<long long>(pairs, num_sms);
   if (grid <= 0) return cudaSuccess;
   tc_leaf_up_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+  return cudaGetLastError();
+}
+
+// Level-0 down-walk of an RNN H = 64 segment on the tensor cores.
+cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
+                                float* grad_init, int num_sms, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_leaf_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_D);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
+  const int grid = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
+  tc_leaf_down_kernel<<<grid, NTHREADS, SMEM_BYTES_D, st>>>(a, C, carry, nblk, grad_h, grad_init);
   return cudaGetLastError();
 }
 

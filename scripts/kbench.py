@@ -10,8 +10,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1907_10134_b200 import api  # noqa: E402
 
-CFG = {"c4": (1 << 20, 16, 64, 64, 32), "c1": (1000, 16, 20, 8, 8), "c2": (30000, 16, 20, 16, 16),
-       "c4s": (1 << 18, 16, 64, 64, 32), "c4b128": (1 << 20, 16, 64, 128, 32), "c4b128c64": (1 << 20, 16, 64, 128, 64),
+CFG = {"c4": (1 << 20, 16, 64, 128, 32), "c1": (1000, 16, 20, 8, 8), "c2": (30000, 16, 20, 16, 16),
+       "c4s": (1 << 18, 16, 64, 128, 32), "c4b128": (1 << 20, 16, 64, 128, 32), "c4b128c64": (1 << 20, 16, 64, 128, 64),
        "c4c64": (1 << 20, 16, 64, 64, 64)}
 
 
