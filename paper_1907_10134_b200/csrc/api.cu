@@ -559,8 +559,10 @@ bppsa_status bppsa_weight_grads_workspace_size(int T, int B, int H, int I, size_
   if (!bytes) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bytes is NULL");
   if (T < 1 || B < 1 || H < 1 || H > BPPSA_MAX_H || I < 0) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad shape");
   if (!wgrad_supported(H, I)) return fail(BPPSA_ERR_NOT_SUPPORTED, "weight gradients need I + 1 <= 64");
-  const long long P = wgrad_parts((long long)T * B);
-  *bytes = align_up((size_t)P * 4 * H * (H + I + 1) * sizeof(float));   // GRU needs NA = 4H
+  const long long rows = (long long)T * B;
+  long long slabs = 4 * wgrad_parts(rows);                               // GRU needs NA = 4H
+  if (tc_wgrad_applies(H, I, rows)) slabs = std::max(slabs, tc_wgrad_parts(rows));
+  *bytes = align_up((size_t)slabs * H * (H + I + 1) * sizeof(float));
   return BPPSA_OK;
 }
 
@@ -580,9 +582,20 @@ bppsa_status bppsa_weight_grads_rnn(int T, int B, int H, int I, const float* x, 
   REQUIRE_DEV(db, "db");
   if (h_init) REQUIRE_DEV(h_init, "h_init");
   if (ws_bytes < need || !is_device_ptr(ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace too small or not device memory");
-  const long long P = wgrad_parts((long long)T * B);
-  cudaError_t e = launch_wgrad_rnn(T, B, H, I, x, h, h_init, grad_h, dW_ih, dW_hh, db, static_cast<float*>(ws), P,
-                                   (cudaStream_t)stream);
+  const long long rows = (long long)T * B;
+  cudaError_t e;
+  auto a16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };    // cp.async.bulk sources
+  if (tc_wgrad_applies(H, I, rows) && a16(h) && a16(grad_h) && a16(h_init) && (I == 0 || a16(x))) {
+    // tensor-core GEMM over K = T*B (tc_wgrad.cu)
+    e = launch_tc_wgrad_partials(B, I, x, h, h_init, grad_h, rows, static_cast<float*>(ws), num_sms(),
+                                 (cudaStream_t)stream);
+    if (e == cudaSuccess)
+      e = launch_wgrad_reduce_rnn(static_cast<float*>(ws), tc_wgrad_parts(rows), H, I, dW_ih, dW_hh, db,
+                                  (cudaStream_t)stream);
+  } else {
+    e = launch_wgrad_rnn(T, B, H, I, x, h, h_init, grad_h, dW_ih, dW_hh, db, static_cast<float*>(ws),
+                         wgrad_parts(rows), (cudaStream_t)stream);
+  }
   return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "weight grads rnn");
 }
 

@@ -1,0 +1,393 @@
+// tc_wgrad.cu — RNN weight gradients (eqn:update_param, tied over
+// time) as a tensor-core GEMM over K = T*B rows, H = 64:
+//     dW_hh = sum_rows delta_row h_{row-B}^T,   delta = (1 - h^2) o grad_h
+// Per 32-row chunk one contraction D[128 x 128] += A[128 x 32] B[128 x 32]^T
+// with A = [delta_hi ; delta_lo] (M = 128, rows = i), B = [hp_hi | hp_lo]
+// (N = 128, rows = k): the four quadrants of D are the products hh, hl, lh, ll
+// (4xTF32) and every MMA is a full-rate N = 128 one.
+//
+// Roles (320 threads, one CTA per SM):
+//   warp 8, lane 0   stages chunks with cp.async.bulk (a 32-row chunk of h, g
+//                    and h_prev is one contiguous 8 KB run each; NS stages
+//                    ahead, mbarrier complete_tx);
+//   warp 9, lane 0   issues the MMAs (NBUF operand buffers in flight);
+//   warps 0..7       converters: warp w owns TMEM lanes 32*(w&3).. (= A rows)
+//                    and K columns [16*(w>>2), +16) of the chunk.  Each thread
+//                    forms delta and the hi/lo splits for its 16 rows, stores
+//                    A with tcgen05.st and its B row into the SW128 tile.
+// Synchronisation is mbarrier-only: full/empty per stage, a_full/freeb per
+// A/B buffer.  The accumulator is flushed into fp32 registers every FLUSH
+// chunks so the tensor core's truncating accumulation never spans more than
+// FLUSH*4 MMAs.  dW_ih and db accumulate on the CUDA cores.  Rows are split
+// into fixed parts (a function of K only); each part writes four slabs
+// (lane half x column half of D) and wgrad_reduce_rnn sums parts*4 slabs in a
+// fixed order (deterministic).
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace bppsa {
+namespace {
+
+constexpr int H = 64, KC = 32, MROWS = 128, NCONV = 256, NTH = NCONV + 64;   // + loader warp + MMA warp
+constexpr int FLUSH = 32;                           // chunks per accumulation window
+constexpr long long PART_ROWS = 16384;              // rows per part (512 chunks)
+constexpr int MAXI = 4;
+constexpr int NS = 6;                               // staging depth (chunks)
+constexpr int NBUF = 4;                             // A (TMEM) / B (SMEM) operand buffers
+constexpr int ROW_BYTES = H * 4;
+constexpr int SB = 3 * KC * ROW_BYTES;              // h, g, h_prev rows: 24 KB per stage
+constexpr int XB = KC * MAXI * 4;                   // x rows: 512 B per stage
+constexpr int B_BYTES = MROWS * KC * 4;             // 16 KB per B buffer
+constexpr int OFF_STAGE = 0;
+constexpr int OFF_BT = NS * SB;                     // 1024-B aligned (SW128 tiles)
+constexpr int OFF_X = OFF_BT + NBUF * B_BYTES;
+constexpr int OFF_BAR = OFF_X + NS * XB;
+constexpr int SMEM = OFF_BAR + (2 * NS + 2 * NBUF + 2) * 8 + 1024;
+static_assert(OFF_BT % 1024 == 0, "SW128 B tiles must be 1024-B aligned");
+constexpr uint32_t TMEM_COLS = 256;                 // D at [0,128), A buffer b at [128+32b, +32)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                           ((uint32_t)(MROWS >> 4) << 24);
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t sw_off(int row, int k) {   // K-major SW128, K < 32
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((k & 31) >> 2) ^ (row & 7)) << 4) + ((k & 3) << 2));
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(c));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
+                   bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ float lds(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+// hi = x rounded to the nearest tf32 (ties away), as an fp32 value with the 13
+// low mantissa bits clear; lo = x - hi is exact in fp32 and |lo| <= 2^-11 |x|.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TWArgs {
+  int B, I;
+  const float *x, *h, *h_init, *g;
+  long long rows;
+  float* ws;            // partials [P][4][H][H + I + 1]
+  long long nparts;
+};
+
+struct ChunkIter {      // walks this CTA's chunks: parts blockIdx.x + j*gridDim.x
+  long long part, c, cg, r0, r1, nch;
+  __device__ void start(long long p, long long rows) {
+    part = p;
+    c = 0;
+    cg = 0;
+    set(rows);
+  }
+  __device__ void set(long long rows) {
+    r0 = part * PART_ROWS;
+    r1 = min(r0 + PART_ROWS, rows);
+    nch = (r1 - r0 + KC - 1) / KC;
+  }
+  __device__ void next(long long rows) {
+    ++cg;
+    if (++c == nch) {
+      part += gridDim.x;
+      c = 0;
+      set(rows);
+    }
+  }
+};
+
+struct Bars {
+  uint32_t b0;
+  __device__ uint32_t full(int s) const { return b0 + 8u * s; }
+  __device__ uint32_t empty(int s) const { return b0 + 8u * (NS + s); }
+  __device__ uint32_t a_full(int b) const { return b0 + 8u * (2 * NS + b); }
+  __device__ uint32_t freeb(int b) const { return b0 + 8u * (2 * NS + NBUF + b); }
+};
+
+// One chunk's rows for this thread: A values (delta hi or lo) and B values
+// (h_prev hi or lo) of rows 16*grp .. 16*grp+15; rows >= n are zero, h_prev
+// rows < nlow (before h_0 with no h_init) are zero.
+template <bool LO, bool FULL>
+__device__ __forceinline__ void convert_rows(uint32_t st, const float* xs, int I, int grp, int n, int nlow,
+                                             float (&av)[16], float (&bv)[16], float& dbias, float (&dih)[MAXI]) {
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) {
+    const int r = 16 * grp + rr;
+    const float hv = lds(st + r * ROW_BYTES), gv = lds(st + (KC + r) * ROW_BYTES),
+                pv = lds(st + (2 * KC + r) * ROW_BYTES);
+    float d = (1.f - hv * hv) * gv, hp = pv;
+    if (!FULL) {
+      d = r < n ? d : 0.f;
+      hp = (r < n && r >= nlow) ? hp : 0.f;
+    }
+    const float dhi = tf32_hi(d), phi = tf32_hi(hp);
+    av[rr] = LO ? d - dhi : dhi;
+    bv[rr] = LO ? hp - phi : phi;
+    if (!LO) {
+      dbias += d;
+#pragma unroll
+      for (int j = 0; j < MAXI; ++j)
+        if (j < I) {
+          float xv = xs[r * I + j];
+          if (!FULL) xv = r < n ? xv : 0.f;
+          dih[j] = fmaf(d, xv, dih[j]);
+        }
+    }
+  }
+}
+
+template <bool LO>
+__device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, const char* smem, Bars br, uint32_t tmem,
+                                           int warp, int lane) {
+  const int wq = warp & 3, grp = warp >> 2;
+  const int m = 32 * wq + lane, i = m & 63;
+  const uint32_t tl = tmem + ((uint32_t)(32 * wq) << 16);
+  const int NB = H + w.I + 1;
+  ChunkIter it;
+  it.start(blockIdx.x, w.rows);
+  while (it.part < w.nparts) {
+    float acc[64];
+#pragma unroll
+    for (int k = 0; k < 64; ++k) acc[k] = 0.f;
+    float dbias = 0.f, dih[MAXI];
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j) dih[j] = 0.f;
+    auto flush = [&]() {
+      float t[32];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        tmem_ld32(tl + 64 * grp + 32 * q, t);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[32 * q + k] += t[k];
+      }
+    };
+    const long long part = it.part, nch = it.nch;
+    for (long long c = 0; c < nch; ++c) {
+      const long long cg = it.cg;
+      const int b = (int)(cg % NBUF), s = (int)(cg % NS);
+      const long long rb = it.r0 + c * KC;
+      const int n = (int)min((long long)KC, it.r1 - rb);
+      const int nlow = w.h_init ? 0 : (int)max(0ll, min((long long)KC, (long long)w.B - rb));
+      mbar_wait(br.full(s), (uint32_t)((cg / NS) & 1));
+      const uint32_t st = s0 + OFF_STAGE + s * SB + 4u * i;
+      const float* xs = reinterpret_cast<const float*>(smem + OFF_X + s * XB);
+      float av[16], bv[16];
+      if (n == KC && nlow == 0) convert_rows<LO, true>(st, xs, w.I, grp, n, nlow, av, bv, dbias, dih);
+      else convert_rows<LO, false>(st, xs, w.I, grp, n, nlow, av, bv, dbias, dih);
+      mbar_arrive(br.empty(s));
+      if (c > 0 && c % FLUSH == 0) {           // window boundary: chunk cg-1 done, read D
+        mbar_wait(br.freeb((int)((cg - 1) % NBUF)), (uint32_t)(((cg - 1) / NBUF) & 1));
+        tc_after();
+        flush();
+      } else if (c >= NBUF) {                  // operand buffer b was last read by chunk cg-NBUF
+        mbar_wait(br.freeb(b), (uint32_t)(((cg - NBUF) / NBUF) & 1));
+        tc_after();
+      }
+      tmem_st16(tl + 128 + 32 * b + 16 * grp, av);
+      const uint32_t bt = s0 + OFF_BT + b * B_BYTES;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        sts4(bt + sw_off(m, 16 * grp + 4 * q), bv[4 * q], bv[4 * q + 1], bv[4 * q + 2], bv[4 * q + 3]);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tc_before();
+      mbar_arrive(br.a_full(b));
+      it.next(w.rows);
+    }
+    // last window of the part
+    const long long cl = it.cg - 1;
+    mbar_wait(br.freeb((int)(cl % NBUF)), (uint32_t)((cl / NBUF) & 1));
+    tc_after();
+    flush();
+    tc_before();
+    const int slab = (LO ? 2 : 0) + grp;
+    float* dst = w.ws + ((part * 4 + slab) * (long long)H + i) * NB;
+#pragma unroll
+    for (int k = 0; k < 64; ++k) dst[k] = acc[k];
+#pragma unroll
+    for (int j = 0; j < MAXI; ++j)
+      if (j < w.I) dst[H + j] = LO ? 0.f : dih[j];
+    dst[H + w.I] = LO ? 0.f : dbias;
+  }
+}
+
+__global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t s0 = su32(smem);
+  const Bars br{s0 + OFF_BAR};
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 8 * (2 * NS + 2 * NBUF));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 9) {
+    if (lane == 0) {
+      for (int s = 0; s < NS; ++s) {
+        mbar_init(br.full(s), 1);
+        mbar_init(br.empty(s), NCONV);
+      }
+      for (int b = 0; b < NBUF; ++b) {
+        mbar_init(br.a_full(b), NCONV);
+        mbar_init(br.freeb(b), 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      // ===== loader: NS chunks ahead of the converters =====
+      ChunkIter ld;
+      ld.start(blockIdx.x, w.rows);
+      const long long B = w.B;
+      while (ld.part < w.nparts) {
+        const int s = (int)(ld.cg % NS);
+        if (ld.cg >= NS) mbar_wait(br.empty(s), (uint32_t)((ld.cg / NS - 1) & 1));
+        const long long rb = ld.r0 + ld.c * KC;
+        const int n = (int)min((long long)KC, ld.r1 - rb);
+        const uint32_t st = s0 + OFF_STAGE + s * SB;
+        // h_prev rows: [rb, rb+nA) come from h_init (rows < B), the rest from h
+        const int nA = (int)max(0ll, min((long long)n, B - rb));
+        uint32_t tx = 2u * n * ROW_BYTES + (uint32_t)(n - nA) * ROW_BYTES;
+        if (w.h_init) tx += (uint32_t)nA * ROW_BYTES;
+        const float* xs = w.x + rb * w.I;
+        const uint32_t xbytes = (uint32_t)(n * w.I * 4);
+        const bool xbulk = w.I > 0 && (xbytes & 15) == 0;
+        if (xbulk) tx += xbytes;
+        else if (w.I > 0) {     // tail chunk with an odd byte count: plain copies before the arrive
+          float* xd = reinterpret_cast<float*>(smem + OFF_X + s * XB);
+          for (int e = 0; e < n * w.I; ++e) xd[e] = xs[e];
+        }
+        mbar_expect_tx(br.full(s), tx);
+        bulk_g2s(st, w.h + rb * H, (uint32_t)n * ROW_BYTES, br.full(s));
+        bulk_g2s(st + KC * ROW_BYTES, w.g + rb * H, (uint32_t)n * ROW_BYTES, br.full(s));
+        if (nA > 0 && w.h_init)
+          bulk_g2s(st + 2 * KC * ROW_BYTES, w.h_init + rb * H, (uint32_t)nA * ROW_BYTES, br.full(s));
+        if (n > nA)
+          bulk_g2s(st + 2 * KC * ROW_BYTES + nA * ROW_BYTES, w.h + (rb + nA - B) * H, (uint32_t)(n - nA) * ROW_BYTES,
+                   br.full(s));
+        if (xbulk) bulk_g2s(s0 + OFF_X + s * XB, xs, xbytes, br.full(s));
+        ld.next(w.rows);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      ChunkIter mm;
+      mm.start(blockIdx.x, w.rows);
+      while (mm.part < w.nparts) {
+        const int b = (int)(mm.cg % NBUF);
+        mbar_wait(br.a_full(b), (uint32_t)((mm.cg / NBUF) & 1));
+        tc_after();
+        const uint32_t bt = s0 + OFF_BT + b * B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < KC / 8; ++kk) {
+          const uint32_t acc = !((mm.c % FLUSH) == 0 && kk == 0);
+          asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                       " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
+                       "r"(tmem + 128 + 32 * b + 8 * kk), "l"(sdesc(bt + 32 * kk)), "r"(IDESC), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         br.freeb(b)) : "memory");
+        mm.next(w.rows);
+      }
+    }
+    __syncwarp();
+  } else if ((warp & 3) >= 2) {
+    converters<true>(w, s0, smem, br, tmem, warp, lane);
+  } else {
+    converters<false>(w, s0, smem, br, tmem, warp, lane);
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace
+
+long long tc_wgrad_parts(long long rows) { return 4 * ((rows + PART_ROWS - 1) / PART_ROWS); }   // slabs
+bool tc_wgrad_applies(int H_, int I, long long rows) {
+  static const int force = [] { const char* e = getenv("BPPSA_FORCE_TC_WGRAD"); return e ? atoi(e) : 0; }();
+  if (H_ != H || I > MAXI) return false;
+  return force == 1 ? true : (force == 2 ? false : rows >= 8 * PART_ROWS);   // debug override (tests)
+}
+
+cudaError_t launch_tc_wgrad_partials(int B, int I, const float* x, const float* h, const float* h_init,
+                                     const float* grad_h, long long rows, float* ws, int num_sms, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  TWArgs a{B, I, x, h, h_init, grad_h, rows, ws, (rows + PART_ROWS - 1) / PART_ROWS};
+  const int grid = (int)std::min<long long>(a.nparts, num_sms);
+  tc_wgrad_kernel<<<grid, NTH, SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace bppsa

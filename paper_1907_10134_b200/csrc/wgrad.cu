@@ -156,49 +156,85 @@ __global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __res
   }
 }
 
-// Sum the parts in order p = 0..P-1 for the requested (a, c) element.
-__device__ __forceinline__ float sum_parts(const float* ws, long long P, int NA, int NB, int a, int c) {
+// Reduction of the partial slabs: block = 32 outputs x 32 part lanes; lane pl
+// sums parts pl, pl+32, ... in order, then a fixed shared-memory tree over pl.
+// The summation order depends on P only (deterministic), loads are coalesced
+// across outputs.
+struct RedMap {
+  int gru, H, I, NA, NB;
+  float *o0, *o1, *o2, *o3;   // RNN: dW_hh, dW_ih, db;  GRU: dW_hh3, dW_ih3, db_ih3, db_hh3
+};
+
+__device__ __forceinline__ float* map_out(const RedMap& m, int e, int& a, int& c) {
+  const int H = m.H, I = m.I;
+  if (!m.gru) {
+    a = e / m.NB;
+    c = e % m.NB;
+    return c < H ? m.o0 + a * H + c : (c < H + I ? m.o1 + a * I + (c - H) : m.o2 + a);
+  }
+  const int n_hh = 3 * H * H, n_ih = 3 * H * I;
+  if (e < n_hh) {
+    const int row = e / H, k = e % H, g = row / H, i = row % H;
+    a = (g == 2 ? 3 : g) * H + i;                      // [dR; dZ; dM] h_prev^T
+    c = k;
+    return m.o0 + e;
+  }
+  if (e < n_hh + n_ih) {
+    const int f = e - n_hh;
+    a = f / I;                                          // [dR; dZ; dN] x^T
+    c = H + f % I;
+    return m.o1 + f;
+  }
+  if (e < n_hh + n_ih + 3 * H) {
+    a = e - n_hh - n_ih;
+    c = H + I;
+    return m.o2 + a;
+  }
+  const int row = e - n_hh - n_ih - 3 * H, g = row / H, i = row % H;
+  a = (g == 2 ? 3 : g) * H + i;
+  c = H + I;
+  return m.o3 + row;
+}
+
+__global__ void __launch_bounds__(1024) wgrad_reduce(const float* __restrict__ ws, long long P, RedMap m,
+                                                     int total) {
+  __shared__ float red[32][33];
+  const int o = threadIdx.x & 31, pl = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + o;
   float s = 0.f;
-  const long long stride = (long long)NA * NB;
-  const float* p = ws + (long long)a * NB + c;
-  for (long long q = 0; q < P; ++q) s += p[q * stride];
-  return s;
-}
-
-__global__ void wgrad_reduce_rnn(const float* __restrict__ ws, long long P, int H, int I, float* dW_ih,
-                                 float* dW_hh, float* db) {
-  const int NB = H + I + 1;
-  const int total = H * NB;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int a = e / NB, c = e % NB;
-    const float s = sum_parts(ws, P, H, NB, a, c);
-    if (c < H) dW_hh[a * H + c] = s;
-    else if (c < H + I) dW_ih[a * I + (c - H)] = s;
-    else db[a] = s;
-  }
-}
-
-__global__ void wgrad_reduce_gru(const float* __restrict__ ws, long long P, int H, int I, float* dW_ih3,
-                                 float* dW_hh3, float* db_ih3, float* db_hh3) {
-  const int NA = 4 * H, NB = H + I + 1;
-  // outputs: dW_hh3 3H*H, dW_ih3 3H*I, db_ih3 3H, db_hh3 3H
-  const int n_hh = 3 * H * H, n_ih = 3 * H * I, total = n_hh + n_ih + 6 * H;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    if (e < n_hh) {
-      const int row = e / H, k = e % H, g = row / H, i = row % H;
-      const int a = (g == 2 ? 3 : g) * H + i;           // [dR; dZ; dM] h_prev^T
-      dW_hh3[e] = sum_parts(ws, P, NA, NB, a, k);
-    } else if (e < n_hh + n_ih) {
-      const int f = e - n_hh, row = f / I, j = f % I;
-      dW_ih3[f] = sum_parts(ws, P, NA, NB, row, H + j);  // [dR; dZ; dN] x^T
-    } else if (e < n_hh + n_ih + 3 * H) {
-      const int row = e - n_hh - n_ih;
-      db_ih3[row] = sum_parts(ws, P, NA, NB, row, H + I);
-    } else {
-      const int row = e - n_hh - n_ih - 3 * H, g = row / H, i = row % H;
-      db_hh3[row] = sum_parts(ws, P, NA, NB, (g == 2 ? 3 : g) * H + i, H + I);
+  float* out = nullptr;
+  if (e < total) {
+    int a, c;
+    out = map_out(m, e, a, c);
+    const long long stride = (long long)m.NA * m.NB;
+    const float* p = ws + (long long)a * m.NB + c;
+    long long q = pl;
+    for (; q + 96 < P; q += 128) {        // four loads in flight, summed in part order
+      const float v0 = __ldg(p + q * stride), v1 = __ldg(p + (q + 32) * stride), v2 = __ldg(p + (q + 64) * stride),
+                  v3 = __ldg(p + (q + 96) * stride);
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
     }
+    for (; q < P; q += 32) s += __ldg(p + q * stride);
   }
+  red[pl][o] = s;
+  __syncthreads();
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    if (pl < w) red[pl][o] += red[pl + w][o];
+    __syncthreads();
+  }
+  if (pl == 0 && e < total) *out = red[0][o];
+}
+
+cudaError_t reduce_rnn(const float* ws, long long P, int H, int I, float* dW_ih, float* dW_hh, float* db,
+                       cudaStream_t st) {
+  const RedMap m{0, H, I, H, H + I + 1, dW_hh, dW_ih, db, nullptr};
+  const int total = H * (H + I + 1);
+  wgrad_reduce<<<(total + 31) / 32, 1024, 0, st>>>(ws, P, m, total);
+  return cudaGetLastError();
 }
 
 cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream_t st) {
@@ -222,9 +258,12 @@ cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const f
   w.NA = H; w.E = I + 1;
   cudaError_t e = run_partials(w, ws, nparts, st);
   if (e != cudaSuccess) return e;
-  const int NB = H + I + 1;
-  wgrad_reduce_rnn<<<(H * NB + 255) / 256, 256, 0, st>>>(ws, nparts, H, I, dW_ih, dW_hh, db);
-  return cudaGetLastError();
+  return reduce_rnn(ws, nparts, H, I, dW_ih, dW_hh, db, st);
+}
+
+cudaError_t launch_wgrad_reduce_rnn(const float* ws, long long nparts, int H, int I, float* dW_ih, float* dW_hh,
+                                    float* db, cudaStream_t st) {
+  return reduce_rnn(ws, nparts, H, I, dW_ih, dW_hh, db, st);
 }
 
 cudaError_t launch_wgrad_gru(int T, int B, int H, int I, const float* x, const float* hp, const float* r,
@@ -240,7 +279,8 @@ cudaError_t launch_wgrad_gru(int T, int B, int H, int I, const float* x, const f
   cudaError_t e = run_partials(w, ws, nparts, st);
   if (e != cudaSuccess) return e;
   const int total = 3 * H * H + 3 * H * I + 6 * H;
-  wgrad_reduce_gru<<<(total + 255) / 256, 256, 0, st>>>(ws, nparts, H, I, dW_ih3, dW_hh3, db_ih3, db_hh3);
+  const RedMap m{1, H, I, 4 * H, H + I + 1, dW_hh3, dW_ih3, db_ih3, db_hh3};
+  wgrad_reduce<<<(total + 31) / 32, 1024, 0, st>>>(ws, nparts, m, total);
   return cudaGetLastError();
 }
 

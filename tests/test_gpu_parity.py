@@ -243,8 +243,11 @@ def test_gru_materialized_large_H(lib):
 
 
 # ------------------------------------------------------------------ weight gradients
-@pytest.mark.parametrize("T,B,H", [(1000, 16, 20), (3000, 16, 64), (1, 1, 5)])
+@pytest.mark.parametrize("T,B,H", [(1000, 16, 20), (3000, 16, 64), (1, 1, 5), (8192, 16, 64), (20000, 17, 64),
+                                   (20001, 17, 64)])
 def test_weight_grads_rnn(lib, T, B, H):
+    """(8192, 16, 64) and (200xx, 17, 64) take the tcgen05 GEMM path (K >= 131072);
+    20001 * 17 rows end in a ragged 17-row chunk."""
     w = W.rnn_workload(T, B, H, seed=1)
     ref, _ = bp.bp_rnn(w.h, w.W_hh, w.g)
     rng = np.random.default_rng(0)
@@ -255,6 +258,24 @@ def test_weight_grads_rnn(lib, T, B, H):
         torch.cuda.synchronize()
         r = bp.weight_grads_rnn(w.x, w.h, ref.astype(np.float32), h_init=hi)
         assert rel(dWih, r[0]) <= TOL and rel(dWhh, r[1]) <= TOL and rel(db, r[2]) <= TOL
+
+
+@pytest.mark.parametrize("I", [0, 3, 4])
+def test_weight_grads_rnn_inputs_tc(lib, I):
+    """Tensor-core path (H = 64, K = T*B >= 131072) with I input columns; random
+    tape (dW_ih = sum delta x^T, dW_hh = sum delta h_prev^T, db = sum delta)."""
+    T, B, H = 4099, 37, 64
+    rng = np.random.default_rng(I)
+    h = rng.uniform(-0.95, 0.95, (T, B, H)).astype(np.float32)
+    g = rng.standard_normal((T, B, H)).astype(np.float32)
+    x = rng.standard_normal((T, B, I)).astype(np.float32)
+    h_init = rng.uniform(-1, 1, (B, H)).astype(np.float32)
+    dWih, dWhh, db = lib.weight_grads_rnn(cu(x), cu(h), cu(g), h_init=cu(h_init))
+    torch.cuda.synchronize()
+    r = bp.weight_grads_rnn(x, h, g, h_init=h_init)
+    assert rel(dWhh, r[1]) <= TOL and rel(db, r[2]) <= TOL
+    if I:
+        assert rel(dWih, r[0]) <= TOL
 
 
 @pytest.mark.parametrize("set_name,B", [("S", 16), ("L", 64)])
