@@ -34,7 +34,7 @@ constexpr int H = 64, KC = 32, MROWS = 128, NCONV = 256, NTH = NCONV + 64;   // 
 constexpr int FLUSH = 32;                           // chunks per accumulation window
 constexpr long long PART_ROWS = 16384;              // rows per part (512 chunks)
 constexpr int MAXI = 4;
-constexpr int NS = 6;                               // staging depth (chunks)
+constexpr int NS = 4;                               // staging depth (chunks, power of 2)
 constexpr int NBUF = 4;                             // A (TMEM) / B (SMEM) operand buffers
 constexpr int ROW_BYTES = H * 4;
 constexpr int SB = 3 * KC * ROW_BYTES;              // h, g, h_prev rows: 24 KB per stage
@@ -159,20 +159,20 @@ struct Bars {
 };
 
 // One chunk's rows for this thread: A values (delta hi or lo) and B values
-// (h_prev hi or lo) of rows 16*grp .. 16*grp+15; rows >= n are zero, h_prev
-// rows < nlow (before h_0 with no h_init) are zero.
-template <bool LO, bool FULL>
-__device__ __forceinline__ void convert_rows(uint32_t st, const float* xs, int I, int grp, int n, int nlow,
-                                             float (&av)[16], float (&bv)[16], float& dbias, float (&dih)[MAXI]) {
+// (h_prev hi or lo) of rows 16*grp .. 16*grp+15 (base = stage + column i +
+// 16*grp rows); rows >= n are zero, h_prev rows < nlow (before h_0 with no
+// h_init) are zero.  IX = number of input columns (hi threads only).
+template <bool LO, int IX, bool FULL>
+__device__ __forceinline__ void convert_rows(uint32_t base, uint32_t xbase, int n, int nlow, float (&av)[16],
+                                             float (&bv)[16], float& dbias, float (&dih)[MAXI]) {
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
-    const int r = 16 * grp + rr;
-    const float hv = lds(st + r * ROW_BYTES), gv = lds(st + (KC + r) * ROW_BYTES),
-                pv = lds(st + (2 * KC + r) * ROW_BYTES);
+    const float hv = lds(base + rr * ROW_BYTES), gv = lds(base + (KC + rr) * ROW_BYTES),
+                pv = lds(base + (2 * KC + rr) * ROW_BYTES);
     float d = (1.f - hv * hv) * gv, hp = pv;
     if (!FULL) {
-      d = r < n ? d : 0.f;
-      hp = (r < n && r >= nlow) ? hp : 0.f;
+      d = rr < n ? d : 0.f;
+      hp = (rr < n && rr >= nlow) ? hp : 0.f;
     }
     const float dhi = tf32_hi(d), phi = tf32_hi(hp);
     av[rr] = LO ? d - dhi : dhi;
@@ -180,26 +180,24 @@ __device__ __forceinline__ void convert_rows(uint32_t st, const float* xs, int I
     if (!LO) {
       dbias += d;
 #pragma unroll
-      for (int j = 0; j < MAXI; ++j)
-        if (j < I) {
-          float xv = xs[r * I + j];
-          if (!FULL) xv = r < n ? xv : 0.f;
-          dih[j] = fmaf(d, xv, dih[j]);
-        }
+      for (int j = 0; j < IX; ++j) {
+        float xv = lds(xbase + 4 * (rr * IX + j));
+        if (!FULL) xv = rr < n ? xv : 0.f;
+        dih[j] = fmaf(d, xv, dih[j]);
+      }
     }
   }
 }
 
-template <bool LO>
-__device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, const char* smem, Bars br, uint32_t tmem,
-                                           int warp, int lane) {
+template <bool LO, int IX>
+__device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br, uint32_t tmem, int warp,
+                                           int lane) {
   const int wq = warp & 3, grp = warp >> 2;
   const int m = 32 * wq + lane, i = m & 63;
   const uint32_t tl = tmem + ((uint32_t)(32 * wq) << 16);
-  const int NB = H + w.I + 1;
-  ChunkIter it;
-  it.start(blockIdx.x, w.rows);
-  while (it.part < w.nparts) {
+  const int NB = H + IX + 1;
+  uint32_t cg = 0;
+  for (long long part = blockIdx.x; part < w.nparts; part += gridDim.x) {
     float acc[64];
 #pragma unroll
     for (int k = 0; k < 64; ++k) acc[k] = 0.f;
@@ -215,26 +213,27 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, const c
         for (int k = 0; k < 32; ++k) acc[32 * q + k] += t[k];
       }
     };
-    const long long part = it.part, nch = it.nch;
-    for (long long c = 0; c < nch; ++c) {
-      const long long cg = it.cg;
-      const int b = (int)(cg % NBUF), s = (int)(cg % NS);
-      const long long rb = it.r0 + c * KC;
-      const int n = (int)min((long long)KC, it.r1 - rb);
-      const int nlow = w.h_init ? 0 : (int)max(0ll, min((long long)KC, (long long)w.B - rb));
-      mbar_wait(br.full(s), (uint32_t)((cg / NS) & 1));
-      const uint32_t st = s0 + OFF_STAGE + s * SB + 4u * i;
-      const float* xs = reinterpret_cast<const float*>(smem + OFF_X + s * XB);
+    const long long r0 = part * PART_ROWS;
+    const int rows_here = (int)(min(r0 + PART_ROWS, w.rows) - r0);
+    const int nch = (rows_here + KC - 1) / KC;
+    const int lowB = w.h_init ? 0 : (int)max(0ll, min((long long)rows_here, (long long)w.B - r0));
+    for (int c = 0; c < nch; ++c, ++cg) {
+      const uint32_t b = cg % NBUF, s = cg % NS;
+      const int n = min(KC, rows_here - c * KC) - 16 * grp;        // valid rows of my half
+      const int nlow = lowB - c * KC - 16 * grp;                     // h_prev rows before h_0
+      mbar_wait(br.full(s), (cg / NS) & 1);
+      const uint32_t base = s0 + OFF_STAGE + s * SB + 4u * i + 16u * grp * ROW_BYTES;
+      const uint32_t xbase = s0 + OFF_X + s * XB + 4u * 16 * grp * IX;
       float av[16], bv[16];
-      if (n == KC && nlow == 0) convert_rows<LO, true>(st, xs, w.I, grp, n, nlow, av, bv, dbias, dih);
-      else convert_rows<LO, false>(st, xs, w.I, grp, n, nlow, av, bv, dbias, dih);
+      if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true>(base, xbase, n, nlow, av, bv, dbias, dih);
+      else convert_rows<LO, IX, false>(base, xbase, n, nlow, av, bv, dbias, dih);
       mbar_arrive(br.empty(s));
       if (c > 0 && c % FLUSH == 0) {           // window boundary: chunk cg-1 done, read D
-        mbar_wait(br.freeb((int)((cg - 1) % NBUF)), (uint32_t)(((cg - 1) / NBUF) & 1));
+        mbar_wait(br.freeb((cg - 1) % NBUF), ((cg - 1) / NBUF) & 1);
         tc_after();
         flush();
       } else if (c >= NBUF) {                  // operand buffer b was last read by chunk cg-NBUF
-        mbar_wait(br.freeb(b), (uint32_t)(((cg - NBUF) / NBUF) & 1));
+        mbar_wait(br.freeb(b), ((cg - NBUF) / NBUF) & 1);
         tc_after();
       }
       tmem_st16(tl + 128 + 32 * b + 16 * grp, av);
@@ -246,11 +245,10 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, const c
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       tc_before();
       mbar_arrive(br.a_full(b));
-      it.next(w.rows);
     }
     // last window of the part
-    const long long cl = it.cg - 1;
-    mbar_wait(br.freeb((int)(cl % NBUF)), (uint32_t)((cl / NBUF) & 1));
+    const uint32_t cl = cg - 1;
+    mbar_wait(br.freeb(cl % NBUF), (cl / NBUF) & 1);
     tc_after();
     flush();
     tc_before();
@@ -259,9 +257,8 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, const c
 #pragma unroll
     for (int k = 0; k < 64; ++k) dst[k] = acc[k];
 #pragma unroll
-    for (int j = 0; j < MAXI; ++j)
-      if (j < w.I) dst[H + j] = LO ? 0.f : dih[j];
-    dst[H + w.I] = LO ? 0.f : dbias;
+    for (int j = 0; j < IX; ++j) dst[H + j] = LO ? 0.f : dih[j];
+    dst[H + IX] = LO ? 0.f : dbias;
   }
 }
 
@@ -355,9 +352,21 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
     }
     __syncwarp();
   } else if ((warp & 3) >= 2) {
-    converters<true>(w, s0, smem, br, tmem, warp, lane);
+    switch (w.I) {     // lo rows ignore x; NB (the slab row length) still depends on I
+      case 0: converters<true, 0>(w, s0, br, tmem, warp, lane); break;
+      case 1: converters<true, 1>(w, s0, br, tmem, warp, lane); break;
+      case 2: converters<true, 2>(w, s0, br, tmem, warp, lane); break;
+      case 3: converters<true, 3>(w, s0, br, tmem, warp, lane); break;
+      default: converters<true, 4>(w, s0, br, tmem, warp, lane); break;
+    }
   } else {
-    converters<false>(w, s0, smem, br, tmem, warp, lane);
+    switch (w.I) {
+      case 0: converters<false, 0>(w, s0, br, tmem, warp, lane); break;
+      case 1: converters<false, 1>(w, s0, br, tmem, warp, lane); break;
+      case 2: converters<false, 2>(w, s0, br, tmem, warp, lane); break;
+      case 3: converters<false, 3>(w, s0, br, tmem, warp, lane); break;
+      default: converters<false, 4>(w, s0, br, tmem, warp, lane); break;
+    }
   }
   tc_before();
   __syncthreads();
