@@ -7,9 +7,11 @@
 // i.e. one dense contraction D[128 x 64] = A[128 x 64] . B[64 x 64] per step
 // and tile, with A = X^T (one row per chain: x = d o c), B[n][k] = W[k][n].
 // fp32 accuracy from 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, x = x_hi +
-// x_lo, x_hi = tf32_rn(x), x_lo = tf32_rn(x - x_hi)).  lo is rounded to
-// nearest explicitly: left to the MMA's operand truncation it carries a
-// one-signed 2^-21 bias per product that grows linearly along a chain.
+// x_lo, x_hi = x with the 13 low mantissa bits cleared — what the MMA reads of
+// a tf32 operand anyway — and x_lo = rn_tf32(x - x_hi), both on the integer
+// pipe: cvt.rna.tf32.f32 is a 4-instruction sequence on sm_100a).  lo is
+// rounded to nearest explicitly: left to the MMA's operand truncation it
+// carries a one-signed 2^-21 bias per product that grows along a chain.
 //
 // A tile = 128 chains = the 64 column chains of block q of sample b and those
 // of sample b+1 (same slots, same length).  A tf32 MMA with M = 128 costs ~60
@@ -160,28 +162,36 @@ __device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, fl
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(sdst)), "l"(gsrc) : "memory");
 }
-// x = d o c for the K-half `kh` (32 columns) of the chain's row, split into
-// tf32 hi / lo and stored into this lane's A_hi / A_lo TMEM columns;
-// hrow = shared address of the block's staged h_t row (broadcast reads)
-__device__ __forceinline__ void write_half(uint32_t t_ahi, uint32_t t_alo, int kh, uint32_t hrow,
+// x -> (x_hi, x_lo) into this lane's A_hi / A_lo TMEM columns (K-half kh):
+// x_hi = x truncated to tf32 (x & ~0x1FFF), x_lo = rn_tf32(x - x_hi) (ties
+// away; x - x_hi is exact), integer ops only
+__device__ __forceinline__ void split_store(uint32_t t_ahi, uint32_t t_alo, int kh, const float (&x)[32]) {
+  uint32_t hi[32], lo[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    hi[k] = __float_as_uint(x[k]) & 0xFFFFE000u;
+    lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
+  }
+  tmem_st32(t_ahi + 32 * kh, hi);
+  tmem_st32(t_alo + 32 * kh, lo);
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+// x = d o c for the K-half `kh` (32 columns) of the chain's row, split and
+// stored; drow = shared address of the block's staged d_t = 1 - h_t^2 row
+// (broadcast reads)
+__device__ __forceinline__ void write_half(uint32_t t_ahi, uint32_t t_alo, int kh, uint32_t drow,
                                           const float (&c)[32]) {
-  uint32_t v[32];
+  float x[32];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const float4 h4 = lds128(hrow + 4u * (32 * kh + 4 * q));
-    const float hv4[4] = {h4.x, h4.y, h4.z, h4.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) v[4 * q + e] = __float_as_uint((1.f - hv4[e] * hv4[e]) * c[4 * q + e]);
+    const float4 d4 = lds128(drow + 4u * (32 * kh + 4 * q));
+    x[4 * q] = d4.x * c[4 * q];
+    x[4 * q + 1] = d4.y * c[4 * q + 1];
+    x[4 * q + 2] = d4.z * c[4 * q + 2];
+    x[4 * q + 3] = d4.w * c[4 * q + 3];
   }
-  uint32_t hi[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) hi[k] = __float_as_uint(tf32_rn(__uint_as_float(v[k])));
-  tmem_st32(t_ahi + 32 * kh, hi);
-#pragma unroll
-  for (int k = 0; k < 32; ++k)   // lo rounded to nearest (not the MMA's truncation: no bias)
-    v[k] = __float_as_uint(tf32_rn(__uint_as_float(v[k]) - __uint_as_float(hi[k])));
-  tmem_st32(t_alo + 32 * kh, v);
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  split_store(t_ahi, t_alo, kh, x);
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -293,7 +303,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
       for (int k = 0; k < 32; ++k) c[k] = (32 * kh + k == j && ok) ? 1.f : 0.f;
       for (long long sc = s0; sc < s1; sc += HCH) {
         const int n = (int)min((long long)HCH, s1 - sc);
-        // stage the h_t rows of this chunk for both blocks of the tile (cp.async)
+        // stage the h_t rows of this chunk for both blocks of the tile (cp.async),
+        // then d = 1 - h^2 in place (each thread converts the pieces it copied)
         named_bar(1 + g, EPI_THREADS);             // previous chunk fully consumed
         for (int e = et; e < 2 * n * 16; e += EPI_THREADS) {
           const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
@@ -305,6 +316,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
             sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
+        for (int e = et; e < 2 * n * 16; e += EPI_THREADS) {
+          const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+          const uint32_t p = hs_s + 4u * ((bb2 * HCH + st) * TH + ch * 4);
+          const float4 h4 = lds128(p);
+          sts128(p, 1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
+        }
         named_bar(1 + g, EPI_THREADS);
         const uint32_t hb = hs_s + 4u * ((row >> 6) * HCH * TH);
         for (int st = 0; st < n; ++st) {
@@ -483,17 +500,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_down_kernel(LeafArgs a, i
 #pragma unroll
           for (int k = 0; k < 32; ++k) dv[k] = 0.f;
         }
-        uint32_t v[32], hi[32];
+        float x[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const float x = dv[k] * c[k];
-          const float h = tf32_rn(x);
-          hi[k] = __float_as_uint(h);
-          v[k] = __float_as_uint(tf32_rn(x - h));
-        }
-        tmem_st32(t_ahi + 32 * kh, hi);
-        tmem_st32(t_alo + 32 * kh, v);
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        for (int k = 0; k < 32; ++k) x[k] = dv[k] * c[k];
+        split_store(t_ahi, t_alo, kh, x);
         tc_fence_before();
         mbar_arrive(&a_full[g]);
         mbar_wait(&d_full[g], ph);
