@@ -19,11 +19,14 @@
 // [W_hi | W_lo] along N and every MMA is a full-rate N = 128 one:
 // D = A_lo [W_hi | W_lo] + A_hi [W_hi | W_lo] (16 MMAs, A_hi / A_lo in TMEM —
 // the TS form, B from shared memory), D[:, :64] + D[:, 64:] summed
-// round-to-nearest in the epilogue (4 products incl. lo*lo, 2 TMEM reads).  CTA = 2 x 8 epilogue warps (thread = chain row x K-half:
-// tcgen05.ld D -> scale by d -> tf32 split -> tcgen05.st A) + 1 MMA-issuer
-// warp; two tiles are in flight so one tile's epilogue overlaps the other
-// tile's MMAs.  Persistent grid, one CTA per SM.
+// round-to-nearest in the epilogue (4 products incl. lo*lo, 2 TMEM reads).
+// Two tiles (slots) are in flight per CTA so one slot's epilogue (tcgen05.ld
+// D -> sum -> scale by d -> tf32 split -> tcgen05.st A) overlaps the other
+// slot's MMAs.  Up-sweep: 2 x 16 epilogue warps, the slot's first warp issues
+// (see tc_leaf_up16_kernel); down-walk: 2 x 8 epilogue warps + 1 issuer warp.
+// Persistent grid, one CTA per SM.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -42,8 +45,6 @@ constexpr int HCH = 64;                   // steps staged per chunk
 constexpr int H_BYTES = 2 * HCH * TH * 4; // one tile's h slices (2 blocks), 32 KB
 constexpr int OFF_B = 0;
 constexpr int OFF_H = OFF_B + B_BYTES;
-constexpr int OFF_BAR = OFF_H + NSLOT * H_BYTES;          // a_full[2], d_full[2], tmem
-constexpr int SMEM_BYTES = OFF_BAR + 64 + 1024;           // + 1024 B alignment slack
 // TMEM columns of slot g (base 256 g): D = A [W_hi | W_lo] accumulated over
 // A = A_lo then A_hi at [0, 128) (cols 0..63: hh + lh, 64..127: hl + ll),
 // A_hi at [128, 192), A_lo at [192, 256)
@@ -95,12 +96,6 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
 // A from TMEM (K-major: row = lane, K along 32-bit columns), B from shared memory
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id,
                                             uint32_t acc) {
@@ -177,34 +172,104 @@ __device__ __forceinline__ void split_store(uint32_t t_ahi, uint32_t t_alo, int 
   asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
-// x = d o c for the K-half `kh` (32 columns) of the chain's row, split and
-// stored; drow = shared address of the block's staged d_t = 1 - h_t^2 row
-// (broadcast reads)
-__device__ __forceinline__ void write_half(uint32_t t_ahi, uint32_t t_alo, int kh, uint32_t drow,
-                                          const float (&c)[32]) {
-  float x[32];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 d4 = lds128(drow + 4u * (32 * kh + 4 * q));
-    x[4 * q] = d4.x * c[4 * q];
-    x[4 * q + 1] = d4.y * c[4 * q + 1];
-    x[4 * q + 2] = d4.z * c[4 * q + 2];
-    x[4 * q + 3] = d4.w * c[4 * q + 3];
-  }
-  split_store(t_ahi, t_alo, kh, x);
-}
-
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
-                                                                 long long n_out, long long q0) {
+// ---------------------------------------------------------------------------
+// Level-0 UP-sweep: 16 epilogue warps per tile slot (1024 threads), thread =
+// (chain row, 16-column group).  Per step the slot's warps meet at a named
+// barrier and the converged first warp of the slot issues the 16 MMAs + commit
+// (one elected stream, under a CTA lock so the two slots' batches never
+// interleave); one lane polls the completion mbarrier while the other warps
+// sleep in bar.sync.  Measured (scripts/tc_up_trace.cu, tc_rate3.cu): polling
+// warps and interleaved batches each cost ~15-25 cycles per MMA.
+// ---------------------------------------------------------------------------
+#ifdef BPPSA_STEP_TRACE
+__device__ long long g_step_trace[2][2][8][4096];   // [slot][warp 0 / warp 13][phase][step]
+#define STEP_TRACE(ph)                                                                            \
+  if (blockIdx.x == 0 && lane == 0 && (wl == 0 || wl == 13) && tstep < 4096)                      \
+    g_step_trace[g][wl == 13][ph][tstep] = clock64();
+#else
+#define STEP_TRACE(ph)
+#endif
+constexpr int EPI16_WARPS = 16;
+constexpr int EPI16_THREADS = 32 * EPI16_WARPS;
+constexpr int NTHREADS16 = EPI16_THREADS * NSLOT;          // 1024
+constexpr int OFF_BAR16 = OFF_H + NSLOT * H_BYTES;         // d_full[2], tmem
+constexpr int SMEM_BYTES16 = OFF_BAR16 + 64 + 1024;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// CTA-scope spin lock in shared memory (one lane per slot contends)
+__device__ __forceinline__ void lock_acquire(uint32_t a) {
+  asm volatile(
+      "{\n .reg .b32 old;\n .reg .pred p;\nL_%=:\n atom.shared.cta.acquire.cas.b32 old, [%0], 0, 1;\n"
+      " setp.ne.b32 p, old, 0;\n @p bra L_%=;\n}\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void lock_release(uint32_t a) {
+  asm volatile("st.shared.release.cta.b32 [%0], 0;\n" ::"r"(a) : "memory");
+}
+
+// The step's 16 MMAs (A_lo then A_hi, K = 64 in 8-wide steps, B = [W_hi | W_lo])
+// and their commit as ONE elected instruction stream of the converged warp:
+// operands stay warp-uniform, so the issue costs ~2 instructions per MMA
+// instead of a per-MMA elect loop with descriptor arithmetic.
+__device__ __forceinline__ void mma16_commit(uint32_t d, const uint64_t (&bd)[8], uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 a;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 a, %0, 192;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %1, %9, f;\n"
+      " add.u32 a, %0, 200;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %2, %9, t;\n"
+      " add.u32 a, %0, 208;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %3, %9, t;\n"
+      " add.u32 a, %0, 216;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %4, %9, t;\n"
+      " add.u32 a, %0, 224;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %5, %9, t;\n"
+      " add.u32 a, %0, 232;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %6, %9, t;\n"
+      " add.u32 a, %0, 240;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %7, %9, t;\n"
+      " add.u32 a, %0, 248;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %8, %9, t;\n"
+      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %1, %9, t;\n"
+      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %2, %9, t;\n"
+      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %3, %9, t;\n"
+      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %4, %9, t;\n"
+      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %5, %9, t;\n"
+      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %6, %9, t;\n"
+      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %7, %9, t;\n"
+      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a], %8, %9, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n"
+      "}\n" ::"r"(d),
+      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "l"(bd[4]), "l"(bd[5]), "l"(bd[6]), "l"(bd[7]), "r"(IDESC128),
+      "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up16_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                     long long n_out, long long q0) {
   extern __shared__ uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* d_full = a_full + NSLOT;
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR16);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  int* issue_lock = reinterpret_cast<int*>(tmem_slot + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int B = a.seg.B;
   const long long S = a.seg.S();
@@ -212,21 +277,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
   const int nbp = (B + 1) / 2;
   const long long ntiles = (long long)nbp * nq;
 
-  // ---- setup: B = W (hi / lo), barriers, TMEM
-  for (int e = threadIdx.x; e < TH * TH; e += NTHREADS) {
+  for (int e = threadIdx.x; e < TH * TH; e += NTHREADS16) {
     const int n = e / TH, k = e % TH;               // B[n][k] = W[k][n]: rows 0..63 hi, 64..127 lo
     const float w = __ldg(a.W + (long long)k * TH + n);
     const float hi = tf32_rn(w);
     *reinterpret_cast<float*>(smem + OFF_B + sw_off(n, k, B_ROWS)) = hi;
     *reinterpret_cast<float*>(smem + OFF_B + sw_off(TH + n, k, B_ROWS)) = tf32_rn(w - hi);
   }
-  const int mma_warp = EPI_WARPS * NSLOT;
-  if (warp == mma_warp) {
+  if (warp == 0) {
     if (lane == 0) {
-      for (int s = 0; s < NSLOT; ++s) {
-        mbar_init(&a_full[s], EPI_THREADS);
-        mbar_init(&d_full[s], 1);
-      }
+      for (int s = 0; s < NSLOT; ++s) mbar_init(&d_full[s], 1);
+      *issue_lock = 0;
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
@@ -240,119 +301,137 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_up_kernel(LeafArgs a, int
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == mma_warp) {
-    // ================= MMA issuer: both tile slots, 16 full-rate N = 128 MMAs per step =====
-    uint32_t pha[NSLOT] = {0, 0};
-    const uint32_t bb = su32(smem + OFF_B);
-    long long len[NSLOT] = {0, 0}, done[NSLOT] = {0, 0}, tau[NSLOT];
-    for (int sl = 0; sl < NSLOT; ++sl) tau[sl] = 2 * (long long)blockIdx.x + sl;
-    auto tile_len = [&](long long t) -> long long {
-      if (t >= ntiles) return 0;
-      const long long q = q0 + t / nbp;
-      return min(q * C + C, S) - q * C;
-    };
-    for (int sl = 0; sl < NSLOT; ++sl) len[sl] = tile_len(tau[sl]);
-    while (len[0] > 0 || len[1] > 0) {
-      for (int sl = 0; sl < NSLOT; ++sl) {
-        if (len[sl] == 0) continue;
-        mbar_wait(&a_full[sl], pha[sl]);
-        pha[sl] ^= 1;
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t d = tmem + 256 * sl, a_hi = d + 128, a_lo = d + 192;
+  const int g = warp / EPI16_WARPS, wl = warp % EPI16_WARPS;
+  const int row = (wl & 3) * 32 + lane;                   // TMEM lane / A row (lane quarter = warp % 4)
+  const int cgp = wl >> 2;                                // 16-column group of D / of A's K
+  const int et = wl * 32 + lane;
+  const bool issuer = wl == 0;
+  const uint32_t slot_base = tmem + 256 * g;
+  const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
+  const uint32_t t_dh = lane_base + 16 * cgp, t_dl = t_dh + 64;
+  const uint32_t t_ahi = lane_base + 128 + 16 * cgp, t_alo = lane_base + 192 + 16 * cgp;
+  float* hs = reinterpret_cast<float*>(smem + OFF_H + g * H_BYTES);   // [2 blocks][HCH][64]
+  const uint32_t hs_s = su32(hs);
+  const uint32_t bb = su32(smem + OFF_B);
+  const uint32_t lock_s = su32(issue_lock);
+  uint64_t bdesc[TH / 8];                                 // B descriptors of the 8 K-steps (constant)
 #pragma unroll
-          for (int pq = 0; pq < 2; ++pq) {              // A_lo first: small terms while D is small
-            const uint32_t aa = pq == 0 ? a_lo : a_hi;
+  for (int kk = 0; kk < TH / 8; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)((kk >> 2) * B_ROWS * 128 + (kk & 3) * 32));
+  uint32_t ph = 0;
+  const long long rowB = (long long)B * TH;
+#ifdef BPPSA_STEP_TRACE
+  int tstep = 0;
+#endif
+  for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+    const long long q = q0 + tau / nbp;
+    const int bp = (int)(tau % nbp);
+    const int b = bp * 2 + (row >> 6);
+    const int j = row & 63;
+    const bool ok = b < B;
+    const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+    float c[16];
 #pragma unroll
-            for (int kk = 0; kk < TH / 8; ++kk) {
-              const uint32_t boff = (uint32_t)((kk >> 2) * B_ROWS * 128 + (kk & 3) * 32);
-              mma_tf32_ts(d, aa + 8 * kk, sdesc(bb + boff), IDESC128, (pq | kk) != 0);
-            }
+    for (int k = 0; k < 16; ++k) c[k] = (16 * cgp + k == j && ok) ? 1.f : 0.f;
+    for (long long sc = s0; sc < s1; sc += HCH) {
+      const int n = (int)min((long long)HCH, s1 - sc);
+      named_bar(1 + g, EPI16_THREADS);             // previous chunk fully consumed
+      for (int e = et; e < 2 * n * 16; e += EPI16_THREADS) {
+        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+        float* dst = hs + (bb2 * HCH + st) * TH + ch * 4;
+        const int bs = bp * 2 + bb2;
+        if (bs < B)
+          cp_async16(dst, a.h + (long long)a.seg.time_of(sc + st) * rowB + (long long)bs * TH + ch * 4);
+        else
+          sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      for (int e = et; e < 2 * n * 16; e += EPI16_THREADS) {   // d = 1 - h^2 in place
+        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+        const uint32_t p = hs_s + 4u * ((bb2 * HCH + st) * TH + ch * 4);
+        const float4 h4 = lds128(p);
+        sts128(p, 1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
+      }
+      named_bar(1 + g, EPI16_THREADS);
+      const uint32_t drow0 = hs_s + 4u * ((row >> 6) * HCH * TH + 16 * cgp);
+      for (int st = 0; st < n; ++st) {
+        STEP_TRACE(0);
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 d4 = lds128(drow0 + 4u * (st * TH + 4 * q4));
+          const float x4[4] = {d4.x * c[4 * q4], d4.y * c[4 * q4 + 1], d4.z * c[4 * q4 + 2], d4.w * c[4 * q4 + 3]};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[4 * q4 + e] = __float_as_uint(x4[e]) & 0xFFFFE000u;
+            lo[4 * q4 + e] = (__float_as_uint(x4[e] - __uint_as_float(hi[4 * q4 + e])) + 0x1000u) & 0xFFFFE000u;
           }
-          mma_commit(&d_full[sl]);
         }
-        __syncwarp();
-        if (++done[sl] == len[sl]) {
-          done[sl] = 0;
-          tau[sl] += 2 * (long long)gridDim.x;
-          len[sl] = tile_len(tau[sl]);
+#ifndef BPPSA_TRACE_NO_EPI
+        tmem_st16(t_ahi, hi);
+        tmem_st16(t_alo, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+#endif
+        STEP_TRACE(1);
+        tc_fence_before();
+        named_bar(3 + g, EPI16_THREADS);           // the slot's A is complete
+        STEP_TRACE(2);
+        if (issuer) {
+          tc_fence_after();
+          // one slot's 16 MMAs go into the tensor queue back to back: with
+          // interleaved batches both slots finish together and their
+          // epilogues lock in phase instead of overlapping the other slot's MMAs
+          if (lane == 0) lock_acquire(lock_s);
+          __syncwarp();
+#ifndef BPPSA_TRACE_NO_MMA
+          mma16_commit(slot_base, bdesc, su32(&d_full[g]));
+#else
+          if (lane == 0) mma_commit(&d_full[g]);
+          __syncwarp();
+#endif
+          if (lane == 0) lock_release(lock_s);
+          __syncwarp();
         }
+        STEP_TRACE(3);
+        // one lane polls the MMA-completion barrier; the slot's other warps
+        // sleep in a hardware barrier (polling warps slow the tensor pipe:
+        // 24 warps in try_wait loops cost ~25 cycles per MMA, scripts/tc_rate3.cu)
+        if (issuer) {
+          if (lane == 0) mbar_wait(&d_full[g], ph);
+          __syncwarp();
+        }
+        named_bar(5 + g, EPI16_THREADS);
+        ph ^= 1;
+        tc_fence_after();
+        STEP_TRACE(4);
+        float t[16];                               // c = (hh + lh) + (hl + ll), round-to-nearest
+#ifndef BPPSA_TRACE_NO_EPI
+        tmem_ld16(t_dh, c);
+        tmem_ld16(t_dl, t);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#else
+        for (int k = 0; k < 16; ++k) t[k] = __uint_as_float(hi[k] ^ lo[k]);
+#endif
+        STEP_TRACE(5);
+#ifdef BPPSA_STEP_TRACE
+        ++tstep;
+#endif
+#pragma unroll
+        for (int k = 0; k < 16; ++k) c[k] += t[k];
       }
     }
-  } else {
-    // ===== tile slot g: 8 warps, thread = (chain row, K-half) =====
-    const int g = warp / EPI_WARPS, wl = warp % EPI_WARPS;
-    const int row = (wl & 3) * 32 + lane;                   // TMEM lane / A row (lane quarter = warp % 4)
-    const int kh = wl >> 2;                                 // column half of D / K-half of A
-    const int et = wl * 32 + lane;                          // 0 .. EPI_THREADS-1
-    const uint32_t lane_base = tmem + ((uint32_t)((wl & 3) * 32) << 16) + 256 * g;
-    const uint32_t t_d = lane_base + 32 * kh, t_ahi = lane_base + 128, t_alo = lane_base + 192;
-    float* hs = reinterpret_cast<float*>(smem + OFF_H + g * H_BYTES);   // [2 blocks][HCH][64]
-    const uint32_t hs_s = su32(hs);
-    uint32_t ph = 0;
-    const long long rowB = (long long)B * TH;
-    for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
-      const long long q = q0 + tau / nbp;
-      const int bp = (int)(tau % nbp);
-      const int b = bp * 2 + (row >> 6);
-      const int j = row & 63;
-      const bool ok = b < B;
-      const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
-      float c[32];
+    if (ok) {
+      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 16 * cgp);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) c[k] = (32 * kh + k == j && ok) ? 1.f : 0.f;
-      for (long long sc = s0; sc < s1; sc += HCH) {
-        const int n = (int)min((long long)HCH, s1 - sc);
-        // stage the h_t rows of this chunk for both blocks of the tile (cp.async),
-        // then d = 1 - h^2 in place (each thread converts the pieces it copied)
-        named_bar(1 + g, EPI_THREADS);             // previous chunk fully consumed
-        for (int e = et; e < 2 * n * 16; e += EPI_THREADS) {
-          const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
-          float* dst = hs + (bb2 * HCH + st) * TH + ch * 4;
-          const int bs = bp * 2 + bb2;
-          if (bs < B)
-            cp_async16(dst, a.h + (long long)a.seg.time_of(sc + st) * rowB + (long long)bs * TH + ch * 4);
-          else
-            sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
-        }
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        for (int e = et; e < 2 * n * 16; e += EPI_THREADS) {
-          const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
-          const uint32_t p = hs_s + 4u * ((bb2 * HCH + st) * TH + ch * 4);
-          const float4 h4 = lds128(p);
-          sts128(p, 1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
-        }
-        named_bar(1 + g, EPI_THREADS);
-        const uint32_t hb = hs_s + 4u * ((row >> 6) * HCH * TH);
-        for (int st = 0; st < n; ++st) {
-          write_half(t_ahi, t_alo, kh, hb + 4u * st * TH, c);
-          tc_fence_before();
-          mbar_arrive(&a_full[g]);
-          mbar_wait(&d_full[g], ph);
-          ph ^= 1;
-          tc_fence_after();
-          float t[32];                           // c = (hh + lh) + (hl + ll), round-to-nearest
-          tmem_ld32(t_d, c);
-          tmem_ld32(t_d + 64, t);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) c[k] += t[k];
-        }
-      }
-      if (ok) {
-        float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 32 * kh);
-#pragma unroll
-        for (int k4 = 0; k4 < 8; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
-      }
+      for (int k4 = 0; k4 < 4; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == EPI_WARPS * NSLOT) {
+  if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // Level-0 DOWN-sweep on the tensor cores: every block (b, q) is a vector chain
@@ -535,17 +614,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_down_kernel(LeafArgs a, i
 // Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.
 cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
                               int num_sms, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   const long long ntiles = (long long)((a.seg.B + 1) / 2) * (n_out - q0);
   const long long pairs = (ntiles + 1) / 2;
   const int grid = (int)std::min<long long>(pairs, num_sms);
   if (grid <= 0) return cudaSuccess;
-  tc_leaf_up_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+  static bool attr16 = false;
+  if (!attr16) {
+    cudaError_t e = cudaFuncSetAttribute(tc_leaf_up16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES16);
+    if (e != cudaSuccess) return e;
+    attr16 = true;
+  }
+  tc_leaf_up16_kernel<<<grid, NTHREADS16, SMEM_BYTES16, st>>>(a, C, agg_out, n_out, q0);
   return cudaGetLastError();
 }
 
