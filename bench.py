@@ -223,7 +223,7 @@ def run_ours(args):
         # flop costs 3 TF32 tensor flops; TF32 peak = measured bf16 x nominal
         # tf32/bf16 ratio (1.125 / 2.25) from B200_PROFILING.md
         peak = pk["bf16_tflops"] * 0.5 / 3.0
-        result["roofline"] = {"bound": "tensor", "kernel": "tc_leaf_up_kernel (level-0 fused fold, tcgen05 3xTF32)",
+        result["roofline"] = {"bound": "tensor", "kernel": "tc_leaf_up16_kernel (level-0 fused fold, tcgen05 3xTF32)",
                               "achieved": round(achieved, 3), "peak": round(peak, 2),
                               "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                               "traffic": load_traffic("tc_leaf_up"),
