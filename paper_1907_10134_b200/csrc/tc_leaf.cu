@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up16_kernel(LeafArgs a,
   uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR16);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
   int* issue_lock = reinterpret_cast<int*>(tmem_slot + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index and TMEM base through a shuffle: provably warp-uniform, so the
+  // issuer's descriptors / TMEM addresses live in uniform registers (a few
+  // instructions per MMA instead of ~15 with per-MMA R2UR and rematerialisation)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int B = a.seg.B;
   const long long S = a.seg.S();
   const long long nq = n_out - q0;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up16_kernel(LeafArgs a,
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   const int g = warp / EPI16_WARPS, wl = warp % EPI16_WARPS;
   const int row = (wl & 3) * 32 + lane;                   // TMEM lane / A row (lane quarter = warp % 4)
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up16_kernel(LeafArgs a,
   const uint32_t t_ahi = lane_base + 128 + 16 * cgp, t_alo = lane_base + 192 + 16 * cgp;
   float* hs = reinterpret_cast<float*>(smem + OFF_H + g * H_BYTES);   // [2 blocks][HCH][64]
   const uint32_t hs_s = su32(hs);
-  const uint32_t bb = su32(smem + OFF_B);
+  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem + OFF_B), 0);   // warp-uniform (see above)
   const uint32_t lock_s = su32(issue_lock);
   uint64_t bdesc[TH / 8];                                 // B descriptors of the 8 K-steps (constant)
 #pragma unroll
