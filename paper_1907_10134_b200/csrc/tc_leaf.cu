@@ -22,8 +22,8 @@
 // round-to-nearest in the epilogue (4 products incl. lo*lo, 2 TMEM reads).
 // Two tiles (slots) are in flight per CTA so one slot's epilogue (tcgen05.ld
 // D -> sum -> scale by d -> tf32 split -> tcgen05.st A) overlaps the other
-// slot's MMAs.  Up-sweep: 2 x 16 epilogue warps, the slot's first warp issues
-// (see tc_leaf_up16_kernel); down-walk: 2 x 8 epilogue warps + 1 issuer warp.
+// slot's MMAs: 2 x 16 epilogue warps per CTA, the slot's first warp issues
+// (tc_leaf_up16_kernel, tc_leaf_down16_kernel).
 // Persistent grid, one CTA per SM.
 #include <algorithm>
 #include <cstdlib>
@@ -36,9 +36,6 @@ namespace {
 constexpr int TH = 64;                    // hidden size of this kernel
 constexpr int TM = 128;                   // chains per tile (UMMA M)
 constexpr int NSLOT = 2;                  // tiles in flight per CTA
-constexpr int EPI_WARPS = 8;               // per tile: 4 lane quarters x 2 column halves
-constexpr int EPI_THREADS = 32 * EPI_WARPS;
-constexpr int NTHREADS = 32 * (EPI_WARPS * NSLOT + 1);   // + one MMA-issuer warp
 constexpr int B_ROWS = 2 * TH;            // B = [W_hi | W_lo] stacked along N
 constexpr int B_BYTES = B_ROWS * TH * 4;  // 32 KB
 constexpr int HCH = 64;                   // steps staged per chunk
@@ -78,9 +75,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(su32(bar)) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -96,45 +90,8 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-// A from TMEM (K-major: row = lane, K along 32-bit columns), B from shared memory
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id,
-                                            uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
-               : "memory");
-}
 
-// 32 consecutive fp32 TMEM columns of this thread's lane
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
 
 __device__ __forceinline__ float tf32_rn(float x) {
   uint32_t r;
@@ -156,20 +113,6 @@ __device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, fl
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(sdst)), "l"(gsrc) : "memory");
-}
-// x -> (x_hi, x_lo) into this lane's A_hi / A_lo TMEM columns (K-half kh):
-// x_hi = x truncated to tf32 (x & ~0x1FFF), x_lo = rn_tf32(x - x_hi) (ties
-// away; x - x_hi is exact), integer ops only
-__device__ __forceinline__ void split_store(uint32_t t_ahi, uint32_t t_alo, int kh, const float (&x)[32]) {
-  uint32_t hi[32], lo[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    hi[k] = __float_as_uint(x[k]) & 0xFFFFE000u;
-    lo[k] = (__float_as_uint(x[k] - __uint_as_float(hi[k])) + 0x1000u) & 0xFFFFE000u;
-  }
-  tmem_st32(t_ahi + 32 * kh, hi);
-  tmem_st32(t_alo + 32 * kh, lo);
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -388,7 +331,9 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up16_kernel(LeafArgs a,
 #ifndef BPPSA_TRACE_NO_MMA
           mma16_commit(slot_base, bdesc, su32(&d_full[g]));
 #else
-          if (lane == 0) mma_commit(&d_full[g]);
+          if (lane == 0)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             su32(&d_full[g])) : "memory");
           __syncwarp();
 #endif
           if (lane == 0) lock_release(lock_s);
@@ -437,46 +382,67 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up16_kernel(LeafArgs a,
 }
 
 // ---------------------------------------------------------------------------
-// Level-0 DOWN-sweep on the tensor cores: every block (b, q) is a vector chain
-// walked from its carry (exclusive prefix; the seed for the head block):
-//     grad_h[t(s)] = v;  v <- J_{t(s)}^T v = W^T (d_t o v)
-// A tile = 128 chains of arbitrary (b, q) (each with its own time window), so
-// each thread streams its own h half-row: a private 2-stage cp.async ring, no
-// barriers.  Same MMA scheme as the up-sweep (16 N = 128 MMAs per step).
+// Level-0 DOWN-walk, 2 x 16 epilogue warps (thread = chain row x 16-column
+// group), same MMA issue scheme as the up-sweep.  Chains are ordered q-major
+// (id = q*B + b) so a tile's h rows at one step are a few runs of consecutive
+// samples; each chain's h row for step st+1 is fetched with one 256-byte
+// cp.async.bulk by the row's owner thread while step st computes (2-stage ring
+// per slot, rows at a 272-byte stride so the column-slice reads are
+// conflict-free), completion counted by an mbarrier with expect_tx.  grad_h is
+// written from registers.  The D-ready and h-ready waits share one barrier.
 // ---------------------------------------------------------------------------
-constexpr int OFF_RING = OFF_B + B_BYTES;                     // [slot][row][kh][2 stages][32 floats]
-constexpr int RING_BYTES = NSLOT * TM * 2 * 2 * 32 * 4;       // 128 KB
-constexpr int OFF_BAR_D = OFF_RING + RING_BYTES;
-constexpr int SMEM_BYTES_D = OFF_BAR_D + 64 + 1024;
+constexpr int DROW = TH * 4 + 16;                          // padded h row in the ring
+constexpr int DSTAGE = TM * DROW;                          // 34816 B
+constexpr int OFF_RING16 = OFF_B + B_BYTES;                // [slot][2 stages][128 rows][DROW]
+constexpr int OFF_BAR_D16 = OFF_RING16 + NSLOT * 2 * DSTAGE;   // d_full[2], h_full[2][2], tmem, lock
+constexpr int SMEM_BYTES_D16 = OFF_BAR_D16 + 128 + 1024;
 
-__global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_down_kernel(LeafArgs a, int C, const float* __restrict__ carry,
-                                                                   long long nblk, float* __restrict__ grad_h,
-                                                                   float* __restrict__ grad_init) {
+__device__ __forceinline__ void bulk_row(uint32_t dst, const float* src, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];\n" ::"r"(dst),
+               "l"(src), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
+                   bar), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_down16_kernel(LeafArgs a, int C, const float* __restrict__ carry,
+                                                                       long long nblk, float* __restrict__ grad_h,
+                                                                       float* __restrict__ grad_init) {
   extern __shared__ uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR_D);
-  uint64_t* d_full = a_full + NSLOT;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR_D16);
+  uint64_t* h_full = d_full + NSLOT;                                    // [slot][stage]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_full + 2 * NSLOT);
+  int* issue_lock = reinterpret_cast<int*>(tmem_slot + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int B = a.seg.B;
   const long long S = a.seg.S();
   const long long nchains = (long long)B * nblk;
   const long long ntiles = (nchains + TM - 1) / TM;
+  const long long rowB = (long long)B * TH;
 
-  for (int e = threadIdx.x; e < TH * TH; e += NTHREADS) {
+  for (int e = threadIdx.x; e < TH * TH; e += NTHREADS16) {
     const int n = e / TH, k = e % TH;               // B[n][k] = W[k][n]: rows 0..63 hi, 64..127 lo
     const float w = __ldg(a.W + (long long)k * TH + n);
     const float hi = tf32_rn(w);
     *reinterpret_cast<float*>(smem + OFF_B + sw_off(n, k, B_ROWS)) = hi;
     *reinterpret_cast<float*>(smem + OFF_B + sw_off(TH + n, k, B_ROWS)) = tf32_rn(w - hi);
   }
-  const int mma_warp = EPI_WARPS * NSLOT;
-  if (warp == mma_warp) {
+  if (warp == 0) {
     if (lane == 0) {
       for (int s = 0; s < NSLOT; ++s) {
-        mbar_init(&a_full[s], EPI_THREADS);
         mbar_init(&d_full[s], 1);
+        for (int st = 0; st < 2; ++st) mbar_init(&h_full[2 * s + st], TM);   // one arrival per chain row
       }
+      *issue_lock = 0;
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
@@ -488,130 +454,133 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_leaf_down_kernel(LeafArgs a, i
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
-  if (warp == mma_warp) {
-    uint32_t pha[NSLOT] = {0, 0};
-    const uint32_t bb = su32(smem + OFF_B);
-    long long done[NSLOT] = {0, 0}, tau[NSLOT];
-    bool live[NSLOT];
-    for (int sl = 0; sl < NSLOT; ++sl) {
-      tau[sl] = 2 * (long long)blockIdx.x + sl;
-      live[sl] = tau[sl] < ntiles;
-    }
-    while (live[0] || live[1]) {
-      for (int sl = 0; sl < NSLOT; ++sl) {
-        if (!live[sl]) continue;
-        mbar_wait(&a_full[sl], pha[sl]);
-        pha[sl] ^= 1;
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t d = tmem + 256 * sl, a_hi = d + 128, a_lo = d + 192;
+  const int g = warp / EPI16_WARPS, wl = warp % EPI16_WARPS;
+  const int row = (wl & 3) * 32 + lane;
+  const int cgp = wl >> 2;
+  const bool issuer = wl == 0, owner = cgp == 0;          // owner: fetches the row's h
+  const uint32_t slot_base = tmem + 256 * g;
+  const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
+  const uint32_t t_dh = lane_base + 16 * cgp, t_dl = t_dh + 64;
+  const uint32_t t_ahi = lane_base + 128 + 16 * cgp, t_alo = lane_base + 192 + 16 * cgp;
+  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem + OFF_B), 0);
+  const uint32_t ring = su32(smem + OFF_RING16) + (uint32_t)(g * 2 * DSTAGE);
+  const uint32_t lock_s = su32(issue_lock);
+  const uint32_t dbar = su32(&d_full[g]), hbar0 = su32(&h_full[2 * g]);
+  uint64_t bdesc[TH / 8];
 #pragma unroll
-          for (int pq = 0; pq < 2; ++pq) {
-            const uint32_t aa = pq == 0 ? a_lo : a_hi;
-#pragma unroll
-            for (int kk = 0; kk < TH / 8; ++kk) {
-              const uint32_t boff = (uint32_t)((kk >> 2) * B_ROWS * 128 + (kk & 3) * 32);
-              mma_tf32_ts(d, aa + 8 * kk, sdesc(bb + boff), IDESC128, (pq | kk) != 0);
-            }
-          }
-          mma_commit(&d_full[sl]);
-        }
-        __syncwarp();
-        if (++done[sl] == C) {
-          done[sl] = 0;
-          tau[sl] += 2 * (long long)gridDim.x;
-          live[sl] = tau[sl] < ntiles;
-        }
-      }
-    }
-  } else {
-    const int g = warp / EPI_WARPS, wl = warp % EPI_WARPS;
-    const int row = (wl & 3) * 32 + lane;
-    const int kh = wl >> 2;
-    const uint32_t lane_base = tmem + ((uint32_t)((wl & 3) * 32) << 16) + 256 * g;
-    const uint32_t t_d = lane_base + 32 * kh, t_ahi = lane_base + 128, t_alo = lane_base + 192;
-    float* ring = reinterpret_cast<float*>(smem + OFF_RING) + ((g * TM + row) * 2 + kh) * 2 * 32;
-    const uint32_t ring_s = su32(ring);
-    uint32_t ph = 0;
-    const long long rowB = (long long)B * TH;
-    for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
-      const long long id = tau * TM + row;
-      const bool valid = id < nchains;
-      const int b = valid ? (int)(id / nblk) : 0;
-      const long long q = valid ? id % nblk : 0;
-      const bool head = a.seg.head && q == 0;
-      const long long s_start = head ? 1 : q * C, s1 = min(q * C + C, S);
-      const long long len = valid ? s1 - s_start : 0;
-      const bool total = valid && grad_init != nullptr && s1 == S;
-      float c[32];
+  for (int kk = 0; kk < TH / 8; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)((kk >> 2) * B_ROWS * 128 + (kk & 3) * 32));
+  uint32_t dph = 0, gs = 0;                                // D phase; global step count of this slot (h ring)
+
+  for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+    const long long id = tau * TM + row;
+    const bool valid = id < nchains;
+    const long long q = valid ? id / B : 0;
+    const int b = valid ? (int)(id % B) : 0;
+    const bool head = a.seg.head && q == 0;
+    const long long s_start = head ? 1 : q * C, s1 = min(q * C + C, S);
+    const int len = valid ? (int)(s1 - s_start) : 0;
+    const bool total = valid && grad_init != nullptr && s1 == S;
+    const float* hb = a.h + (long long)b * TH;
+    float* gb = grad_h + (long long)b * TH + 16 * cgp;
+    float c[16];
+    {
       const float* src0 = head ? a.seed + (long long)b * TH : carry + ((long long)b * nblk + q) * TH;
 #pragma unroll
-      for (int k4 = 0; k4 < 8; ++k4) {
-        const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(src0 + 32 * kh) + k4)
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(src0 + 16 * cgp) + k4)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
         c[4 * k4] = v.x; c[4 * k4 + 1] = v.y; c[4 * k4 + 2] = v.z; c[4 * k4 + 3] = v.w;
       }
-      auto prefetch = [&](long long st) {      // h row of step st into ring stage st & 1
-        if (st < len) {
-          const float* hp = a.h + (long long)a.seg.time_of(s_start + st) * rowB + (long long)b * TH + 32 * kh;
+    }
+    // h row of step 0 into stage gs & 1
+    if (owner) {
+      const uint32_t bar = hbar0 + 8u * (gs & 1);
+      if (len > 0) {
+        mbar_arrive_tx(bar, 256);
+        bulk_row(ring + (gs & 1) * DSTAGE + row * DROW, hb + (long long)a.seg.time_of(s_start) * rowB, bar);
+      } else {
+        mbar_arrive_s(bar);
+      }
+    }
+    if (issuer) {
+      if (lane == 0) mbar_wait_s(hbar0 + 8u * (gs & 1), (gs >> 1) & 1);
+      __syncwarp();
+    }
+    named_bar(5 + g, EPI16_THREADS);
+    for (int st = 0; st < C; ++st, ++gs) {
+      const bool active = st < len;
+      if (active) {                                  // exclusive output: grad_h[t(s)] = v before J_{t(s)}^T
+        float4* gp = reinterpret_cast<float4*>(gb + (long long)a.seg.time_of(s_start + st) * rowB);
 #pragma unroll
-          for (int k4 = 0; k4 < 8; ++k4) cp_async16(ring + (st & 1) * 32 + 4 * k4, hp + 4 * k4);
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-      };
-      prefetch(0);
-      for (long long st = 0; st < C; ++st) {
-        prefetch(st + 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        const bool active = st < len;
-        float dv[32];
-        if (active) {
-          float* gp = grad_h + (long long)a.seg.time_of(s_start + st) * rowB + (long long)b * TH + 32 * kh;
-#pragma unroll
-          for (int k4 = 0; k4 < 8; ++k4)
-            reinterpret_cast<float4*>(gp)[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
-#pragma unroll
-          for (int k4 = 0; k4 < 8; ++k4) {
-            const float4 h4 = lds128(ring_s + 4u * ((st & 1) * 32 + 4 * k4));
-            dv[4 * k4] = 1.f - h4.x * h4.x; dv[4 * k4 + 1] = 1.f - h4.y * h4.y;
-            dv[4 * k4 + 2] = 1.f - h4.z * h4.z; dv[4 * k4 + 3] = 1.f - h4.w * h4.w;
-          }
+        for (int k4 = 0; k4 < 4; ++k4) gp[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+      }
+      if (owner && st + 1 < C) {                     // prefetch step st+1 (its stage was read at step st-1)
+        const uint32_t nb = gs + 1;
+        const uint32_t bar = hbar0 + 8u * (nb & 1);
+        if (st + 1 < len) {
+          mbar_arrive_tx(bar, 256);
+          bulk_row(ring + (nb & 1) * DSTAGE + row * DROW, hb + (long long)a.seg.time_of(s_start + st + 1) * rowB, bar);
         } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) dv[k] = 0.f;
-        }
-        float x[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) x[k] = dv[k] * c[k];
-        split_store(t_ahi, t_alo, kh, x);
-        tc_fence_before();
-        mbar_arrive(&a_full[g]);
-        mbar_wait(&d_full[g], ph);
-        ph ^= 1;
-        tc_fence_after();
-        float t[32];
-        tmem_ld32(t_d, c);
-        tmem_ld32(t_d + 64, t);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) c[k] += t[k];
-        if (total && st == len - 1) {          // inclusive extra: J_{t(S-1)}^T grad_h[t(S-1)]
-          float4* dst = reinterpret_cast<float4*>(grad_init + (long long)b * TH + 32 * kh);
-#pragma unroll
-          for (int k4 = 0; k4 < 8; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+          mbar_arrive_s(bar);
         }
       }
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      uint32_t hi[16], lo[16];
+      const uint32_t hrow = ring + (gs & 1) * DSTAGE + row * DROW + 64u * cgp;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        float4 h4 = lds128(hrow + 16u * q4);
+        if (!active) h4 = make_float4(1.f, 1.f, 1.f, 1.f);   // d = 0: an idle row contributes nothing
+        const float x4[4] = {(1.f - h4.x * h4.x) * c[4 * q4], (1.f - h4.y * h4.y) * c[4 * q4 + 1],
+                             (1.f - h4.z * h4.z) * c[4 * q4 + 2], (1.f - h4.w * h4.w) * c[4 * q4 + 3]};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hi[4 * q4 + e] = __float_as_uint(x4[e]) & 0xFFFFE000u;
+          lo[4 * q4 + e] = (__float_as_uint(x4[e] - __uint_as_float(hi[4 * q4 + e])) + 0x1000u) & 0xFFFFE000u;
+        }
+      }
+      tmem_st16(t_ahi, hi);
+      tmem_st16(t_alo, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tc_fence_before();
+      named_bar(3 + g, EPI16_THREADS);               // the slot's A is complete (and stage gs&1 consumed)
+      if (issuer) {
+        tc_fence_after();
+        if (lane == 0) lock_acquire(lock_s);
+        __syncwarp();
+        mma16_commit(slot_base, bdesc, dbar);
+        if (lane == 0) {
+          lock_release(lock_s);
+          mbar_wait_s(dbar, dph);
+          if (st + 1 < C) mbar_wait_s(hbar0 + 8u * ((gs + 1) & 1), ((gs + 1) >> 1) & 1);
+        }
+        __syncwarp();
+      }
+      named_bar(5 + g, EPI16_THREADS);               // D of step st and h of step st+1 are ready
+      dph ^= 1;
+      tc_fence_after();
+      float t[16];
+      tmem_ld16(t_dh, c);
+      tmem_ld16(t_dl, t);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < 16; ++k) c[k] += t[k];
+      if (total && st == len - 1) {                  // inclusive extra: J_{t(S-1)}^T grad_h[t(S-1)]
+        float4* dst = reinterpret_cast<float4*>(grad_init + (long long)b * TH + 16 * cgp);
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) dst[k4] = make_float4(c[4 * k4], c[4 * k4 + 1], c[4 * k4 + 2], c[4 * k4 + 3]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == EPI_WARPS * NSLOT) {
+  if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
+
 }  // namespace
 
 // Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.
@@ -635,15 +604,16 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
 // Level-0 down-walk of an RNN H = 64 segment on the tensor cores.
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                                 float* grad_init, int num_sms, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_leaf_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES_D);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
   const int grid = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
-  tc_leaf_down_kernel<<<grid, NTHREADS, SMEM_BYTES_D, st>>>(a, C, carry, nblk, grad_h, grad_init);
+  static bool attr16 = false;
+  if (!attr16) {
+    cudaError_t e = cudaFuncSetAttribute(tc_leaf_down16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES_D16);
+    if (e != cudaSuccess) return e;
+    attr16 = true;
+  }
+  tc_leaf_down16_kernel<<<grid, NTHREADS16, SMEM_BYTES_D16, st>>>(a, C, carry, nblk, grad_h, grad_init);
   return cudaGetLastError();
 }
 
