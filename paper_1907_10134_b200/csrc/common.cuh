@@ -71,9 +71,10 @@ struct LeafArgs {            // implicit leaves (RNN / GRU)
 // level-0 fold: blocks q in [q0, q0+nq) of C slots -> agg_out [B][n_out][H*H] (column-major)
 cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
                            long long nq, cudaStream_t st);
-// same on the tensor cores (tcgen05, 3xTF32): RNN, H == 64, matrix blocks q in [q0, n_out)
+// same on the tensor cores (tcgen05): RNN, H == 64, matrix blocks q in [q0, n_out);
+// prec 0 = 3xFP16 with per-chain scaling, 1 = 3xTF32
 cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
-                              int num_sms, cudaStream_t st);
+                              int num_sms, cudaStream_t st, int prec);
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                                 float* grad_init, int num_sms, cudaStream_t st);
 // level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable

@@ -28,6 +28,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace bppsa {
@@ -581,15 +583,659 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_down16_kernel(LeafArgs 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Level-0 UP-sweep on kind::f16 (3xFP16 with per-chain power-of-two scaling).
+//
+// fp16 has tf32's 11 significant bits but runs at twice the tensor rate, so a
+// 2-term split x = x1 + x2, W = W1 + W2 gives the same 22-bit products as
+// 3xTF32 for half the MMA time — provided every operand sits in fp16's
+// exponent range.  W is scaled once by 2^sw (max |W| 2^sw in [2^14, 2^15)).
+// Every chain row is rescaled at every step by a power of two 2^s chosen from
+// a BOUND on the row's new maximum, known before the step's data:
+//     |x'_s|_inf <= dmax_s * |c'_s|_inf <= dmax_s * G * M_{s-1}
+// (d = 1 - h^2 in [0, 1]; dmax_s = max_k d_s[k] of the sample, computed when
+// h is staged; G = max_n sum_k |B[n][k]| of the scaled W; M_{s-1} = the exact
+// row maximum of the previous scaled operand, exchanged between the row's four
+// threads through shared memory WITHOUT a barrier of its own — the step's
+// MMA barriers order it, double-buffered by step parity).  So x^ = x' 2^s <
+// 2^15 always (no fp16 overflow) and, for random W, its maximum sits near
+// 2^11: x1 is normal for entries down to 2^-24 of it and the absolute error
+// of anything smaller stays below 2^-35 of the row maximum.
+// The scaled chain c' = c 2^E keeps its exponent E (an integer per row, the
+// same in the row's four threads); the aggregate is written as c' 2^-E.
+// Per step and tile: 8 MMAs M128 N128 K16 (A2 then A1 against [W1 | W2]);
+// measured 76 cycles each (scripts/tc_f16_probe.cu) against 16 x 64 for the
+// tf32 form.  A1 / A2 are packed f16x2 in TMEM (even k in the low half).
+// ---------------------------------------------------------------------------
+constexpr int F_B_BYTES = 2 * TH * TH * 2;                 // [W1 | W2]: 128 rows x 64 fp16 = 16 KB
+constexpr int F_OFF_H = F_B_BYTES;
+constexpr int F_OFF_RED = F_OFF_H + NSLOT * H_BYTES;       // [slot][parity][128 rows][4 column groups] u32
+constexpr int F_OFF_DMX = F_OFF_RED + NSLOT * 2 * TM * 16; // [slot][2 samples][HCH] dmax
+constexpr int F_OFF_BAR = F_OFF_DMX + NSLOT * 2 * HCH * 4;
+constexpr int F_SMEM_BYTES = F_OFF_BAR + 64 + 1024;
+__host__ __device__ constexpr uint32_t idesc_f16(int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);   // D f32, A/B f16, K-major
+}
+constexpr uint32_t IDESC_F16 = idesc_f16(128);
+
+// element (row, k) of a K-major SWIZZLE_128B fp16 tile with K = 64 (one 128-byte row per row)
+__device__ __forceinline__ uint32_t sw16_off(int row, int k) {
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + (((k >> 3) ^ (row & 7)) << 4) + (k & 7) * 2);
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+// A2 (corrections) then A1, K = 64 in 16-wide steps, B = [W1 | W2]; one
+// elected stream of the converged issuer warp (see mma16_commit)
+__device__ __forceinline__ void mma8_f16_commit(uint32_t d, const uint64_t (&bd)[4], uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 a;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %5, f;\n"
+      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
+      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
+      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
+      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %5, t;\n"
+      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
+      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
+      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
+      "}\n" ::"r"(d),
+      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// W exponent shift sw (max |W| 2^sw in [2^14, 2^15), clamped: W = 0 gives a
+// harmless shift) and G = max_n sum_k |W[k][n]| 2^sw (rounded up by 2^-8).
+// Called by all threads; red[0..1] are zeroed shared words.
+__device__ __forceinline__ void w_scale(const float* W, uint32_t* red, int* sw_out, float* G_out) {
+  uint32_t m = 0;
+  for (int e = threadIdx.x; e < TH * TH; e += blockDim.x) m = max(m, __float_as_uint(fabsf(__ldg(W + e))));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(red, m);
+  __syncthreads();
+  const int sw = max(-100, min(100, 141 - (int)(red[0] >> 23)));
+  uint32_t gs = 0;
+  if (threadIdx.x < TH) {
+    float acc = 0.f;
+    for (int k = 0; k < TH; ++k) acc += fabsf(__ldg(W + (long long)k * TH + threadIdx.x));
+    gs = __float_as_uint(ldexpf(acc, sw) * (1.f + 1.f / 256.f));
+  }
+  gs = __reduce_max_sync(0xffffffffu, gs);
+  if ((threadIdx.x & 31) == 0 && threadIdx.x < TH) atomicMax(red + 1, gs);
+  __syncthreads();
+  *sw_out = sw;
+  *G_out = __uint_as_float(red[1]);
+}
+
+__global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                       long long n_out, long long q0) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + F_OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  int* issue_lock = reinterpret_cast<int*>(tmem_slot + 1);
+  uint32_t* wred = reinterpret_cast<uint32_t*>(issue_lock + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nq = n_out - q0;
+  const int nbp = (B + 1) / 2;
+  const long long ntiles = (long long)nbp * nq;
+
+  if (threadIdx.x < 2) wred[threadIdx.x] = 0;
+  __syncthreads();
+  int sw;
+  float G;
+  w_scale(a.W, wred, &sw, &G);
+  {
+    const float wsc = __int_as_float((sw + 127) << 23);
+    for (int e = threadIdx.x; e < TH * TH; e += NTHREADS16) {
+      const int n = e / TH, k = e % TH;             // B[n][k] = W[k][n] 2^sw: rows 0..63 W1, 64..127 W2
+      const float w = __ldg(a.W + (long long)k * TH + n) * wsc;
+      const __half w1 = __float2half_rn(w);
+      *reinterpret_cast<__half*>(smem + sw16_off(n, k)) = w1;
+      *reinterpret_cast<__half*>(smem + sw16_off(TH + n, k)) = __float2half_rn(w - __half2float(w1));
+    }
+  }
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) mbar_init(&d_full[s], 1);
+      *issue_lock = 0;
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int g = warp / EPI16_WARPS, wl = warp % EPI16_WARPS;
+  const int row = (wl & 3) * 32 + lane;
+  const int cgp = wl >> 2;
+  const int et = wl * 32 + lane;
+  const bool issuer = wl == 0;
+  const uint32_t slot_base = tmem + 256 * g;
+  const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
+  const uint32_t t_d1 = lane_base + 16 * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_a1 = lane_base + 128 + 8 * cgp, t_a2 = lane_base + 160 + 8 * cgp;
+  float* hs = reinterpret_cast<float*>(smem + F_OFF_H + g * H_BYTES);
+  const uint32_t hs_s = su32(hs);
+  float* dmx = reinterpret_cast<float*>(smem + F_OFF_DMX) + g * 2 * HCH;       // [2 samples][HCH]
+  const uint32_t red0 = su32(smem + F_OFF_RED) + (uint32_t)(((g * 2) * TM + row) * 16);   // parity 0 row word
+  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+  const uint32_t lock_s = su32(issue_lock);
+  uint64_t bdesc[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  uint32_t ph = 0, par = 0;                        // D phase; parity of the max exchange buffer
+#ifdef BPPSA_STEP_TRACE
+  int tstep = 0;
+#endif
+  const long long rowB = (long long)B * TH;
+  for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+    const long long q = q0 + tau / nbp;
+    const int bp = (int)(tau % nbp);
+    const int b = bp * 2 + (row >> 6);
+    const int j = row & 63;
+    const bool ok = b < B;
+    const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+    float2 c2[8];                                  // c' = c 2^E (pairs of columns)
+    int E = 0;
+    float bound = 1.f / G;                         // G * bound = |c'_0|_inf bound (one-hot start)
+    bool first = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      c2[i] = make_float2((16 * cgp + 2 * i == j && ok) ? 1.f : 0.f, (16 * cgp + 2 * i + 1 == j && ok) ? 1.f : 0.f);
+    for (long long sc = s0; sc < s1; sc += HCH) {
+      const int n = (int)min((long long)HCH, s1 - sc);
+      named_bar(1 + g, EPI16_THREADS);             // previous chunk fully consumed (d is read into registers)
+      for (int e = et; e < 2 * n * 16; e += EPI16_THREADS) {
+        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+        float* dst = hs + (bb2 * HCH + st) * TH + ch * 4;
+        const int bs = bp * 2 + bb2;
+        if (bs < B)
+          cp_async16(dst, a.h + (long long)a.seg.time_of(sc + st) * rowB + (long long)bs * TH + ch * 4);
+        else
+          sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      // d = 1 - h^2 in place and dmax per (sample, step): 16 consecutive lanes
+      // hold one 64-wide row (2n*16 is a multiple of 32: whole warps iterate)
+      for (int e = et; e < 2 * n * 16; e += EPI16_THREADS) {
+        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+        const uint32_t p = hs_s + 4u * ((bb2 * HCH + st) * TH + ch * 4);
+        const float4 h4 = lds128(p);
+        const float4 d4 = make_float4(1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
+        sts128(p, d4.x, d4.y, d4.z, d4.w);
+        float m = fmaxf(fmaxf(d4.x, d4.y), fmaxf(d4.z, d4.w));
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (ch == 0) dmx[bb2 * HCH + st] = m;
+      }
+      named_bar(1 + g, EPI16_THREADS);
+      uint32_t dp = hs_s + 4u * ((row >> 6) * HCH * TH + 16 * cgp);   // this thread's d slice of step st
+      uint32_t dmp = su32(dmx + (row >> 6) * HCH);                      // dmax of step st
+      for (int st = 0; st < n; ++st, dp += 4u * TH, dmp += 4u) {
+        STEP_TRACE(0);
+        // (overlaps the previous step's MMAs) scale 2^s from the bound
+        // dmax_s * G * M_{s-1}, folded into d: ds = d 2^s
+        float dms;
+        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(dms) : "r"(dmp));
+        const float f = G * bound * dms;
+        const int s = min(127, 141 - (int)(__float_as_uint(f) >> 23));
+        const float2 scl = make_float2(__int_as_float((s + 127) << 23), __int_as_float((s + 127) << 23));
+        E += s + sw;
+        float2 ds[8];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 d4 = lds128(dp + 16u * q4);
+          ds[2 * q4] = __fmul2_rn(make_float2(d4.x, d4.y), scl);
+          ds[2 * q4 + 1] = __fmul2_rn(make_float2(d4.z, d4.w), scl);
+        }
+        if (!first) {                              // D of the previous step
+          if (issuer) {
+            STEP_TRACE(6);
+            if (lane == 0) mbar_wait(&d_full[g], ph);
+            STEP_TRACE(7);
+            __syncwarp();
+          }
+          named_bar(5 + g, EPI16_THREADS);
+          ph ^= 1;
+          tc_fence_after();
+          STEP_TRACE(4);
+          float t1[16], t2[16];
+          tmem_ld16(t_d1, t1);
+#ifndef EXP_NO_D2
+          tmem_ld16(t_d2, t2);
+#else
+          for (int i = 0; i < 16; ++i) t2[i] = 0.f;
+#endif
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          STEP_TRACE(5);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            c2[i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
+        }
+        first = false;
+        float pm = 0.f;
+        uint32_t p1[8], p2[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 x = __fmul2_rn(c2[i], ds[i]);
+          pm = fmaxf(pm, fmaxf(fabsf(x.x), fabsf(x.y)));
+          // x1 = x truncated to 11 significant bits (exact in fp16 for |x| >= 2^-14;
+          // below that the conversion rounds at 2^-25, < 2^-36 of the row maximum)
+          const float2 f1 = make_float2(__uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                                        __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
+          const float2 r = __fadd2_rn(x, make_float2(-f1.x, -f1.y));
+          p1[i] = h2_bits(__floats2half2_rn(f1.x, f1.y));
+          p2[i] = h2_bits(__floats2half2_rn(r.x, r.y));
+        }
+        const uint32_t redp = red0 + par * (TM * 16);
+        asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+        tmem_st8(t_a1, p1);
+#ifndef EXP_NO_A2
+        tmem_st8(t_a2, p2);
+#endif
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        STEP_TRACE(1);
+        tc_fence_before();
+        named_bar(3 + g, EPI16_THREADS);           // the slot's A and the row maxima are complete
+        STEP_TRACE(2);
+        if (issuer) {
+          tc_fence_after();
+          mma8_f16_commit(slot_base, bdesc, su32(&d_full[g]));
+          STEP_TRACE(3);
+        }
+        uint32_t m4[4];
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                     : "=r"(m4[0]), "=r"(m4[1]), "=r"(m4[2]), "=r"(m4[3])
+                     : "r"(redp)
+                     : "memory");
+        bound = __uint_as_float(max(max(m4[0], m4[1]), max(m4[2], m4[3])));
+        par ^= 1;
+#ifdef BPPSA_STEP_TRACE
+        ++tstep;
+#endif
+      }
+    }
+    // D of the tile's last step
+    if (issuer) {
+      if (lane == 0) mbar_wait(&d_full[g], ph);
+      __syncwarp();
+    }
+    named_bar(5 + g, EPI16_THREADS);
+    ph ^= 1;
+    tc_fence_after();
+    {
+      float t1[16], t2[16];
+      tmem_ld16(t_d1, t1);
+      tmem_ld16(t_d2, t2);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        c2[i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
+    }
+    if (ok) {
+      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 16 * cgp);
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4)
+        dst[k4] = make_float4(ldexpf(c2[2 * k4].x, -E), ldexpf(c2[2 * k4].y, -E), ldexpf(c2[2 * k4 + 1].x, -E),
+                              ldexpf(c2[2 * k4 + 1].y, -E));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Same fold, all 32 warps on ONE tile at a time: two tiles (slots X, Y) of a
+// pair advance in lockstep and their epilogues alternate, so MMA X runs while
+// every warp works on epilogue Y and vice versa (thread = chain row x 8
+// columns).  Per tile-step: bar BD (D ready; the issuer warp polls the
+// commit barrier, then joins) -> LDTM -> 3xFP16 split -> STTM -> bar.arrive
+// BA (A ready; only the issuer warp waits, then issues).  The row maximum of
+// a tile's scaled operand (8 partials per row) is read after the next BD of
+// the other tile, which orders it; the scale of the next step is computed
+// while that tile's MMA still runs.
+// ---------------------------------------------------------------------------
+constexpr int P_THREADS = 1024;
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+
+struct PTile {              // per-thread state of one tile of the pair
+  float2 c[4];              // c' = c 2^E, this thread's 8 columns
+  float bound;              // M_{s-1} (row max of the previous scaled operand), or 1/G at the start
+  int E;
+  int len;                  // steps of this tile (0: no tile)
+};
+
+// scale of step st from the bound, folded into d: ds = d 2^s (E += s + sw)
+__device__ __forceinline__ void p_scale(PTile& T, uint32_t dp, uint32_t dmp, float G, int sw, float2 (&ds)[4]) {
+  float dms;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(dms) : "r"(dmp));
+  const int s = min(127, 141 - (int)(__float_as_uint(G * T.bound * dms) >> 23));
+  const float sc = __int_as_float((s + 127) << 23);
+  T.E += s + sw;
+  const float4 d0 = lds128(dp), d1 = lds128(dp + 16u);
+  ds[0] = __fmul2_rn(make_float2(d0.x, d0.y), make_float2(sc, sc));
+  ds[1] = __fmul2_rn(make_float2(d0.z, d0.w), make_float2(sc, sc));
+  ds[2] = __fmul2_rn(make_float2(d1.x, d1.y), make_float2(sc, sc));
+  ds[3] = __fmul2_rn(make_float2(d1.z, d1.w), make_float2(sc, sc));
+}
+
+// c' <- D1 + D2 (the tile's accumulator halves)
+__device__ __forceinline__ void p_load_d(PTile& T, uint32_t t_d) {
+  float t1[8], t2[8];
+  tmem_ld8(t_d, t1);
+  tmem_ld8(t_d + 64, t2);
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    T.c[i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
+}
+
+// x^ = c' o ds split into fp16 pairs -> A1 / A2 in TMEM; partial row max -> red
+__device__ __forceinline__ void p_split_store(const PTile& T, const float2 (&ds)[4], uint32_t t_a, uint32_t red_w) {
+  float pm = 0.f;
+  uint32_t p1[4], p2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __fmul2_rn(T.c[i], ds[i]);
+    pm = fmaxf(pm, fmaxf(fabsf(x.x), fabsf(x.y)));
+    const __half2 h1 = __floats2half2_rn(x.x, x.y);
+    const float2 f1 = __half22float2(h1);
+    const float2 r = __fadd2_rn(x, make_float2(-f1.x, -f1.y));
+    p1[i] = h2_bits(h1);
+    p2[i] = h2_bits(__floats2half2_rn(r.x, r.y));
+  }
+  asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(red_w), "r"(__float_as_uint(pm)) : "memory");
+  tmem_st4(t_a, p1);
+  tmem_st4(t_a + 32, p2);
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ float p_row_max(uint32_t red_row) {
+  uint32_t m[8];
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(m[0]), "=r"(m[1]), "=r"(m[2]), "=r"(m[3]) : "r"(red_row) : "memory");
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(m[4]), "=r"(m[5]), "=r"(m[6]), "=r"(m[7]) : "r"(red_row + 16u) : "memory");
+  return __uint_as_float(max(max(max(m[0], m[1]), max(m[2], m[3])), max(max(m[4], m[5]), max(m[6], m[7]))));
+}
+
+__global__ void __launch_bounds__(P_THREADS, 1) tc_leaf_up_f16p_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                       long long n_out, long long q0) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + F_OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  uint32_t* wred = tmem_slot + 2;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nq = n_out - q0;
+  const int nbp = (B + 1) / 2;
+  const long long ntiles = (long long)nbp * nq;
+
+  if (threadIdx.x < 2) wred[threadIdx.x] = 0;
+  __syncthreads();
+  int sw;
+  float G;
+  w_scale(a.W, wred, &sw, &G);
+  {
+    const float wsc = __int_as_float((sw + 127) << 23);
+    for (int e = threadIdx.x; e < TH * TH; e += P_THREADS) {
+      const int n = e / TH, k = e % TH;             // B[n][k] = W[k][n] 2^sw: rows 0..63 W1, 64..127 W2
+      const float w = __ldg(a.W + (long long)k * TH + n) * wsc;
+      const __half w1 = __float2half_rn(w);
+      *reinterpret_cast<__half*>(smem + sw16_off(n, k)) = w1;
+      *reinterpret_cast<__half*>(smem + sw16_off(TH + n, k)) = __float2half_rn(w - __half2float(w1));
+    }
+  }
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) mbar_init(&d_full[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int row = (warp & 3) * 32 + lane;                 // TMEM lane / chain row of both tiles
+  const int cg = warp >> 2;                               // 8-column group
+  const bool issuer = warp == 0;
+  const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t t_d[2] = {lane_base + 8 * cg, lane_base + 256 + 8 * cg};
+  const uint32_t t_a[2] = {lane_base + 128 + 4 * cg, lane_base + 256 + 128 + 4 * cg};
+  const uint32_t hs_s = su32(smem + F_OFF_H);                       // [slot][2 samples][HCH][64] d
+  const uint32_t dmx_s = su32(smem + F_OFF_DMX);                    // [slot][2 samples][HCH] dmax
+  const uint32_t red_s = su32(smem + F_OFF_RED);                    // [slot][128 rows][8] u32
+  const uint32_t red_row[2] = {red_s + (uint32_t)row * 32u, red_s + (uint32_t)(TM + row) * 32u};
+  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+  uint64_t bdesc[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  const uint32_t dbar[2] = {su32(&d_full[0]), su32(&d_full[1])};
+  uint32_t ph[2] = {0, 0};
+  const long long rowB = (long long)B * TH;
+  const int j = row & 63, half = row >> 6;
+#ifdef BPPSA_STEP_TRACE
+  int tstep = -1;
+#define PTRACE(ph)                                                                                 \
+  if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 13) && tstep < 4096)                 \
+    g_step_trace[g][warp == 13][ph][tstep] = clock64();
+#else
+#define PTRACE(ph)
+#endif
+
+  for (long long tau = 2 * (long long)blockIdx.x; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+    PTile T[2];
+    long long qq[2], s0[2];
+    int bpp[2];
+    int nmax = 0;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const long long tt = tau + g;
+      const bool have = tt < ntiles;
+      qq[g] = q0 + (have ? tt / nbp : 0);
+      bpp[g] = have ? (int)(tt % nbp) : 0;
+      s0[g] = qq[g] * C;
+      T[g].len = have ? (int)(min(s0[g] + (long long)C, S) - s0[g]) : 0;
+      T[g].E = 0;
+      T[g].bound = 1.f / G;
+      const bool ok = have && bpp[g] * 2 + half < B;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        T[g].c[i] = make_float2((8 * cg + 2 * i == j && ok) ? 1.f : 0.f, (8 * cg + 2 * i + 1 == j && ok) ? 1.f : 0.f);
+      nmax = max(nmax, T[g].len);
+    }
+    for (int st = 0; st < nmax; ++st) {
+#ifdef BPPSA_STEP_TRACE
+      ++tstep;
+#endif
+      const int ch = st % HCH;
+      if (ch == 0) {                               // stage h -> d (and dmax) of both tiles for HCH steps
+        __syncthreads();                           // every thread's d of the previous chunk is in registers
+        const int n = min(HCH, nmax - st);
+        for (int e = threadIdx.x; e < 2 * 2 * n * 16; e += P_THREADS) {
+          const int g = e / (2 * n * 16), r0 = e % (2 * n * 16);
+          const int bb2 = r0 / (n * 16), rem = r0 % (n * 16), sst = rem / 16, c4 = rem % 16;
+          const uint32_t dst = hs_s + 4u * ((((g * 2) + bb2) * HCH + sst) * TH + c4 * 4);
+          const int bs = (g ? bpp[1] : bpp[0]) * 2 + bb2;
+          if (bs < B && st + sst < (g ? T[1].len : T[0].len))
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                         "l"(a.h + (long long)a.seg.time_of((g ? s0[1] : s0[0]) + st + sst) * rowB +
+                             (long long)bs * TH + c4 * 4)
+                         : "memory");
+          else
+            sts128(dst, 1.f, 1.f, 1.f, 1.f);       // h = 1: d = 0
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        for (int e = threadIdx.x; e < 2 * 2 * n * 16; e += P_THREADS) {   // whole warps: 16 lanes per row
+          const int g = e / (2 * n * 16), r0 = e % (2 * n * 16);
+          const int bb2 = r0 / (n * 16), rem = r0 % (n * 16), sst = rem / 16, c4 = rem % 16;
+          const uint32_t p = hs_s + 4u * ((((g * 2) + bb2) * HCH + sst) * TH + c4 * 4);
+          const float4 h4 = lds128(p);
+          const float4 d4 = make_float4(1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
+          sts128(p, d4.x, d4.y, d4.z, d4.w);
+          float m = fmaxf(fmaxf(d4.x, d4.y), fmaxf(d4.z, d4.w));
+#pragma unroll
+          for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          if (c4 == 0)
+            asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(dmx_s + 4u * (((g * 2) + bb2) * HCH + sst)), "f"(m) : "memory");
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        PTile& Tg = T[g];
+        const bool act = st < Tg.len;
+        PTRACE(0);
+        float2 ds[4];
+        if (act)
+          p_scale(Tg, hs_s + 4u * ((((g * 2) + half) * HCH + ch) * TH + 8 * cg),
+                  dmx_s + 4u * (((g * 2) + half) * HCH + ch), G, sw, ds);
+        const bool had = st > 0 && st - 1 < Tg.len;  // D of this tile's previous step to consume
+        if (issuer && had) {
+          if (lane == 0) mbar_wait_s(dbar[g], ph[g]);
+          __syncwarp();
+        }
+        named_bar(3 + g, P_THREADS);               // BD: D ready; orders the other tile's row maxima
+        PTRACE(1);
+        if (had) {
+          ph[g] ^= 1;
+          tc_fence_after();
+          p_load_d(Tg, t_d[g]);
+        }
+        PTRACE(2);
+        if (g == 1) {
+          if (st < T[0].len) T[0].bound = p_row_max(red_row[0]);              // tile 0, step st
+        } else if (st > 0 && st - 1 < T[1].len) {
+          T[1].bound = p_row_max(red_row[1]);                                 // tile 1, step st-1
+        }
+        if (act) {
+          p_split_store(Tg, ds, t_a[g], red_row[g] + 4u * cg);
+          tc_fence_before();
+        }
+        PTRACE(3);
+        if (issuer) {
+          named_bar(1 + g, P_THREADS);             // every warp's A of this tile is stored
+          if (act) {
+            tc_fence_after();
+            mma8_f16_commit(tmem + 256 * g, bdesc, dbar[g]);
+          }
+        } else {
+          bar_arrive(1 + g, P_THREADS);
+        }
+        PTRACE(4);
+      }
+    }
+    // D of each tile's last step, then the aggregates
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      PTile& Tg = T[g];
+      if (Tg.len > 0) {
+        if (issuer) {
+          if (lane == 0) mbar_wait_s(dbar[g], ph[g]);
+          __syncwarp();
+        }
+        named_bar(3 + g, P_THREADS);
+        ph[g] ^= 1;
+        tc_fence_after();
+        p_load_d(Tg, t_d[g]);
+        const int b = bpp[g] * 2 + half;
+        if (b < B) {
+          float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + qq[g]) * TH + j) * TH + 8 * cg);
+          dst[0] = make_float4(ldexpf(Tg.c[0].x, -Tg.E), ldexpf(Tg.c[0].y, -Tg.E), ldexpf(Tg.c[1].x, -Tg.E),
+                               ldexpf(Tg.c[1].y, -Tg.E));
+          dst[1] = make_float4(ldexpf(Tg.c[2].x, -Tg.E), ldexpf(Tg.c[2].y, -Tg.E), ldexpf(Tg.c[3].x, -Tg.E),
+                               ldexpf(Tg.c[3].y, -Tg.E));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 }  // namespace
 
-// Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.
+// Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.  prec 0: 3xFP16
+// row-scaled (tc_leaf_up_f16_kernel), 1: 3xTF32 (tc_leaf_up16_kernel).
 cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
-                              int num_sms, cudaStream_t st) {
+                              int num_sms, cudaStream_t st, int prec) {
   const long long ntiles = (long long)((a.seg.B + 1) / 2) * (n_out - q0);
   const long long pairs = (ntiles + 1) / 2;
   const int grid = (int)std::min<long long>(pairs, num_sms);
   if (grid <= 0) return cudaSuccess;
+  if (prec == 2) {
+    const int gridp = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
+    static bool attrp = false;
+    if (!attrp) {
+      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           F_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attrp = true;
+    }
+    tc_leaf_up_f16p_kernel<<<gridp, P_THREADS, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+    return cudaGetLastError();
+  }
+  if (prec == 0) {
+    static bool attrf = false;
+    if (!attrf) {
+      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           F_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attrf = true;
+    }
+    tc_leaf_up_f16_kernel<<<grid, NTHREADS16, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+    return cudaGetLastError();
+  }
   static bool attr16 = false;
   if (!attr16) {
     cudaError_t e = cudaFuncSetAttribute(tc_leaf_up16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -10,6 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1907_10134_b200 import api  # noqa: E402
 
+IMPL = os.environ.get("BPPSA_LEAF_IMPL", "auto")
 CFG = {"c4": (1 << 20, 16, 64, 128, 32), "c1": (1000, 16, 20, 8, 8), "c2": (30000, 16, 20, 16, 16),
        "c4s": (1 << 18, 16, 64, 128, 32), "c4b128": (1 << 20, 16, 64, 128, 32), "c4b128c64": (1 << 20, 16, 64, 128, 64),
        "c4c64": (1 << 20, 16, 64, 64, 64), "c4b256": (1 << 20, 16, 64, 256, 32), "c4b512": (1 << 20, 16, 64, 512, 32),
@@ -28,13 +29,13 @@ def run(name, reps=5):
     ws = api.workspace(api.scan_workspace_size(jac, "blocked", C0, C))
     wsw = api.workspace(api.weight_grads_workspace_size(T, B, H, 1))
     for _ in range(2):
-        api.scan(jac, seed, grad_h=grad, ws=ws, block0=C0, block=C)
+        api.scan(jac, seed, grad_h=grad, ws=ws, block0=C0, block=C, leaf_impl=IMPL)
     torch.cuda.synchronize()
     traces = [api.LaunchTrace(32) for _ in range(reps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for t in traces:
-        api.scan(jac, seed, grad_h=grad, ws=ws, block0=C0, block=C, trace=t)
+        api.scan(jac, seed, grad_h=grad, ws=ws, block0=C0, block=C, trace=t, leaf_impl=IMPL)
     e1.record()
     torch.cuda.synchronize()
     tot = e0.elapsed_time(e1) / reps
@@ -47,7 +48,7 @@ def run(name, reps=5):
     w1.record()
     torch.cuda.synchronize()
     flops0 = B * T * 2.0 * H ** 3
-    print(f"{name}: scan {tot:.3f} ms  kernels {[round(k, 3) for k in ks]}  wgrad {w0.elapsed_time(w1) / reps:.3f} ms"
+    print(f"{name} [{IMPL}]: scan {tot:.3f} ms  kernels {[round(k, 3) for k in ks]}  wgrad {w0.elapsed_time(w1) / reps:.3f} ms"
           f"  leaf_up {flops0 / ks[0] / 1e9:.1f} TFLOP/s")
 
 

@@ -7,8 +7,9 @@
 #include <algorithm>
 #include "../paper_1907_10134_b200/csrc/tc_leaf.cu"
 
-int main() {
-  const int T = 1 << 18, B = 16, H = 64, C = 128;
+int main(int argc, char** argv) {
+  const int prec = argc > 1 ? atoi(argv[1]) : 0;   // 0 = 3xFP16, 1 = 3xTF32
+  const int T = 1 << 18, B = 16, H = 64, C = 256;
   std::vector<float> h((size_t)T * B * H), W(H * H);
   unsigned s = 1;
   auto rnd = [&] { s = s * 1664525u + 1013904223u; return (s >> 8) / 16777216.f; };
@@ -24,17 +25,35 @@ int main() {
   a.seg = bppsa::Seg{T, B, H, 0};
   a.kind = BPPSA_JAC_RNN_TANH;
   a.h = dh; a.W = dW;
-  for (int rep = 0; rep < 2; ++rep) bppsa::launch_tc_leaf_up(a, C, dagg, nblk, 0, 148, 0);
+  for (int rep = 0; rep < 2; ++rep) bppsa::launch_tc_leaf_up(a, C, dagg, nblk, 0, 148, 0, prec);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  bppsa::launch_tc_leaf_up(a, C, dagg, nblk, 0, 148, 0);
+  bppsa::launch_tc_leaf_up(a, C, dagg, nblk, 0, 148, 0, prec);
   cudaEventRecord(e1);
   cudaError_t err = cudaDeviceSynchronize();
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  printf("status %s  time %.3f ms (T=%d)\n", cudaGetErrorString(err), ms, T);
+  printf("prec %d status %s  time %.3f ms (T=%d)\n", prec, cudaGetErrorString(err), ms, T);
   static long long tr[2][2][8][4096];
   cudaMemcpyFromSymbol(tr, bppsa::g_step_trace, sizeof(tr));
   const char* names[] = {"start", "A stored", "after bar", "issued", "D ready", "D loaded"};
+  if (prec == 2) {   // pair kernel phases
+    const char* pn[] = {"start", "BD passed", "D loaded", "A stored", "BA done"};
+    for (int g = 0; g < 2; ++g)
+      for (int w = 0; w < 2; ++w) {
+        printf("tile %d warp %s:", g, w ? "13" : "0 ");
+        for (int p = 1; p <= 4; ++p) {
+          std::vector<long long> d;
+          for (int st = 200; st < 3000; ++st) d.push_back(tr[g][w][p][st] - tr[g][w][p - 1][st]);
+          std::sort(d.begin(), d.end());
+          printf("  %s-%s %lld", pn[p - 1], pn[p], d[d.size() / 2]);
+        }
+        std::vector<long long> d;
+        for (int st = 200; st < 3000; ++st) d.push_back(tr[g][w][0][st + 1] - tr[g][w][0][st]);
+        std::sort(d.begin(), d.end());
+        printf("  | step %lld\n", d[d.size() / 2]);
+      }
+    return 0;
+  }
   for (int g = 0; g < 2; ++g)
     for (int w = 0; w < 2; ++w) {
       printf("slot %d warp %s:", g, w ? "13" : "0 ");
@@ -47,7 +66,14 @@ int main() {
       std::vector<long long> d;
       for (int st = 200; st < 3000; ++st) d.push_back(tr[g][w][0][st + 1] - tr[g][w][0][st]);
       std::sort(d.begin(), d.end());
-      printf("  | step %lld\n", d[d.size() / 2]);
+      printf("  | step %lld", d[d.size() / 2]);
+      if (w == 0) {
+        std::vector<long long> l, r;
+        for (int st = 200; st < 3000; ++st) l.push_back(tr[g][0][6][st] - tr[g][0][2][st]), r.push_back(tr[g][0][7][st] - tr[g][0][3][st]);
+        std::sort(l.begin(), l.end()); std::sort(r.begin(), r.end());
+        printf("  | bar->locked %lld  issued->released %lld", l[l.size() / 2], r[r.size() / 2]);
+      }
+      printf("\n");
     }
   // absolute timeline of a few steps: events of both slots (warp 13 = non-issuer; issuer for 'issued')
   {
@@ -62,6 +88,15 @@ int main() {
         }
     std::sort(ev.begin(), ev.end(), [](const Ev& x, const Ev& y) { return x.t < y.t; });
     for (auto& e : ev) printf("  t=%6lld slot %d step %d  %s\n", e.t, e.g, e.st, names[e.p]);
+  }
+  for (int g = 0; g < 2; ++g) {
+    std::vector<long long> a1, a2;
+    for (int st = 200; st < 3000; ++st) {
+      a1.push_back(tr[g][0][7][st + 1] - tr[g][0][3][st]);   // issued (step st) -> poll success (next step)
+      a2.push_back(tr[g][0][7][st + 1] - tr[g][0][6][st + 1]);
+    }
+    std::sort(a1.begin(), a1.end()); std::sort(a2.begin(), a2.end());
+    printf("slot %d: issued -> MMA done seen %lld  (polling time %lld)\n", g, a1[a1.size() / 2], a2[a2.size() / 2]);
   }
   // cross-slot: when slot 1 issues relative to slot 0's D ready
   std::vector<long long> d;

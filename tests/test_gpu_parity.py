@@ -66,21 +66,63 @@ def test_rnn_H_and_block_sweep(lib, H, blocks):
 BIAS_PER_STEP = 16 * 2.0 ** -24
 
 
+TENSOR_IMPLS = ["tensor", "tensor_tf32"]
+
+
+@pytest.mark.parametrize("impl", TENSOR_IMPLS)
 @pytest.mark.parametrize("T", [64, 65, 127, 300, 1000, 5000])
-@pytest.mark.parametrize("blocks", [(0, 0), (16, 4), (32, 8)])
-def test_rnn_tensor_leaf_realistic(lib, T, blocks):
+@pytest.mark.parametrize("blocks", [(0, 0), (16, 4), (32, 8), (256, 32)])
+def test_rnn_tensor_leaf_realistic(lib, T, blocks, impl):
     w = W.rnn_workload(T, 16, 64, seed=T + blocks[0])
     ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
-    grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=blocks[0], block=blocks[1], leaf_impl="tensor")
+    grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=blocks[0], block=blocks[1], leaf_impl=impl)
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
 
 
+@pytest.mark.parametrize("wscale", [1e-20, 1e-3, 1.0])
+def test_rnn_tensor_leaf_scaling_range(lib, wscale):
+    """The 3xFP16 fold rescales W once and every chain row at every step by
+    powers of two: tiny W_hh, saturated steps (d = 0 for a whole
+    sample) and an all-zero chain must keep the fp32 accuracy of the FFMA fold."""
+    T, B, H = 700, 5, 64
+    w = W.rnn_workload(T, B, H, seed=int(-np.log10(wscale)) + 40)
+    Wm = (w.W_hh * wscale).astype(np.float32)
+    h = w.h.copy()
+    h[600:603, 1, :] = 1.0            # d = 0 for sample 1 at three steps
+    h[650, :, ::2] = -1.0             # half the units saturated at one step
+    g = w.g.copy()
+    g[3] = 0.0                        # an all-zero chain
+    ref, ref_init = bp.bp_rnn(h, Wm, g)
+    for C0 in (64, 256):
+        gt, it = run_rnn(lib, h, Wm, g, leaf_impl="tensor", block0=C0)
+        gf, i_f = run_rnn(lib, h, Wm, g, leaf_impl="ffma", block0=C0)
+        et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
+        assert np.isfinite(gt.cpu().numpy()).all()
+        assert et <= max(TOL, 4 * ef), (C0, et, ef)
+
+
+@pytest.mark.parametrize("s", [0.5, 2.0])
+def test_rnn_tensor_leaf_growth_and_decay(lib, s):
+    """Chains that grow (2^k) or shrink (2^-k) every step: block aggregates
+    span 2^+-64 and the per-row exponents E run far from 0."""
+    T, B = 120, 5
+    f = W.norm_preserving_rnn(T, B, 64, seed=int(s * 10))
+    Wm = (f["W_hh"] * s).astype(np.float32)
+    ref, ref_init = bp.bp_rnn(f["h"], Wm, f["g"])
+    for C0 in (16, 64):
+        gt, it = run_rnn(lib, f["h"], Wm, f["g"], leaf_impl="tensor", block0=C0)
+        gf, i_f = run_rnn(lib, f["h"], Wm, f["g"], leaf_impl="ffma", block0=C0)
+        et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
+        assert et <= max(TOL, 4 * ef), (C0, et, ef)
+
+
+@pytest.mark.parametrize("impl", TENSOR_IMPLS)
 @pytest.mark.parametrize("B", [1, 2, 3, 16, 17])
-def test_rnn_tensor_leaf_norm_preserving_bias_bound(lib, B):
+def test_rnn_tensor_leaf_norm_preserving_bias_bound(lib, B, impl):
     T = 2000
     f = W.norm_preserving_rnn(T, B, 64, seed=B)
     ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
-    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], leaf_impl="tensor")
+    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], leaf_impl=impl)
     gf, i_f = run_rnn(lib, f["h"], f["W_hh"], f["g"], leaf_impl="ffma")
     et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
     print(f"B={B}: tensor {et:.2e}  ffma {ef:.2e}")
