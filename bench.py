@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BPPSA backward ms vs sequential BP (1/2/4/8 GPU); % HBM/tensor roofline"
 C4 = dict(T=1 << 20, B=16, H=64, I=1)
-C4_BLOCK0, C4_BLOCK = 256, 32
+C4_BLOCK0, C4_BLOCK = 512, 32
 SMALL = {   # secondary configs (N = 1 sweep): (T, B, H, block0, block)
     "c1": dict(T=1000, B=16, H=20, block0=8, block=8),
     "c2": dict(T=30000, B=16, H=20, block0=16, block=16),

@@ -120,9 +120,8 @@ typedef struct bppsa_scan_opts {
   int leaf_impl; /* level-0 fold engine: 0 = auto (tensor cores where they apply:
                   * RNN with H = 64), 1 = FFMA (CUDA cores), 2 = tensor cores
                   * (up-sweep fold as 3xFP16 with per-chain power-of-two
-                  * scaling), 3 = tensor cores with the 3xTF32 up-sweep fold,
-                  * 4 = 3xFP16 fold with all warps on one tile at a time
-                  * (experimental).  2..4 fail with BPPSA_ERR_NOT_SUPPORTED outside the tanh
+                  * scaling), 3 = tensor cores with the 3xTF32 up-sweep fold.
+                  * 2 and 3 fail with BPPSA_ERR_NOT_SUPPORTED outside the tanh
                   * RNN with H = 64.                                          */
   /* Optional instrumentation (all may be NULL/0): if `events` is non-NULL the
    * library records events[2k] / events[2k+1] (cudaEvent_t, created by the

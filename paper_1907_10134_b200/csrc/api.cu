@@ -165,7 +165,7 @@ bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts
   const size_t HH = (size_t)j.H * j.H, B = (size_t)j.B;
   size_t off = 0;
   p->leaf_impl = opts ? opts->leaf_impl : 0;
-  if (p->leaf_impl < 0 || p->leaf_impl > 4) return fail(BPPSA_ERR_INVALID_ARGUMENT, "leaf_impl must be in [0, 4]");
+  if (p->leaf_impl < 0 || p->leaf_impl > 3) return fail(BPPSA_ERR_INVALID_ARGUMENT, "leaf_impl must be 0, 1, 2 or 3");
   if (p->leaf_impl >= 2 && !(j.kind == BPPSA_JAC_RNN_TANH && j.H == 64))
     return fail(BPPSA_ERR_NOT_SUPPORTED, "tensor-core leaf fold is built for the tanh RNN with H = 64");
   p->has_dense = (j.kind == BPPSA_JAC_DENSE) && mode != BPPSA_SCAN_ALG1;
@@ -267,10 +267,17 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
       const LeafArgs la = leaf_args(j, head, seed);
       if (use_tensor_leaf(j, p.leaf_impl)) {
-        // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
-        e = head ? launch_leaf_up(la, p.C[0], dst, p.n[1], 0, 1, st) : cudaSuccess;
-        if (e == cudaSuccess) e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], head, num_sms(), st,
-                                                     p.leaf_impl == 3 ? 1 : (p.leaf_impl == 4 ? 2 : 0));
+        const int prec = p.leaf_impl == 3 ? 1 : 0;
+        if (prec == 0) {
+          // 3xFP16 fold: the head block is folded as the matrix of its leaves
+          // with all other blocks, then applied to the seed
+          e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], 0, num_sms(), st, prec);
+          if (e == cudaSuccess && head) e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, st);
+        } else {
+          // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
+          e = head ? launch_leaf_up(la, p.C[0], dst, p.n[1], 0, 1, st) : cudaSuccess;
+          if (e == cudaSuccess) e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], head, num_sms(), st, prec);
+        }
       } else {
         e = launch_leaf_up(la, p.C[0], dst, p.n[1], 0, p.n[1], st);
       }

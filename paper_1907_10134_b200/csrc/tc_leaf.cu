@@ -754,7 +754,9 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
     const int b = bp * 2 + (row >> 6);
     const int j = row & 63;
     const bool ok = b < B;
-    const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+    // the head block (slot 0 = the seed vector) is folded as the matrix of its
+    // leaves, slots 1..C-1; head_apply_kernel then applies it to the seed
+    const long long s0 = (a.seg.head && q == 0) ? 1 : q * C, s1 = min(q * C + (long long)C, S);
     float2 c2[8];                                  // c' = c 2^E (pairs of columns)
     int E = 0;
     float bound = 1.f / G;                         // G * bound = |c'_0|_inf bound (one-hot start)
@@ -821,11 +823,7 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
           STEP_TRACE(4);
           float t1[16], t2[16];
           tmem_ld16(t_d1, t1);
-#ifndef EXP_NO_D2
           tmem_ld16(t_d2, t2);
-#else
-          for (int i = 0; i < 16; ++i) t2[i] = 0.f;
-#endif
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
           STEP_TRACE(5);
 #pragma unroll
@@ -850,9 +848,7 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
         const uint32_t redp = red0 + par * (TM * 16);
         asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
         tmem_st8(t_a1, p1);
-#ifndef EXP_NO_A2
         tmem_st8(t_a2, p2);
-#endif
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         STEP_TRACE(1);
         tc_fence_before();
@@ -875,7 +871,8 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
 #endif
       }
     }
-    // D of the tile's last step
+    // D of the tile's last step (none for an empty head block: the identity)
+    if (!first) {
     if (issuer) {
       if (lane == 0) mbar_wait(&d_full[g], ph);
       __syncwarp();
@@ -883,7 +880,6 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
     named_bar(5 + g, EPI16_THREADS);
     ph ^= 1;
     tc_fence_after();
-    {
       float t1[16], t2[16];
       tmem_ld16(t_d1, t1);
       tmem_ld16(t_d2, t2);
@@ -908,302 +904,32 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Same fold, all 32 warps on ONE tile at a time: two tiles (slots X, Y) of a
-// pair advance in lockstep and their epilogues alternate, so MMA X runs while
-// every warp works on epilogue Y and vice versa (thread = chain row x 8
-// columns).  Per tile-step: bar BD (D ready; the issuer warp polls the
-// commit barrier, then joins) -> LDTM -> 3xFP16 split -> STTM -> bar.arrive
-// BA (A ready; only the issuer warp waits, then issues).  The row maximum of
-// a tile's scaled operand (8 partials per row) is read after the next BD of
-// the other tile, which orders it; the scale of the next step is computed
-// while that tile's MMA still runs.
-// ---------------------------------------------------------------------------
-constexpr int P_THREADS = 1024;
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
-               "r"(r[2]), "r"(r[3])
-               : "memory");
-}
 
-struct PTile {              // per-thread state of one tile of the pair
-  float2 c[4];              // c' = c 2^E, this thread's 8 columns
-  float bound;              // M_{s-1} (row max of the previous scaled operand), or 1/G at the start
-  int E;
-  int len;                  // steps of this tile (0: no tile)
-};
-
-// scale of step st from the bound, folded into d: ds = d 2^s (E += s + sw)
-__device__ __forceinline__ void p_scale(PTile& T, uint32_t dp, uint32_t dmp, float G, int sw, float2 (&ds)[4]) {
-  float dms;
-  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(dms) : "r"(dmp));
-  const int s = min(127, 141 - (int)(__float_as_uint(G * T.bound * dms) >> 23));
-  const float sc = __int_as_float((s + 127) << 23);
-  T.E += s + sw;
-  const float4 d0 = lds128(dp), d1 = lds128(dp + 16u);
-  ds[0] = __fmul2_rn(make_float2(d0.x, d0.y), make_float2(sc, sc));
-  ds[1] = __fmul2_rn(make_float2(d0.z, d0.w), make_float2(sc, sc));
-  ds[2] = __fmul2_rn(make_float2(d1.x, d1.y), make_float2(sc, sc));
-  ds[3] = __fmul2_rn(make_float2(d1.z, d1.w), make_float2(sc, sc));
-}
-
-// c' <- D1 + D2 (the tile's accumulator halves)
-__device__ __forceinline__ void p_load_d(PTile& T, uint32_t t_d) {
-  float t1[8], t2[8];
-  tmem_ld8(t_d, t1);
-  tmem_ld8(t_d + 64, t2);
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    T.c[i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
-}
-
-// x^ = c' o ds split into fp16 pairs -> A1 / A2 in TMEM; partial row max -> red
-__device__ __forceinline__ void p_split_store(const PTile& T, const float2 (&ds)[4], uint32_t t_a, uint32_t red_w) {
-  float pm = 0.f;
-  uint32_t p1[4], p2[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 x = __fmul2_rn(T.c[i], ds[i]);
-    pm = fmaxf(pm, fmaxf(fabsf(x.x), fabsf(x.y)));
-    const __half2 h1 = __floats2half2_rn(x.x, x.y);
-    const float2 f1 = __half22float2(h1);
-    const float2 r = __fadd2_rn(x, make_float2(-f1.x, -f1.y));
-    p1[i] = h2_bits(h1);
-    p2[i] = h2_bits(__floats2half2_rn(r.x, r.y));
-  }
-  asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(red_w), "r"(__float_as_uint(pm)) : "memory");
-  tmem_st4(t_a, p1);
-  tmem_st4(t_a + 32, p2);
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-}
-
-__device__ __forceinline__ float p_row_max(uint32_t red_row) {
-  uint32_t m[8];
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(m[0]), "=r"(m[1]), "=r"(m[2]), "=r"(m[3]) : "r"(red_row) : "memory");
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(m[4]), "=r"(m[5]), "=r"(m[6]), "=r"(m[7]) : "r"(red_row + 16u) : "memory");
-  return __uint_as_float(max(max(max(m[0], m[1]), max(m[2], m[3])), max(max(m[4], m[5]), max(m[6], m[7]))));
-}
-
-__global__ void __launch_bounds__(P_THREADS, 1) tc_leaf_up_f16p_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
-                                                                       long long n_out, long long q0) {
-  extern __shared__ uint8_t smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + F_OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
-  uint32_t* wred = tmem_slot + 2;
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int B = a.seg.B;
-  const long long S = a.seg.S();
-  const long long nq = n_out - q0;
-  const int nbp = (B + 1) / 2;
-  const long long ntiles = (long long)nbp * nq;
-
-  if (threadIdx.x < 2) wred[threadIdx.x] = 0;
+// Head block of level 1: slot 0 holds the column-major aggregate M of the
+// head block's leaves (written by the fold above); replace it in place by the
+// vector M . seed (the head aggregate of the scan: a[C-1]...a[1] a[0]
+// with a[0] = the seed).  One CTA per sample; the matrix is read before the
+// vector overwrites its first column.
+__global__ void __launch_bounds__(TH) head_apply_kernel(float* __restrict__ lvl, long long bstride,
+                                                        const float* __restrict__ seed) {
+  __shared__ float sd[TH];
+  const int b = blockIdx.x, i = threadIdx.x;
+  float* M = lvl + (long long)b * bstride;
+  sd[i] = seed[(long long)b * TH + i];
   __syncthreads();
-  int sw;
-  float G;
-  w_scale(a.W, wred, &sw, &G);
-  {
-    const float wsc = __int_as_float((sw + 127) << 23);
-    for (int e = threadIdx.x; e < TH * TH; e += P_THREADS) {
-      const int n = e / TH, k = e % TH;             // B[n][k] = W[k][n] 2^sw: rows 0..63 W1, 64..127 W2
-      const float w = __ldg(a.W + (long long)k * TH + n) * wsc;
-      const __half w1 = __float2half_rn(w);
-      *reinterpret_cast<__half*>(smem + sw16_off(n, k)) = w1;
-      *reinterpret_cast<__half*>(smem + sw16_off(TH + n, k)) = __float2half_rn(w - __half2float(w1));
-    }
-  }
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int s = 0; s < NSLOT; ++s) mbar_init(&d_full[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
-  }
-  fence_async_smem();
-  tc_fence_before();
+  float v = 0.f;
+#pragma unroll 8
+  for (int j = 0; j < TH; ++j) v = fmaf(M[(long long)j * TH + i], sd[j], v);
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-
-  const int row = (warp & 3) * 32 + lane;                 // TMEM lane / chain row of both tiles
-  const int cg = warp >> 2;                               // 8-column group
-  const bool issuer = warp == 0;
-  const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  const uint32_t t_d[2] = {lane_base + 8 * cg, lane_base + 256 + 8 * cg};
-  const uint32_t t_a[2] = {lane_base + 128 + 4 * cg, lane_base + 256 + 128 + 4 * cg};
-  const uint32_t hs_s = su32(smem + F_OFF_H);                       // [slot][2 samples][HCH][64] d
-  const uint32_t dmx_s = su32(smem + F_OFF_DMX);                    // [slot][2 samples][HCH] dmax
-  const uint32_t red_s = su32(smem + F_OFF_RED);                    // [slot][128 rows][8] u32
-  const uint32_t red_row[2] = {red_s + (uint32_t)row * 32u, red_s + (uint32_t)(TM + row) * 32u};
-  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
-  uint64_t bdesc[4];
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
-  const uint32_t dbar[2] = {su32(&d_full[0]), su32(&d_full[1])};
-  uint32_t ph[2] = {0, 0};
-  const long long rowB = (long long)B * TH;
-  const int j = row & 63, half = row >> 6;
-#ifdef BPPSA_STEP_TRACE
-  int tstep = -1;
-#define PTRACE(ph)                                                                                 \
-  if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 13) && tstep < 4096)                 \
-    g_step_trace[g][warp == 13][ph][tstep] = clock64();
-#else
-#define PTRACE(ph)
-#endif
-
-  for (long long tau = 2 * (long long)blockIdx.x; tau < ntiles; tau += 2 * (long long)gridDim.x) {
-    PTile T[2];
-    long long qq[2], s0[2];
-    int bpp[2];
-    int nmax = 0;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const long long tt = tau + g;
-      const bool have = tt < ntiles;
-      qq[g] = q0 + (have ? tt / nbp : 0);
-      bpp[g] = have ? (int)(tt % nbp) : 0;
-      s0[g] = qq[g] * C;
-      T[g].len = have ? (int)(min(s0[g] + (long long)C, S) - s0[g]) : 0;
-      T[g].E = 0;
-      T[g].bound = 1.f / G;
-      const bool ok = have && bpp[g] * 2 + half < B;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        T[g].c[i] = make_float2((8 * cg + 2 * i == j && ok) ? 1.f : 0.f, (8 * cg + 2 * i + 1 == j && ok) ? 1.f : 0.f);
-      nmax = max(nmax, T[g].len);
-    }
-    for (int st = 0; st < nmax; ++st) {
-#ifdef BPPSA_STEP_TRACE
-      ++tstep;
-#endif
-      const int ch = st % HCH;
-      if (ch == 0) {                               // stage h -> d (and dmax) of both tiles for HCH steps
-        __syncthreads();                           // every thread's d of the previous chunk is in registers
-        const int n = min(HCH, nmax - st);
-        for (int e = threadIdx.x; e < 2 * 2 * n * 16; e += P_THREADS) {
-          const int g = e / (2 * n * 16), r0 = e % (2 * n * 16);
-          const int bb2 = r0 / (n * 16), rem = r0 % (n * 16), sst = rem / 16, c4 = rem % 16;
-          const uint32_t dst = hs_s + 4u * ((((g * 2) + bb2) * HCH + sst) * TH + c4 * 4);
-          const int bs = (g ? bpp[1] : bpp[0]) * 2 + bb2;
-          if (bs < B && st + sst < (g ? T[1].len : T[0].len))
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
-                         "l"(a.h + (long long)a.seg.time_of((g ? s0[1] : s0[0]) + st + sst) * rowB +
-                             (long long)bs * TH + c4 * 4)
-                         : "memory");
-          else
-            sts128(dst, 1.f, 1.f, 1.f, 1.f);       // h = 1: d = 0
-        }
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncthreads();
-        for (int e = threadIdx.x; e < 2 * 2 * n * 16; e += P_THREADS) {   // whole warps: 16 lanes per row
-          const int g = e / (2 * n * 16), r0 = e % (2 * n * 16);
-          const int bb2 = r0 / (n * 16), rem = r0 % (n * 16), sst = rem / 16, c4 = rem % 16;
-          const uint32_t p = hs_s + 4u * ((((g * 2) + bb2) * HCH + sst) * TH + c4 * 4);
-          const float4 h4 = lds128(p);
-          const float4 d4 = make_float4(1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
-          sts128(p, d4.x, d4.y, d4.z, d4.w);
-          float m = fmaxf(fmaxf(d4.x, d4.y), fmaxf(d4.z, d4.w));
-#pragma unroll
-          for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-          if (c4 == 0)
-            asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(dmx_s + 4u * (((g * 2) + bb2) * HCH + sst)), "f"(m) : "memory");
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        PTile& Tg = T[g];
-        const bool act = st < Tg.len;
-        PTRACE(0);
-        float2 ds[4];
-        if (act)
-          p_scale(Tg, hs_s + 4u * ((((g * 2) + half) * HCH + ch) * TH + 8 * cg),
-                  dmx_s + 4u * (((g * 2) + half) * HCH + ch), G, sw, ds);
-        const bool had = st > 0 && st - 1 < Tg.len;  // D of this tile's previous step to consume
-        if (issuer && had) {
-          if (lane == 0) mbar_wait_s(dbar[g], ph[g]);
-          __syncwarp();
-        }
-        named_bar(3 + g, P_THREADS);               // BD: D ready; orders the other tile's row maxima
-        PTRACE(1);
-        if (had) {
-          ph[g] ^= 1;
-          tc_fence_after();
-          p_load_d(Tg, t_d[g]);
-        }
-        PTRACE(2);
-        if (g == 1) {
-          if (st < T[0].len) T[0].bound = p_row_max(red_row[0]);              // tile 0, step st
-        } else if (st > 0 && st - 1 < T[1].len) {
-          T[1].bound = p_row_max(red_row[1]);                                 // tile 1, step st-1
-        }
-        if (act) {
-          p_split_store(Tg, ds, t_a[g], red_row[g] + 4u * cg);
-          tc_fence_before();
-        }
-        PTRACE(3);
-        if (issuer) {
-          named_bar(1 + g, P_THREADS);             // every warp's A of this tile is stored
-          if (act) {
-            tc_fence_after();
-            mma8_f16_commit(tmem + 256 * g, bdesc, dbar[g]);
-          }
-        } else {
-          bar_arrive(1 + g, P_THREADS);
-        }
-        PTRACE(4);
-      }
-    }
-    // D of each tile's last step, then the aggregates
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      PTile& Tg = T[g];
-      if (Tg.len > 0) {
-        if (issuer) {
-          if (lane == 0) mbar_wait_s(dbar[g], ph[g]);
-          __syncwarp();
-        }
-        named_bar(3 + g, P_THREADS);
-        ph[g] ^= 1;
-        tc_fence_after();
-        p_load_d(Tg, t_d[g]);
-        const int b = bpp[g] * 2 + half;
-        if (b < B) {
-          float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + qq[g]) * TH + j) * TH + 8 * cg);
-          dst[0] = make_float4(ldexpf(Tg.c[0].x, -Tg.E), ldexpf(Tg.c[0].y, -Tg.E), ldexpf(Tg.c[1].x, -Tg.E),
-                               ldexpf(Tg.c[1].y, -Tg.E));
-          dst[1] = make_float4(ldexpf(Tg.c[2].x, -Tg.E), ldexpf(Tg.c[2].y, -Tg.E), ldexpf(Tg.c[3].x, -Tg.E),
-                               ldexpf(Tg.c[3].y, -Tg.E));
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
-  }
+  M[i] = v;
 }
 
 }  // namespace
+
+cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, cudaStream_t st) {
+  head_apply_kernel<<<B, TH, 0, st>>>(lvl, bstride, seed);
+  return cudaGetLastError();
+}
 
 // Matrix blocks q in [q0, n_out) of an RNN H = 64 segment.  prec 0: 3xFP16
 // row-scaled (tc_leaf_up_f16_kernel), 1: 3xTF32 (tc_leaf_up16_kernel).
@@ -1213,18 +939,6 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
   const long long pairs = (ntiles + 1) / 2;
   const int grid = (int)std::min<long long>(pairs, num_sms);
   if (grid <= 0) return cudaSuccess;
-  if (prec == 2) {
-    const int gridp = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
-    static bool attrp = false;
-    if (!attrp) {
-      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           F_SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-      attrp = true;
-    }
-    tc_leaf_up_f16p_kernel<<<gridp, P_THREADS, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
-    return cudaGetLastError();
-  }
   if (prec == 0) {
     static bool attrf = false;
     if (!attrf) {

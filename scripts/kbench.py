@@ -14,7 +14,8 @@ IMPL = os.environ.get("BPPSA_LEAF_IMPL", "auto")
 CFG = {"c4": (1 << 20, 16, 64, 128, 32), "c1": (1000, 16, 20, 8, 8), "c2": (30000, 16, 20, 16, 16),
        "c4s": (1 << 18, 16, 64, 128, 32), "c4b128": (1 << 20, 16, 64, 128, 32), "c4b128c64": (1 << 20, 16, 64, 128, 64),
        "c4c64": (1 << 20, 16, 64, 64, 64), "c4b256": (1 << 20, 16, 64, 256, 32), "c4b512": (1 << 20, 16, 64, 512, 32),
-       "c4b256c64": (1 << 20, 16, 64, 256, 64)}
+       "c4b256c64": (1 << 20, 16, 64, 256, 64), "c4b512c16": (1 << 20, 16, 64, 512, 16),
+       "c4b512c64": (1 << 20, 16, 64, 512, 64), "c4b384": (1 << 20, 16, 64, 384, 32)}
 
 
 def run(name, reps=5):
