@@ -268,7 +268,7 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
       const LeafArgs la = leaf_args(j, head, seed);
       if (use_tensor_leaf(j, p.leaf_impl)) {
         const int prec = p.leaf_impl == 3 ? 1 : 0;
-        if (prec == 0) {
+        if (prec != 1) {
           // 3xFP16 fold: the head block is folded as the matrix of its leaves
           // with all other blocks, then applied to the seed
           e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], 0, num_sms(), st, prec);

@@ -133,8 +133,8 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 #ifdef BPPSA_STEP_TRACE
 __device__ long long g_step_trace[2][2][8][4096];   // [slot][warp 0 / warp 13][phase][step]
 #define STEP_TRACE(ph)                                                                            \
-  if (blockIdx.x == 0 && lane == 0 && (wl == 0 || wl == 13) && tstep < 4096)                      \
-    g_step_trace[g][wl == 13][ph][tstep] = clock64();
+  if (blockIdx.x == 0 && lane == 0 && (wl == 0 || wl == 5) && tstep < 4096)                      \
+    g_step_trace[g][wl == 5][ph][tstep] = clock64();
 #else
 #define STEP_TRACE(ph)
 #endif
@@ -678,8 +678,31 @@ __device__ __forceinline__ void w_scale(const float* W, uint32_t* red, int* sw_o
   *G_out = __uint_as_float(red[1]);
 }
 
-__global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
-                                                                       long long n_out, long long q0) {
+// c' <- D1 + D2 for this thread's CPT columns (the accumulator halves), RN
+template <int CPT, int NP>
+__device__ __forceinline__ void load_d_sum(uint32_t t_d1, uint32_t t_d2, float2 (&c2)[NP]) {
+#pragma unroll
+  for (int h = 0; h < CPT / 16; ++h) {
+    float t1[16], t2[16];
+    tmem_ld16(t_d1 + 16 * h, t1);
+    tmem_ld16(t_d2 + 16 * h, t2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      c2[8 * h + i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
+  }
+}
+
+// WPS = epilogue warps per slot.  8 (thread = chain row x 32 columns, 512
+// threads, up to 128 registers) measured best at C4: 29.8 ms against 34.8
+// with 16 (row x 16 columns: 64 registers force address rematerialisation and
+// the per-thread overhead is amortised over half the elements) and 31.7 with
+// 4 (one thread per row, no max exchange, but one warp per SMSP per slot).
+template <int WPS>
+__global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                   long long n_out, long long q0) {
+  constexpr int EPI = 32 * WPS, NT = 2 * EPI;     // threads per slot / per CTA
+  constexpr int NCG = WPS / 4, CPT = TH / NCG, NP = CPT / 2;   // column groups; columns / pairs per thread
   extern __shared__ uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + F_OFF_BAR);
@@ -700,7 +723,7 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
   w_scale(a.W, wred, &sw, &G);
   {
     const float wsc = __int_as_float((sw + 127) << 23);
-    for (int e = threadIdx.x; e < TH * TH; e += NTHREADS16) {
+    for (int e = threadIdx.x; e < TH * TH; e += NT) {
       const int n = e / TH, k = e % TH;             // B[n][k] = W[k][n] 2^sw: rows 0..63 W1, 64..127 W2
       const float w = __ldg(a.W + (long long)k * TH + n) * wsc;
       const __half w1 = __float2half_rn(w);
@@ -725,15 +748,15 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
-  const int g = warp / EPI16_WARPS, wl = warp % EPI16_WARPS;
+  const int g = warp / WPS, wl = warp % WPS;
   const int row = (wl & 3) * 32 + lane;
   const int cgp = wl >> 2;
   const int et = wl * 32 + lane;
   const bool issuer = wl == 0;
   const uint32_t slot_base = tmem + 256 * g;
   const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
-  const uint32_t t_d1 = lane_base + 16 * cgp, t_d2 = t_d1 + 64;
-  const uint32_t t_a1 = lane_base + 128 + 8 * cgp, t_a2 = lane_base + 160 + 8 * cgp;
+  const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_a1 = lane_base + 128 + NP * cgp, t_a2 = lane_base + 160 + NP * cgp;
   float* hs = reinterpret_cast<float*>(smem + F_OFF_H + g * H_BYTES);
   const uint32_t hs_s = su32(hs);
   float* dmx = reinterpret_cast<float*>(smem + F_OFF_DMX) + g * 2 * HCH;       // [2 samples][HCH]
@@ -757,17 +780,17 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
     // the head block (slot 0 = the seed vector) is folded as the matrix of its
     // leaves, slots 1..C-1; head_apply_kernel then applies it to the seed
     const long long s0 = (a.seg.head && q == 0) ? 1 : q * C, s1 = min(q * C + (long long)C, S);
-    float2 c2[8];                                  // c' = c 2^E (pairs of columns)
+    float2 c2[NP];                                 // c' = c 2^E (pairs of columns)
     int E = 0;
     float bound = 1.f / G;                         // G * bound = |c'_0|_inf bound (one-hot start)
     bool first = true;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      c2[i] = make_float2((16 * cgp + 2 * i == j && ok) ? 1.f : 0.f, (16 * cgp + 2 * i + 1 == j && ok) ? 1.f : 0.f);
+    for (int i = 0; i < NP; ++i)
+      c2[i] = make_float2((CPT * cgp + 2 * i == j && ok) ? 1.f : 0.f, (CPT * cgp + 2 * i + 1 == j && ok) ? 1.f : 0.f);
     for (long long sc = s0; sc < s1; sc += HCH) {
       const int n = (int)min((long long)HCH, s1 - sc);
-      named_bar(1 + g, EPI16_THREADS);             // previous chunk fully consumed (d is read into registers)
-      for (int e = et; e < 2 * n * 16; e += EPI16_THREADS) {
+      named_bar(1 + g, EPI);             // previous chunk fully consumed (d is read into registers)
+      for (int e = et; e < 2 * n * 16; e += EPI) {
         const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
         float* dst = hs + (bb2 * HCH + st) * TH + ch * 4;
         const int bs = bp * 2 + bb2;
@@ -779,7 +802,7 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       // d = 1 - h^2 in place and dmax per (sample, step): 16 consecutive lanes
       // hold one 64-wide row (2n*16 is a multiple of 32: whole warps iterate)
-      for (int e = et; e < 2 * n * 16; e += EPI16_THREADS) {
+      for (int e = et; e < 2 * n * 16; e += EPI) {
         const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
         const uint32_t p = hs_s + 4u * ((bb2 * HCH + st) * TH + ch * 4);
         const float4 h4 = lds128(p);
@@ -790,8 +813,8 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
         for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (ch == 0) dmx[bb2 * HCH + st] = m;
       }
-      named_bar(1 + g, EPI16_THREADS);
-      uint32_t dp = hs_s + 4u * ((row >> 6) * HCH * TH + 16 * cgp);   // this thread's d slice of step st
+      named_bar(1 + g, EPI);
+      uint32_t dp = hs_s + 4u * ((row >> 6) * HCH * TH + CPT * cgp);  // this thread's d slice of step st
       uint32_t dmp = su32(dmx + (row >> 6) * HCH);                      // dmax of step st
       for (int st = 0; st < n; ++st, dp += 4u * TH, dmp += 4u) {
         STEP_TRACE(0);
@@ -803,9 +826,9 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
         const int s = min(127, 141 - (int)(__float_as_uint(f) >> 23));
         const float2 scl = make_float2(__int_as_float((s + 127) << 23), __int_as_float((s + 127) << 23));
         E += s + sw;
-        float2 ds[8];
+        float2 ds[NP];
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
+        for (int q4 = 0; q4 < CPT / 4; ++q4) {
           const float4 d4 = lds128(dp + 16u * q4);
           ds[2 * q4] = __fmul2_rn(make_float2(d4.x, d4.y), scl);
           ds[2 * q4 + 1] = __fmul2_rn(make_float2(d4.z, d4.w), scl);
@@ -817,24 +840,18 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
             STEP_TRACE(7);
             __syncwarp();
           }
-          named_bar(5 + g, EPI16_THREADS);
+          named_bar(5 + g, EPI);
           ph ^= 1;
           tc_fence_after();
           STEP_TRACE(4);
-          float t1[16], t2[16];
-          tmem_ld16(t_d1, t1);
-          tmem_ld16(t_d2, t2);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          load_d_sum<CPT>(t_d1, t_d2, c2);
           STEP_TRACE(5);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            c2[i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
         }
         first = false;
         float pm = 0.f;
-        uint32_t p1[8], p2[8];
+        uint32_t p1[NP], p2[NP];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < NP; ++i) {
           const float2 x = __fmul2_rn(c2[i], ds[i]);
           pm = fmaxf(pm, fmaxf(fabsf(x.x), fabsf(x.y)));
           // x1 = x truncated to 11 significant bits (exact in fp16 for |x| >= 2^-14;
@@ -846,25 +863,37 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
           p2[i] = h2_bits(__floats2half2_rn(r.x, r.y));
         }
         const uint32_t redp = red0 + par * (TM * 16);
-        asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
-        tmem_st8(t_a1, p1);
-        tmem_st8(t_a2, p2);
+        if constexpr (NCG > 1)
+          asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+#pragma unroll
+        for (int h8 = 0; h8 < NP / 8; ++h8) {
+          tmem_st8(t_a1 + 8 * h8, *reinterpret_cast<const uint32_t(*)[8]>(p1 + 8 * h8));
+          tmem_st8(t_a2 + 8 * h8, *reinterpret_cast<const uint32_t(*)[8]>(p2 + 8 * h8));
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         STEP_TRACE(1);
         tc_fence_before();
-        named_bar(3 + g, EPI16_THREADS);           // the slot's A and the row maxima are complete
+        named_bar(3 + g, EPI);           // the slot's A and the row maxima are complete
         STEP_TRACE(2);
         if (issuer) {
           tc_fence_after();
           mma8_f16_commit(slot_base, bdesc, su32(&d_full[g]));
           STEP_TRACE(3);
         }
-        uint32_t m4[4];
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
-                     : "=r"(m4[0]), "=r"(m4[1]), "=r"(m4[2]), "=r"(m4[3])
-                     : "r"(redp)
-                     : "memory");
-        bound = __uint_as_float(max(max(m4[0], m4[1]), max(m4[2], m4[3])));
+        if constexpr (NCG == 4) {
+          uint32_t m4[4];
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                       : "=r"(m4[0]), "=r"(m4[1]), "=r"(m4[2]), "=r"(m4[3])
+                       : "r"(redp)
+                       : "memory");
+          bound = __uint_as_float(max(max(m4[0], m4[1]), max(m4[2], m4[3])));
+        } else if constexpr (NCG == 1) {
+          bound = pm;                              // the whole row is this thread's
+        } else {
+          uint32_t m2[2];
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
+          bound = __uint_as_float(max(m2[0], m2[1]));
+        }
         par ^= 1;
 #ifdef BPPSA_STEP_TRACE
         ++tstep;
@@ -877,21 +906,15 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_up_f16_kernel(LeafArgs 
       if (lane == 0) mbar_wait(&d_full[g], ph);
       __syncwarp();
     }
-    named_bar(5 + g, EPI16_THREADS);
+    named_bar(5 + g, EPI);
     ph ^= 1;
     tc_fence_after();
-      float t1[16], t2[16];
-      tmem_ld16(t_d1, t1);
-      tmem_ld16(t_d2, t2);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        c2[i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]), make_float2(t2[2 * i], t2[2 * i + 1]));
+      load_d_sum<CPT>(t_d1, t_d2, c2);
     }
     if (ok) {
-      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 16 * cgp);
+      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + CPT * cgp);
 #pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4)
+      for (int k4 = 0; k4 < CPT / 4; ++k4)
         dst[k4] = make_float4(ldexpf(c2[2 * k4].x, -E), ldexpf(c2[2 * k4].y, -E), ldexpf(c2[2 * k4 + 1].x, -E),
                               ldexpf(c2[2 * k4 + 1].y, -E));
     }
@@ -939,15 +962,15 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
   const long long pairs = (ntiles + 1) / 2;
   const int grid = (int)std::min<long long>(pairs, num_sms);
   if (grid <= 0) return cudaSuccess;
-  if (prec == 0) {
+  if (prec == 0) {                                 // 3xFP16, 8 epilogue warps per slot
     static bool attrf = false;
     if (!attrf) {
-      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            F_SMEM_BYTES);
       if (e != cudaSuccess) return e;
       attrf = true;
     }
-    tc_leaf_up_f16_kernel<<<grid, NTHREADS16, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+    tc_leaf_up_f16_kernel<8><<<grid, 64 * 8, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
     return cudaGetLastError();
   }
   static bool attr16 = false;

@@ -139,12 +139,19 @@ __global__ void probe(const float* X, const float* W, float* D, int variant) {
 }
 
 template <int N>
-__global__ void rate(int nbatch, int wait_each, long long* cycles) {
+__global__ void rate(int nbatch, int wait_each, long long* cycles, int pattern = 0) {
   extern __shared__ uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
-  for (int i = threadIdx.x; i < N * 32; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x1c001c00u;
+  // operand patterns: 0 = constants, 1 = A random normal halves, 2 = A random incl. subnormal halves,
+  // 3 = A and B random normal, 4 = A and B incl. subnormals
+  for (int i = threadIdx.x; i < N * 32; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    uint32_t bn = ((h >> 3) & 0x03FF03FFu) | 0x3C003C00u;          // normal halves in [1, 2)
+    uint32_t bs = (h & 0x83FF83FFu);                                // subnormal halves
+    reinterpret_cast<uint32_t*>(smem)[i] = pattern == 3 ? bn : (pattern == 4 ? ((i & 1) ? bs : bn) : 0x1c001c00u);
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -158,15 +165,31 @@ __global__ void rate(int nbatch, int wait_each, long long* cycles) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tslot;
+  if (pattern != 0) {
+    const uint32_t lb = tmem + ((uint32_t)((threadIdx.x >> 5) * 32) << 16);
+    for (int c = 0; c < 64; ++c) {
+      uint32_t h = (uint32_t)(threadIdx.x * 64 + c) * 2246822519u;
+      uint32_t v = ((h >> 3) & 0x03FF03FFu) | 0x3C003C00u;
+      if (pattern == 2 || pattern == 4) v = (c & 1) ? (h & 0x83FF83FFu) : v;
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(lb + 256 + c), "r"(v) : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  }
   long long t0 = clock64();
   if (threadIdx.x < 32) {
     uint32_t ph = 0;
     for (int b = 0; b < nbatch; ++b) {
       if (threadIdx.x == 0) {
+        // pattern 20: alternate two slots (D at 0 / 256, A at 128 / 384) like the fold kernel
+        const uint32_t dbase = (pattern == 20 && (b & 1)) ? 256u : 0u;
+        const uint32_t abase = pattern == 20 ? dbase + 128u : (pattern >= 10 ? 128u : 256u);
         for (int i = 0; i < 8; ++i) {
           asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                       " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
-                       "r"(tmem + 256 + 8 * (i & 7)), "l"(sdesc(su32(smem) + 32 * (i & 3))), "r"(idesc_f16(N)),
+                       " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + dbase),
+                       "r"(tmem + abase + 8 * (i & 3) + 32 * (i >> 2)), "l"(sdesc(su32(smem) + 32 * (i & 3))), "r"(idesc_f16(N)),
                        "r"(i));
         }
         if (wait_each || b == nbatch - 1)
@@ -189,12 +212,13 @@ __global__ void rate(int nbatch, int wait_each, long long* cycles) {
 }
 
 template <int N>
-void run_rate(long long* d) {
+void run_rate(long long* d, int pattern = 0) {
   const int smem = 256 * 128 + 2048;
   cudaFuncSetAttribute(rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  printf("pattern %d: ", pattern);
   for (int we = 0; we < 2; ++we) {
     const int nb = 4000;
-    rate<N><<<148, 128, smem>>>(nb, we, d);
+    rate<N><<<148, 128, smem>>>(nb, we, d, pattern);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
     long long h[148];
@@ -216,7 +240,7 @@ int main() {
   cudaMalloc(&dW, W.size() * 4);
   cudaMalloc(&dD, D.size() * 4);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 40 * 1024);
-  for (int data = 0; data < 3; ++data) {
+  for (int data = 0; data < 0; ++data) {
     for (int m = 0; m < 128; ++m) {
       // rows of wildly different magnitudes: per-row scaling must absorb them
       const float rs = data == 0 ? 1.f : (data == 1 ? ldexpf(1.f, (m % 41) * 7 - 140) : 1e-3f);
@@ -253,8 +277,6 @@ int main() {
   }
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
-  run_rate<64>(d);
-  run_rate<128>(d);
-  run_rate<256>(d);
+  for (int pat : {0, 10, 20}) run_rate<128>(d, pat);
   return 0;
 }
