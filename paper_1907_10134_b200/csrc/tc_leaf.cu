@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda.h>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -947,6 +948,358 @@ __global__ void __launch_bounds__(TH) head_apply_kernel(float* __restrict__ lvl,
   M[i] = v;
 }
 
+// ---------------------------------------------------------------------------
+// Level-0 DOWN-walk on kind::f16 (3xFP16, true-scale chains).
+//
+// A tile = G = floor(128 / B8) whole groups of B chains (one level-0 block q,
+// all B samples; B8 = B rounded up to 8 rows), so the h rows a tile needs at
+// one step are G contiguous runs h[t(q, st)][0..B)[0..64) of the time-major
+// input: the elected issuer lane loads each run with TWO 2D TMA copies
+// (column halves, box 32 x B, SWIZZLE_128B) into a 3-stage ring — 2G copies
+// per step instead of one bulk copy per chain row, and the 128-byte swizzle
+// makes the threads' column-slice reads conflict-free.  Chains stay in true
+// fp32 scale (grad_h is written every step); only the MMA operand is scaled:
+// x^ = (d o v) 2^s, D = x^ [W1|W2] 2^sw, v <- (D1 + D2) 2^-(s + sw), with s
+// from the bound  max|x| <= max|v| <= G M 2^-(s_prev + sw)  (M = the exact row
+// maximum of the previous x^, exchanged through shared memory and ordered by
+// the step's A barrier), so x^ < 2^15.  8 epilogue warps per slot, thread =
+// chain row x 32 columns (one column half), two slots in flight.
+// ---------------------------------------------------------------------------
+constexpr int W_NST = 3;                                    // ring stages
+constexpr int W_STAGE = 2 * TM * 128;                       // [half][128 rows][128 B] = 32 KB
+constexpr int W_OFF_RING = F_B_BYTES;                       // [slot][stage]
+constexpr int W_OFF_RED = W_OFF_RING + NSLOT * W_NST * W_STAGE;   // [slot][parity][128 rows][2] u32
+constexpr int W_OFF_BAR = W_OFF_RED + NSLOT * 2 * TM * 8;
+constexpr int W_SMEM_BYTES = W_OFF_BAR + 128 + 1024;
+constexpr int W_WPS = 8, W_EPI = 32 * W_WPS, W_NT = 2 * W_EPI;
+
+
+__global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, const __grid_constant__ CUtensorMap h3,
+                                                                     const __grid_constant__ CUtensorMap h5,
+                                                                     const __grid_constant__ CUtensorMap g3,
+                                                                     const __grid_constant__ CUtensorMap g5,
+                                                                     int C, const float* __restrict__ carry,
+                                                                     long long nblk, float* __restrict__ grad_h,
+                                                                     float* __restrict__ grad_init, int G) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + W_OFF_BAR);
+  uint64_t* h_full = d_full + NSLOT;                                    // [slot][stage]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_full + NSLOT * W_NST);
+  uint32_t* wred = tmem_slot + 2;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+
+  if (threadIdx.x < 2) wred[threadIdx.x] = 0;
+  for (int e = threadIdx.x; e < NSLOT * W_NST * W_STAGE / 16; e += W_NT)
+    sts128(su32(smem + W_OFF_RING) + 16u * e, 0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  int sw;
+  float G_w;
+  w_scale(a.W, wred, &sw, &G_w);
+  const int eG = (int)(__float_as_uint(G_w) >> 23) - 126;          // G < 2^eG
+  {
+    const float wsc = __int_as_float((sw + 127) << 23);
+    for (int e = threadIdx.x; e < TH * TH; e += W_NT) {
+      const int n = e / TH, k = e % TH;             // B[n][k] = W[k][n] 2^sw: rows 0..63 W1, 64..127 W2
+      const float w = __ldg(a.W + (long long)k * TH + n) * wsc;
+      const __half w1 = __float2half_rn(w);
+      *reinterpret_cast<__half*>(smem + sw16_off(n, k)) = w1;
+      *reinterpret_cast<__half*>(smem + sw16_off(TH + n, k)) = __float2half_rn(w - __half2float(w1));
+    }
+  }
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) {
+        mbar_init(&d_full[s], 1);
+        for (int k = 0; k < W_NST; ++k) mbar_init(&h_full[s * W_NST + k], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&h3)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&h5)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&g3)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&g5)) : "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int g = warp / W_WPS, wl = warp % W_WPS;
+  const int row = (wl & 3) * 32 + lane;
+  const int cgp = wl >> 2;                                // column half
+  const bool issuer = wl == 0;
+  const uint32_t slot_base = tmem + 256 * g;
+  const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
+  const uint32_t t_d1 = lane_base + 32 * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_a1 = lane_base + 128 + 16 * cgp, t_a2 = lane_base + 160 + 16 * cgp;
+  const uint32_t ring = su32(smem + W_OFF_RING) + (uint32_t)(g * W_NST * W_STAGE);
+  const uint32_t hrow_off = (uint32_t)(row * 256 + cgp * 128);          // this thread's row half in a stage
+  const int swz = (2 * row + cgp) & 7;                                    // its 128-byte line's swizzle
+  const uint32_t red0 = su32(smem + W_OFF_RED) + (uint32_t)((g * 2 * TM + row) * 8);
+  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+  uint64_t bdesc[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  const uint32_t dbar = su32(&d_full[g]), hbar0 = su32(&h_full[g * W_NST]);
+  uint32_t dph = 0, par = 0, gs = 0;                       // D phase; exchange parity; slot step counter
+  // tile row = j B + b holds group r = G-1-j (block q = qb + r), sample b: the
+  // 5D TMA box delivers the groups of one step in decreasing q order
+  const int jrow = row / B, bsm = row % B, grp = G - 1 - jrow;
+  // view of the time axis as (block c4, step c3): t = c4 C + c3 = Tm - q C - st
+  const long long Tm = (long long)a.seg.T - 1 + a.seg.head;
+  const int A_blk = (int)(Tm / C), R_off = (int)(Tm % C);
+  // tiles: [0] = block 0 alone; [1 .. nfull] = G blocks each whose merged box
+  // stays inside the view at every step (blocks 1 .. A-1); then the remaining
+  // blocks two per tile (per-group copies: few TMA ops, so no slow tile)
+  const long long nfull = A_blk > 1 ? (A_blk - 1) / G : 0;
+  const long long rem0 = 1 + nfull * G;
+  const long long ntiles = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
+#ifdef BPPSA_STEP_TRACE
+  int tstep = 0;
+#define WTRACE(ph)                                                                                  \
+  if (blockIdx.x == 0 && lane == 0 && (wl == 0 || wl == 5) && tstep < 4096)                        \
+    g_step_trace[g][wl == 5][ph][tstep] = clock64();
+#else
+#define WTRACE(ph)
+#endif
+
+  for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+    const bool merged = tau >= 1 && tau <= nfull;
+    const long long qb = tau == 0 ? 0 : (merged ? 1 + (tau - 1) * G : rem0 + 2 * (tau - nfull - 1));
+    const int ng = tau == 0 ? 1 : (merged ? G : (int)min(2LL, nblk - qb));   // groups in this tile
+    const long long q = qb + grp;
+    const bool valid = jrow < G && grp < ng;
+    const bool head = a.seg.head && q == 0;
+    const long long s_start = head ? 1 : q * C, s1 = min(q * C + C, S);
+    const int len = valid ? (int)(s1 - s_start) : 0;
+    const bool total = valid && grad_init != nullptr && s1 == S;
+    float2 v[16];                                          // this thread's 32 columns of the chain (true scale)
+    {
+      const float* src = head ? a.seed + (long long)bsm * TH : carry + ((long long)bsm * nblk + q) * TH;
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const float4 f = valid ? __ldg(reinterpret_cast<const float4*>(src + 32 * cgp) + k4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[2 * k4] = make_float2(f.x, f.y);
+        v[2 * k4 + 1] = make_float2(f.z, f.w);
+      }
+    }
+    // TMA traffic of one step.  Tiles without block 0: ONE 5D box {32, 2, B, 1,
+    // G} for all groups (loads of h into the ring stage, stores of grad_h from
+    // it; coordinates below 0 are out of range: zero-filled / skipped).  The
+    // tile holding block 0 (its head slot shifts the time by one) issues one 3D
+    // box {32, 2, B} per group, one group per lane.  Each thread overwrites the
+    // h half-row it consumed with its v (the exclusive output).
+    // (negative box coordinates fault, so a step whose box would leave the
+    // view, and the tile holding block 0, go per group)
+    long long my_ss = 0, my_len = 0;
+    const bool my_on = lane < ng;
+    if (my_on) {
+      const long long qr = qb + lane;
+      my_ss = (a.seg.head && qr == 0) ? 1 : qr * C;
+      my_len = min(qr * C + C, S) - my_ss;
+    }
+    const uint32_t my_dst = (uint32_t)((G - 1 - lane) * B * 256);
+    auto c5 = [&](int st, int& c3, int& c4) {
+      c3 = R_off - st;
+      c4 = A_blk - (int)(qb + G - 1);
+      if (c3 < 0) { c3 += C; c4 -= 1; }
+      return merged;                                        // (then c4 >= 0 at every step)
+    };
+    auto issue_loads = [&](int st, uint32_t gstep) {       // all lanes of the issuer warp
+      const uint32_t stage = ring + (gstep % W_NST) * W_STAGE;
+      const uint32_t bar = hbar0 + 8u * (gstep % W_NST);
+      int c3, c4;
+      if (c5(st, c3, c4)) {
+        if (lane == 0) {
+          mbar_arrive_tx(bar, 256u * (uint32_t)(B * G));
+          asm volatile(
+              "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+              "%6}], [%7];\n" ::"r"(stage),
+              "l"(reinterpret_cast<uint64_t>(&h5)), "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(bar)
+              : "memory");
+        }
+      } else {
+        uint32_t bytes = 0;
+        for (int r = 0; r < ng; ++r) {
+          const long long qr = qb + r;
+          const long long ss = (a.seg.head && qr == 0) ? 1 : qr * C, se = min(qr * C + C, S);
+          if (st < se - ss) bytes += 256u * (uint32_t)B;
+        }
+        if (lane == 0) mbar_arrive_tx(bar, bytes);
+        if (my_on && st < my_len)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+              "[%5];\n" ::"r"(stage + my_dst),
+              "l"(reinterpret_cast<uint64_t>(&h3)), "r"(0), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(bar)
+              : "memory");
+      }
+    };
+    auto issue_stores = [&](int st, uint32_t gstep) {
+      const uint32_t stage = ring + (gstep % W_NST) * W_STAGE;
+      int c3, c4;
+      if (c5(st, c3, c4)) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(
+                           reinterpret_cast<uint64_t>(&g5)),
+                       "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(stage)
+                       : "memory");
+        }
+      } else if (my_on && st < my_len) {
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                         reinterpret_cast<uint64_t>(&g3)),
+                     "r"(0), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(stage + my_dst)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    };
+    if (issuer) {
+      // the stages about to be refilled were last stored from by these lanes
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      issue_loads(0, gs);
+      if (C > 1) issue_loads(1, gs + 1);
+      __syncwarp();
+    }
+    // bound of step 0 from the exact row maximum of the carry (two threads per row)
+    int s_cur;
+    {
+      float pm = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pm = fmaxf(pm, fmaxf(fabsf(v[i].x), fabsf(v[i].y)));
+      const uint32_t redp = red0 + par * (TM * 8);
+      asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+      named_bar(3 + g, W_EPI);
+      uint32_t m2[2];
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
+      const int eM = (int)(max(m2[0], m2[1]) >> 23) - 127;
+      s_cur = 14 - eM;                                      // max|x| <= max|v| < 2^(eM+1)
+      s_cur = max(-127 - sw, min(126 - sw, s_cur));
+      par ^= 1;
+      named_bar(5 + g, W_EPI);                              // the exchange words may be reused
+    }
+    int s_prev = 0;
+    for (int st = 0; st < C; ++st, ++gs) {
+      WTRACE(0);
+      if (issuer) {                                         // D of step st-1 and h of step st
+        if (lane == 0) {
+          if (st > 0) mbar_wait_s(dbar, dph);
+          mbar_wait_s(hbar0 + 8u * (gs % W_NST), (gs / W_NST) & 1);
+        }
+        __syncwarp();
+      }
+      named_bar(5 + g, W_EPI);
+      WTRACE(1);
+      if (st > 0) {                                         // v_st = (D1 + D2) 2^-(s_prev + sw)
+        dph ^= 1;
+        tc_fence_after();
+        float2 t[16];
+        load_d_sum<32>(t_d1, t_d2, t);
+        const float f = __int_as_float((127 - s_prev - sw) << 23);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __fmul2_rn(t[i], make_float2(f, f));
+        if (total && st == len) {                           // inclusive extra: J_0^T grad_h[0]
+          float4* dst = reinterpret_cast<float4*>(grad_init + (long long)bsm * TH + 32 * cgp);
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) dst[k4] = make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+        }
+      }
+      WTRACE(2);
+      WTRACE(3);
+      // x^ = (d o v) 2^s from the staged, swizzled h row; split into fp16 pairs
+      const uint32_t stg = ring + (gs % W_NST) * W_STAGE + hrow_off;
+      const float sc = __int_as_float((s_cur + 127) << 23);
+      float pm = 0.f;
+      uint32_t p1[16], p2[16];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t hp = stg + (uint32_t)((c ^ swz) << 4);
+        const float4 h4 = lds128(hp);
+        sts128(hp, v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);   // grad_h[t(s)] = v (exclusive)
+        const float2 d0 = make_float2(fmaf(-h4.x, h4.x, 1.f), fmaf(-h4.y, h4.y, 1.f));
+        const float2 d1 = make_float2(fmaf(-h4.z, h4.z, 1.f), fmaf(-h4.w, h4.w, 1.f));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float2 x = __fmul2_rn(__fmul2_rn(u ? d1 : d0, v[2 * c + u]), make_float2(sc, sc));
+          pm = fmaxf(pm, fmaxf(fabsf(x.x), fabsf(x.y)));
+          const float2 f1 = make_float2(__uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                                        __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
+          const float2 r = __fadd2_rn(x, make_float2(-f1.x, -f1.y));
+          p1[2 * c + u] = h2_bits(__floats2half2_rn(f1.x, f1.y));
+          p2[2 * c + u] = h2_bits(__floats2half2_rn(r.x, r.y));
+        }
+      }
+      fence_async_smem();                                   // grad_h rows -> visible to the TMA store
+      const uint32_t redp = red0 + par * (TM * 8);
+      asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+#pragma unroll
+      for (int h8 = 0; h8 < 2; ++h8) {
+        tmem_st8(t_a1 + 8 * h8, *reinterpret_cast<const uint32_t(*)[8]>(p1 + 8 * h8));
+        tmem_st8(t_a2 + 8 * h8, *reinterpret_cast<const uint32_t(*)[8]>(p2 + 8 * h8));
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tc_fence_before();
+      WTRACE(4);
+      named_bar(3 + g, W_EPI);                              // A stored, row maxima written, stage consumed
+      WTRACE(5);
+      if (issuer) {
+        tc_fence_after();
+        mma8_f16_commit(slot_base, bdesc, dbar);
+        issue_stores(st, gs);
+        if (st + 2 < C) {
+          // stage (gs+2) % 3 was stored from at step st-1: its reads must be done
+          asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+          issue_loads(st + 2, gs + 2);
+        }
+        __syncwarp();
+      }
+      uint32_t m2[2];
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
+      const int eM = (int)(max(m2[0], m2[1]) >> 23) - 127;
+      s_prev = s_cur;
+      s_cur = max(-127 - sw, min(126 - sw, 14 - eG - eM + s_cur + sw));
+      par ^= 1;
+      WTRACE(6);
+#ifdef BPPSA_STEP_TRACE
+      ++tstep;
+#endif
+    }
+    // D of the last step (keeps the barrier phase; grad_init if the chain ends here)
+    if (issuer) {
+      if (lane == 0) mbar_wait_s(dbar, dph);
+      __syncwarp();
+    }
+    named_bar(5 + g, W_EPI);
+    dph ^= 1;
+    tc_fence_after();
+    {
+      float2 t[16];
+      load_d_sum<32>(t_d1, t_d2, t);
+      if (total && len == C) {
+        const float f = __int_as_float((127 - s_prev - sw) << 23);
+        float4* dst = reinterpret_cast<float4*>(grad_init + (long long)bsm * TH + 32 * cgp);
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4)
+          dst[k4] = make_float4(t[2 * k4].x * f, t[2 * k4].y * f, t[2 * k4 + 1].x * f, t[2 * k4 + 1].y * f);
+      }
+    }
+  }
+  if (warp % W_WPS == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // grad_h stores done
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, cudaStream_t st) {
@@ -984,9 +1337,71 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
   return cudaGetLastError();
 }
 
-// Level-0 down-walk of an RNN H = 64 segment on the tensor cores.
+// Tensor maps of the walk over a [T][B][64] fp32 array (h or grad_h), 128-byte
+// swizzle: 3D {32, 2, T B} with box {32, 2, B} (one step of one level-0 block),
+// or 5D {32, 2, B, C, A} (time t = c4 C + c3, t < A C) with box {32, 2, B, 1,
+// G} (one step of G consecutive blocks).  The driver entry point is fetched
+// through the runtime, so nothing links against libcuda.
+static cudaError_t make_walk_map(const float* base, int T, int B, int C, long long A, bool five, int G,
+                                 CUtensorMap* map) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  const cuuint64_t row = (cuuint64_t)TH * sizeof(float);
+  const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+  CUresult r;
+  if (!five) {
+    const cuuint64_t dims[3] = {32, 2, (cuuint64_t)T * B};
+    const cuuint64_t strides[2] = {128, row};
+    const cuuint32_t box[3] = {32u, 2u, (cuuint32_t)B};
+    r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    if (A < 1) A = 1;
+    const cuuint64_t dims[5] = {32, 2, (cuuint64_t)B, (cuuint64_t)C, (cuuint64_t)A};
+    const cuuint64_t strides[4] = {128, row, row * B, row * B * C};
+    const cuuint32_t box[5] = {32u, 2u, (cuuint32_t)B, 1u, (cuuint32_t)G};
+    r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// Level-0 down-walk of an RNN H = 64 segment on the tensor cores: the 3xFP16
+// walk with per-run TMA loads (B <= 128), else the 3xTF32 per-row walk.
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                                 float* grad_init, int num_sms, cudaStream_t st) {
+  if (a.seg.B <= TM && !std::getenv("BPPSA_WALK_TF32")) {
+    const int B = a.seg.B, G = TM / B;
+    const long long Tm = (long long)a.seg.T - 1 + a.seg.head;
+    CUtensorMap maps[4];
+    cudaError_t e = cudaSuccess;
+    for (int m = 0; m < 4 && e == cudaSuccess; ++m)
+      e = make_walk_map(m < 2 ? a.h : grad_h, a.seg.T, B, C, Tm / C, m % 2 == 1, G, &maps[m]);
+    if (e != cudaSuccess) return e;
+    const long long A = Tm / C, nfull = A > 1 ? (A - 1) / G : 0, rem0 = 1 + nfull * G;
+    const long long nt = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
+    const int gridw = (int)std::min<long long>((nt + 1) / 2, num_sms);
+    static bool attrw = false;
+    if (!attrw) {
+      e = cudaFuncSetAttribute(tc_leaf_down_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attrw = true;
+    }
+    tc_leaf_down_f16_kernel<<<gridw, W_NT, W_SMEM_BYTES, st>>>(a, maps[0], maps[1], maps[2], maps[3], C, carry, nblk,
+                                                               grad_h, grad_init, G);
+    return cudaGetLastError();
+  }
   const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
   const int grid = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
   static bool attr16 = false;
