@@ -80,34 +80,59 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
     }
     s = s0 + 1;
   }
-  float pre[Tl::PER];
-  if (s < s1) {
-    const float* m = A.mat(b, s);
-#pragma unroll
-    for (int u = 0; u < Tl::PER; ++u) {
-      const int e = tid + u * Tl::NT;
-      pre[u] = (e < HH) ? m[e] : 0.f;
-    }
-  }
   int pc = 0, ac = 0;
-  for (; s < s1; ++s) {
+  if (HP == 64 && H == 64 && Tl::NT == 256) {
+    // H = 64: the next A_s (16 KB, column-major = A[k][i] rows of 64) is
+    // prefetched as four coalesced float4 per thread (scalar loads made this
+    // kernel LSU-throttled: r01h ncu, lg_throttle 20 %, LSU 47 %)
+    float4 pre4[4];
+    if (s < s1) {
+      const float4* m = reinterpret_cast<const float4*>(A.mat(b, s));
 #pragma unroll
-    for (int u = 0; u < Tl::PER; ++u) {         // element (i, k) at k*H + i -> A[k][i]
-      const int e = tid + u * Tl::NT;
-      if (e < HH) Ab[ac][(e / H) * HP + (e % H)] = pre[u];
+      for (int u = 0; u < 4; ++u) pre4[u] = __ldg(m + tid + u * 256);
     }
-    if (s + 1 < s1) {
-      const float* m = A.mat(b, s + 1);
+    for (; s < s1; ++s) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) reinterpret_cast<float4*>(Ab[ac])[tid + u * 256] = pre4[u];
+      if (s + 1 < s1) {
+        const float4* m = reinterpret_cast<const float4*>(A.mat(b, s + 1));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pre4[u] = __ldg(m + tid + u * 256);
+      }
+      __syncthreads();
+      gemm_step<HP, TM, TN>(Ab[ac], Pb[pc], Pb[pc ^ 1], tid);
+      pc ^= 1;
+      ac ^= 1;
+    }
+  } else {
+    float pre[Tl::PER];
+    if (s < s1) {
+      const float* m = A.mat(b, s);
 #pragma unroll
       for (int u = 0; u < Tl::PER; ++u) {
         const int e = tid + u * Tl::NT;
         pre[u] = (e < HH) ? m[e] : 0.f;
       }
     }
-    __syncthreads();
-    gemm_step<HP, TM, TN>(Ab[ac], Pb[pc], Pb[pc ^ 1], tid);
-    pc ^= 1;
-    ac ^= 1;
+    for (; s < s1; ++s) {
+#pragma unroll
+      for (int u = 0; u < Tl::PER; ++u) {         // element (i, k) at k*H + i -> A[k][i]
+        const int e = tid + u * Tl::NT;
+        if (e < HH) Ab[ac][(e / H) * HP + (e % H)] = pre[u];
+      }
+      if (s + 1 < s1) {
+        const float* m = A.mat(b, s + 1);
+#pragma unroll
+        for (int u = 0; u < Tl::PER; ++u) {
+          const int e = tid + u * Tl::NT;
+          pre[u] = (e < HH) ? m[e] : 0.f;
+        }
+      }
+      __syncthreads();
+      gemm_step<HP, TM, TN>(Ab[ac], Pb[pc], Pb[pc ^ 1], tid);
+      pc ^= 1;
+      ac ^= 1;
+    }
   }
   __syncthreads();
   float* dst = agg_out + ((long long)b * n_out + q) * HH;
