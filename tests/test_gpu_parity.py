@@ -411,3 +411,21 @@ def test_rnn_config4_full_size(lib):
     ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
     grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=bench.C4_BLOCK0, block=bench.C4_BLOCK)
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 5])
+def test_streamed_backward_from_host(lib, chunks):
+    """stream.py: host inputs copied in reverse-time chunks, each chunk's up/down
+    sweep launched as it lands (the bench's e2e path) == the oracle."""
+    from paper_1907_10134_b200.stream import StreamedRnnBackward
+    T, B, H, I = 3001, 4, 64, 1
+    w = W.rnn_workload(T, B, H, seed=77)
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    rW = bp.weight_grads_rnn(w.x, w.h, ref)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    sb = StreamedRnnBackward(T, B, H, I, chunks=chunks, block0=64, block=8)
+    dWih, dWhh, db, grad, gi = sb.run(pin(w.h), pin(w.x), pin(w.W_hh), pin(w.g))
+    torch.cuda.synchronize()
+    assert rel_pair(grad, ref, gi, ref_init) <= TOL
+    for got, want in zip((dWih, dWhh, db), rW):
+        assert rel(got, want) <= TOL
