@@ -164,11 +164,13 @@ struct Bars {
 // h_init) are zero.  IX = number of input columns (hi threads only).
 template <bool LO, int IX, bool FULL>
 __device__ __forceinline__ void convert_rows(uint32_t base, uint32_t xbase, int n, int nlow, float (&av)[16],
-                                             float (&bv)[16], float& dbias, float (&dih)[MAXI]) {
+                                             float (&bv)[16], float& dbias, float (&dih)[MAXI], uint32_t hp_lo,
+                                             uint32_t hp_hi, int nsplit) {
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
+    // h_prev row rr: rows < nsplit from hp_lo, the rest from hp_hi (see converters)
     const float hv = lds(base + rr * ROW_BYTES), gv = lds(base + (KC + rr) * ROW_BYTES),
-                pv = lds(base + (2 * KC + rr) * ROW_BYTES);
+                pv = lds(rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES);
     float d = (1.f - hv * hv) * gv, hp = pv;
     if (!FULL) {
       d = rr < n ? d : 0.f;
@@ -196,6 +198,7 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
   const int m = 32 * wq + lane, i = m & 63;
   const uint32_t tl = tmem + ((uint32_t)(32 * wq) << 16);
   const int NB = H + IX + 1;
+  const bool reuse = w.B <= KC;
   uint32_t cg = 0;
   for (long long part = blockIdx.x; part < w.nparts; part += gridDim.x) {
     float acc[64];
@@ -224,10 +227,31 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
       mbar_wait(br.full(s), (cg / NS) & 1);
       const uint32_t base = s0 + OFF_STAGE + s * SB + 4u * i + 16u * grp * ROW_BYTES;
       const uint32_t xbase = s0 + OFF_X + s * XB + 4u * 16 * grp * IX;
+      // h_prev = h shifted back by B rows: with B <= KC every chunk but a part's
+      // first reads it from its own h rows and the previous chunk's (still
+      // staged: a stage is released one chunk late), no third copy
+      uint32_t hp_lo, hp_hi;
+      int nsplit;
+      if (reuse && c > 0) {
+        const int r0 = 16 * grp - w.B;                    // chunk-relative row of my first h_prev
+        const uint32_t prev = s0 + OFF_STAGE + ((cg - 1) % NS) * SB + 4u * i;
+        hp_lo = prev + (uint32_t)((KC + r0) * ROW_BYTES);   // rows r0 .. -1 of the previous chunk
+        hp_hi = s0 + OFF_STAGE + s * SB + 4u * i + (uint32_t)(max(r0, 0) * ROW_BYTES);
+        nsplit = max(0, -r0);
+      } else {
+        hp_lo = base + 2 * KC * ROW_BYTES;
+        hp_hi = hp_lo;
+        nsplit = 0;
+      }
       float av[16], bv[16];
-      if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true>(base, xbase, n, nlow, av, bv, dbias, dih);
-      else convert_rows<LO, IX, false>(base, xbase, n, nlow, av, bv, dbias, dih);
-      mbar_arrive(br.empty(s));
+      if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
+      else convert_rows<LO, IX, false>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
+      if (!reuse) {
+        mbar_arrive(br.empty(s));
+      } else {
+        if (c > 0) mbar_arrive(br.empty((cg - 1) % NS));   // the previous chunk's rows are no longer read
+        if (c == nch - 1) mbar_arrive(br.empty(s));         // a part's last chunk is not read again
+      }
       if (c > 0 && c % FLUSH == 0) {           // window boundary: chunk cg-1 done, read D
         mbar_wait(br.freeb((cg - 1) % NBUF), ((cg - 1) / NBUF) & 1);
         tc_after();
@@ -305,8 +329,10 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
         const uint32_t st = s0 + OFF_STAGE + s * SB;
         // h_prev rows: [rb, rb+nA) come from h_init (rows < B), the rest from h
         const int nA = (int)max(0ll, min((long long)n, B - rb));
-        uint32_t tx = 2u * n * ROW_BYTES + (uint32_t)(n - nA) * ROW_BYTES;
-        if (w.h_init) tx += (uint32_t)nA * ROW_BYTES;
+        const bool reuse = B <= KC && ld.c > 0;          // h_prev from the staged h rows (converters)
+        uint32_t tx = 2u * n * ROW_BYTES;
+        if (!reuse) tx += (uint32_t)(n - nA) * ROW_BYTES;
+        if (!reuse && w.h_init) tx += (uint32_t)nA * ROW_BYTES;
         const float* xs = w.x + rb * w.I;
         const uint32_t xbytes = (uint32_t)(n * w.I * 4);
         const bool xbulk = w.I > 0 && (xbytes & 15) == 0;
@@ -318,9 +344,9 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
         mbar_expect_tx(br.full(s), tx);
         bulk_g2s(st, w.h + rb * H, (uint32_t)n * ROW_BYTES, br.full(s));
         bulk_g2s(st + KC * ROW_BYTES, w.g + rb * H, (uint32_t)n * ROW_BYTES, br.full(s));
-        if (nA > 0 && w.h_init)
+        if (!reuse && nA > 0 && w.h_init)
           bulk_g2s(st + 2 * KC * ROW_BYTES, w.h_init + rb * H, (uint32_t)nA * ROW_BYTES, br.full(s));
-        if (n > nA)
+        if (!reuse && n > nA)
           bulk_g2s(st + 2 * KC * ROW_BYTES + nA * ROW_BYTES, w.h + (rb + nA - B) * H, (uint32_t)(n - nA) * ROW_BYTES,
                    br.full(s));
         if (xbulk) bulk_g2s(s0 + OFF_X + s * XB, xs, xbytes, br.full(s));
