@@ -272,7 +272,11 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
           // 3xFP16 fold: the head block is folded as the matrix of its leaves
           // with all other blocks, then applied to the seed
           e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], 0, num_sms(), st, prec);
-          if (e == cudaSuccess && head) e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, st);
+          if (e == cudaSuccess && head) {                  // its own traced launch
+            tr.end(st);
+            tr.begin(st);
+            e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, st);
+          }
         } else {
           // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
           e = head ? launch_leaf_up(la, p.C[0], dst, p.n[1], 0, 1, st) : cudaSuccess;
