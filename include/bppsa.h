@@ -117,12 +117,14 @@ typedef struct bppsa_scan_opts {
   int mode;    /* bppsa_scan_mode                                              */
   int block0;  /* BLOCKED: leaf block length in slots (0 = default)            */
   int block;   /* BLOCKED: block length of the upper levels (0 = default)      */
-  int leaf_impl; /* level-0 fold engine: 0 = auto (tensor cores where they apply:
-                  * RNN with H = 64), 1 = FFMA (CUDA cores), 2 = tensor cores
-                  * (up-sweep fold as 3xFP16 with per-chain power-of-two
-                  * scaling), 3 = tensor cores with the 3xTF32 up-sweep fold.
-                  * 2 and 3 fail with BPPSA_ERR_NOT_SUPPORTED outside the tanh
-                  * RNN with H = 64.                                          */
+  int leaf_impl; /* level-0 fold engine: 0 = auto (tensor cores for the tanh
+                  * RNN with H = 64, CUDA cores otherwise), 1 = FFMA (CUDA
+                  * cores), 2 = tensor cores (up-sweep fold as 3xFP16 with
+                  * per-chain power-of-two scaling; tanh RNN with 16 <= H <= 64,
+                  * H % 4 == 0; the level-0 walk uses the tensor cores at H = 64
+                  * only), 3 = tensor cores with the 3xTF32 up-sweep fold (H =
+                  * 64).  2 and 3 fail with BPPSA_ERR_NOT_SUPPORTED outside
+                  * their range.                                              */
   /* Optional instrumentation (all may be NULL/0): if `events` is non-NULL the
    * library records events[2k] / events[2k+1] (cudaEvent_t, created by the
    * caller) on `stream` immediately before / after its k-th kernel launch,

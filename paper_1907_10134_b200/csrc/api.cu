@@ -99,9 +99,21 @@ int num_sms() {
 
 // tcgen05 level-0 fold: tanh RNN with H = 64 (a dense 64-wide contraction per
 // step); everything else runs on the CUDA cores.
+// fold: the 3xFP16 kernels take 16 <= H <= 64 with H % 4 == 0 (the 3xTF32
+// fold, leaf_impl 3, H = 64 only); the tensor-core walk is H = 64 only
+bool tensor_fold_ok(const bppsa_jac& j, int leaf_impl) {
+  if (j.kind != BPPSA_JAC_RNN_TANH) return false;
+  return leaf_impl == 3 ? j.H == 64 : (j.H >= 16 && j.H <= 64 && j.H % 4 == 0);
+}
+// auto (leaf_impl 0) takes the tensor cores at H = 64 only: below, the fold is
+// latency-bound (C2, H = 20: 0.45 ms on either engine; C1: 0.042 tensor vs
+// 0.033 ms FFMA) and the CUDA-core kernel keeps ~100x more chains in flight
 bool use_tensor_leaf(const bppsa_jac& j, int leaf_impl) {
-  const bool ok = j.kind == BPPSA_JAC_RNN_TANH && j.H == 64;
-  return leaf_impl >= 2 ? ok : (leaf_impl == 0 && ok);
+  const bool ok = tensor_fold_ok(j, leaf_impl);
+  return leaf_impl >= 2 ? ok : (leaf_impl == 0 && ok && j.H == 64);
+}
+bool use_tensor_walk(const bppsa_jac& j, int leaf_impl) {
+  return use_tensor_leaf(j, leaf_impl) && j.H == 64;
 }
 
 struct Plan {
@@ -166,8 +178,9 @@ bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts
   size_t off = 0;
   p->leaf_impl = opts ? opts->leaf_impl : 0;
   if (p->leaf_impl < 0 || p->leaf_impl > 3) return fail(BPPSA_ERR_INVALID_ARGUMENT, "leaf_impl must be 0, 1, 2 or 3");
-  if (p->leaf_impl >= 2 && !(j.kind == BPPSA_JAC_RNN_TANH && j.H == 64))
-    return fail(BPPSA_ERR_NOT_SUPPORTED, "tensor-core leaf fold is built for the tanh RNN with H = 64");
+  if (p->leaf_impl >= 2 && !tensor_fold_ok(j, p->leaf_impl))
+    return fail(BPPSA_ERR_NOT_SUPPORTED,
+                "tensor-core leaf fold: tanh RNN with 16 <= H <= 64, H % 4 == 0 (3xTF32: H = 64)");
   p->has_dense = (j.kind == BPPSA_JAC_DENSE) && mode != BPPSA_SCAN_ALG1;
   if (p->has_dense) {
     p->dense_off = off;
@@ -275,7 +288,7 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
           if (e == cudaSuccess && head) {                  // its own traced launch
             tr.end(st);
             tr.begin(st);
-            e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, st);
+            e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, H, st);
           }
         } else {
           // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
@@ -312,7 +325,7 @@ bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Pla
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
       // tcgen05 walk: many short chains (the linear scan's single long chain per
       // sample stays on the CUDA cores; so do single-block segments)
-      if (use_tensor_leaf(j, p.leaf_impl) && nblk >= 2 && Cl >= 8)
+      if (use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8)
         e = launch_tc_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st);
       else
         e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st);

@@ -76,7 +76,7 @@ cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n
 cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0,
                               int num_sms, cudaStream_t st, int prec);
 // level-1 head slot: column-major H = 64 matrix at lvl + b*bstride -> M . seed_b (in place)
-cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, cudaStream_t st);
+cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, int H, cudaStream_t st);
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                                 float* grad_init, int num_sms, cudaStream_t st);
 // level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable

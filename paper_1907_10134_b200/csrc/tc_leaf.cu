@@ -929,23 +929,288 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
 }
 
 
+// ---------------------------------------------------------------------------
+// The 3xFP16 fold for 16 <= H < 64 (H % 4 == 0; configs 1-2 have H = 20):
+// the H = 64 machinery with W zero-padded to 64 x 64, and a tile packed with
+// G = 128 / H groups of H chains (group = one level-0 block of one sample;
+// groups in (block, sample) order, so a tile may span blocks of different
+// lengths: every row carries its own start slot and length, its aggregate is
+// captured right after its last real step and its h rows stage as zeros
+// afterwards).  8 epilogue warps per slot as in tc_leaf_up_f16_kernel<8>;
+// columns >= H stay zero (d = 0 there).  HG steps are staged per chunk.
+// ---------------------------------------------------------------------------
+constexpr int HG = 16;
+
+__device__ __forceinline__ void w_scale_h(const float* W, int H, uint32_t* red, int* sw_out, float* G_out) {
+  uint32_t m = 0;
+  for (int e = threadIdx.x; e < H * H; e += blockDim.x) m = max(m, __float_as_uint(fabsf(__ldg(W + e))));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(red, m);
+  __syncthreads();
+  const int sw = max(-100, min(100, 141 - (int)(red[0] >> 23)));
+  uint32_t gs = 0;
+  if (threadIdx.x < H) {
+    float acc = 0.f;
+    for (int k = 0; k < H; ++k) acc += fabsf(__ldg(W + (long long)k * H + threadIdx.x));
+    gs = __float_as_uint(ldexpf(acc, sw) * (1.f + 1.f / 256.f));
+  }
+  gs = __reduce_max_sync(0xffffffffu, gs);
+  if ((threadIdx.x & 31) == 0 && threadIdx.x < ((H + 31) & ~31)) atomicMax(red + 1, gs);
+  __syncthreads();
+  *sw_out = sw;
+  *G_out = __uint_as_float(red[1]);
+}
+
+__global__ void __launch_bounds__(512, 1) tc_leaf_up_f16g_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                 long long n_out, long long q0) {
+  constexpr int WPS = 8, EPI = 32 * WPS, NT = 2 * EPI, NCG = 2, CPT = 32, NP = 16;
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + F_OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  uint32_t* wred = tmem_slot + 2;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B, H = a.seg.H;
+  const int GRP = TM / H;                                   // groups per tile
+  const long long S = a.seg.S();
+  const long long nq = n_out - q0;
+  const long long ngroups = (long long)B * nq;
+  const long long ntiles = (ngroups + GRP - 1) / GRP;
+
+  if (threadIdx.x < 2) wred[threadIdx.x] = 0;
+  __syncthreads();
+  int sw;
+  float G;
+  w_scale_h(a.W, H, wred, &sw, &G);
+  {
+    const float wsc = __int_as_float((sw + 127) << 23);
+    for (int e = threadIdx.x; e < TH * TH; e += NT) {
+      const int n = e / TH, k = e % TH;             // B[n][k] = W[k][n] 2^sw (zero beyond H)
+      const float w = (n < H && k < H) ? __ldg(a.W + (long long)k * H + n) * wsc : 0.f;
+      const __half w1 = __float2half_rn(w);
+      *reinterpret_cast<__half*>(smem + sw16_off(n, k)) = w1;
+      *reinterpret_cast<__half*>(smem + sw16_off(TH + n, k)) = __float2half_rn(w - __half2float(w1));
+    }
+  }
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) mbar_init(&d_full[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int g = warp / WPS, wl = warp % WPS;
+  const int row = (wl & 3) * 32 + lane;
+  const int cgp = wl >> 2;
+  const int et = wl * 32 + lane;
+  const bool issuer = wl == 0;
+  const uint32_t slot_base = tmem + 256 * g;
+  const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
+  const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_a1 = lane_base + 128 + NP * cgp, t_a2 = lane_base + 160 + NP * cgp;
+  float* hs = reinterpret_cast<float*>(smem + F_OFF_H + g * H_BYTES);    // [GRP][HG][64] d
+  const uint32_t hs_s = su32(hs);
+  float* dmx = reinterpret_cast<float*>(smem + F_OFF_DMX) + g * 2 * HCH;  // [GRP][HG] dmax (2 HCH >= 8 HG)
+  const uint32_t red0 = su32(smem + F_OFF_RED) + (uint32_t)(((g * 2) * TM + row) * 16);
+  const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+  uint64_t bdesc[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  uint32_t ph = 0, par = 0;
+  const long long rowB = (long long)B * H;
+  const int grp = row / H, j = row % H;
+  for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
+    const long long gf = tau * GRP + grp;
+    const bool ok = grp < GRP && gf < ngroups;
+    const long long q = q0 + (ok ? gf / B : 0);
+    const int b = ok ? (int)(gf % B) : 0;
+    const long long s0 = (a.seg.head && q == 0) ? 1 : q * C, s1 = min(q * C + (long long)C, S);
+    const int len = ok ? (int)max(0LL, s1 - s0) : 0;
+    // steps of the tile: the longest of its groups
+    int nsteps = 0;
+    for (int r = 0; r < GRP; ++r) {
+      const long long gr = tau * GRP + r;
+      if (gr >= ngroups) break;
+      const long long qr = q0 + gr / B;
+      const long long sr0 = (a.seg.head && qr == 0) ? 1 : qr * C, sr1 = min(qr * C + (long long)C, S);
+      nsteps = max(nsteps, (int)max(0LL, sr1 - sr0));
+    }
+    float2 c2[NP];
+    int E = 0;
+    float bound = 1.f / G;
+    bool first = true;
+    float* aggrow = agg_out + (((long long)b * n_out + q) * H + j) * H;
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+      c2[i] = make_float2((CPT * cgp + 2 * i == j && ok) ? 1.f : 0.f, (CPT * cgp + 2 * i + 1 == j && ok) ? 1.f : 0.f);
+    if (ok && len == 0) {                           // an empty head block: the identity
+      for (int c = 0; c < H; ++c)
+        if (c >= CPT * cgp && c < CPT * cgp + CPT) aggrow[c] = (c == j) ? 1.f : 0.f;
+    }
+    for (int sb = 0; sb < nsteps; sb += HG) {
+      const int n = min(HG, nsteps - sb);
+      named_bar(1 + g, EPI);                        // the previous chunk's d is consumed
+      // stage h rows (H floats, 16-byte pieces) of every group, zeros past a group's length
+      const int nc4 = H / 4;
+      for (int e = et; e < GRP * n * 16; e += EPI) {
+        const int r = e / (n * 16), rem = e % (n * 16), st = rem / 16, c4 = rem % 16;
+        float* dst = hs + (r * HG + st) * TH + c4 * 4;
+        const long long gr = tau * GRP + r;
+        bool live = false;
+        long long src = 0;
+        if (gr < ngroups && c4 < nc4) {
+          const long long qr = q0 + gr / B;
+          const int br = (int)(gr % B);
+          const long long sr0 = (a.seg.head && qr == 0) ? 1 : qr * C, sr1 = min(qr * C + (long long)C, S);
+          if (sb + st < sr1 - sr0) {
+            live = true;
+            src = (long long)a.seg.time_of(sr0 + sb + st) * rowB + (long long)br * H + c4 * 4;
+          }
+        }
+        if (live) cp_async16(dst, a.h + src);
+        else sts128(su32(dst), 1.f, 1.f, 1.f, 1.f);  // h = 1: d = 0 (padding columns, finished groups)
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      named_bar(1 + g, EPI);
+      const int tot = GRP * n * 16;
+      for (int e = et; e < ((tot + 31) & ~31); e += EPI) {   // d = 1 - h^2 in place, dmax per (group, step)
+        const bool v = e < tot;                     // whole warps iterate (16 lanes per row)
+        const int r = e / (n * 16), rem = e % (n * 16), st = rem / 16, c4 = rem % 16;
+        float m = 0.f;
+        if (v) {
+          const uint32_t p = hs_s + 4u * ((r * HG + st) * TH + c4 * 4);
+          const float4 h4 = lds128(p);
+          const float4 d4 = make_float4(1.f - h4.x * h4.x, 1.f - h4.y * h4.y, 1.f - h4.z * h4.z, 1.f - h4.w * h4.w);
+          sts128(p, d4.x, d4.y, d4.z, d4.w);
+          m = fmaxf(fmaxf(d4.x, d4.y), fmaxf(d4.z, d4.w));
+        }
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (v && c4 == 0) dmx[r * HG + st] = m;
+      }
+      named_bar(1 + g, EPI);
+      const int grs = min(grp, GRP - 1);            // idle rows read group GRP-1's data (finite, unused)
+      uint32_t dp = hs_s + 4u * (grs * HG * TH + CPT * cgp);
+      uint32_t dmp = su32(dmx + grs * HG);
+      for (int st = 0; st < n; ++st, dp += 4u * TH, dmp += 4u) {
+        const int gst = sb + st;
+        float dms;
+        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(dms) : "r"(dmp));
+        const float f = G * bound * dms;
+        const int s = min(127, 141 - (int)(__float_as_uint(f) >> 23));
+        const float2 scl = make_float2(__int_as_float((s + 127) << 23), __int_as_float((s + 127) << 23));
+        float2 ds[NP];
+#pragma unroll
+        for (int q4 = 0; q4 < CPT / 4; ++q4) {
+          const float4 d4 = lds128(dp + 16u * q4);
+          ds[2 * q4] = __fmul2_rn(make_float2(d4.x, d4.y), scl);
+          ds[2 * q4 + 1] = __fmul2_rn(make_float2(d4.z, d4.w), scl);
+        }
+        if (!first) {
+          if (issuer) {
+            if (lane == 0) mbar_wait(&d_full[g], ph);
+            __syncwarp();
+          }
+          named_bar(5 + g, EPI);
+          ph ^= 1;
+          tc_fence_after();
+          load_d_sum<CPT>(t_d1, t_d2, c2);
+          if (ok && gst == len) {                   // aggregate after the group's last real step
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+              const int c = CPT * cgp + 2 * i;
+              if (c < H) aggrow[c] = ldexpf(c2[i].x, -E);
+              if (c + 1 < H) aggrow[c + 1] = ldexpf(c2[i].y, -E);
+            }
+          }
+        }
+        E += s + sw;
+        first = false;
+        float pm = 0.f;
+        uint32_t p1[NP], p2[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const float2 x = __fmul2_rn(c2[i], ds[i]);
+          pm = fmaxf(pm, fmaxf(fabsf(x.x), fabsf(x.y)));
+          const float2 f1 = make_float2(__uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                                        __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
+          const float2 r = __fadd2_rn(x, make_float2(-f1.x, -f1.y));
+          p1[i] = h2_bits(__floats2half2_rn(f1.x, f1.y));
+          p2[i] = h2_bits(__floats2half2_rn(r.x, r.y));
+        }
+        const uint32_t redp = red0 + par * (TM * 16);
+        asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+#pragma unroll
+        for (int h8 = 0; h8 < NP / 8; ++h8) {
+          tmem_st8(t_a1 + 8 * h8, *reinterpret_cast<const uint32_t(*)[8]>(p1 + 8 * h8));
+          tmem_st8(t_a2 + 8 * h8, *reinterpret_cast<const uint32_t(*)[8]>(p2 + 8 * h8));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        named_bar(3 + g, EPI);
+        if (issuer) {
+          tc_fence_after();
+          mma8_f16_commit(slot_base, bdesc, su32(&d_full[g]));
+        }
+        uint32_t m2[2];
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
+        bound = __uint_as_float(max(m2[0], m2[1]));
+        par ^= 1;
+      }
+    }
+    if (!first) {                                   // D of the tile's last step
+      if (issuer) {
+        if (lane == 0) mbar_wait(&d_full[g], ph);
+        __syncwarp();
+      }
+      named_bar(5 + g, EPI);
+      ph ^= 1;
+      tc_fence_after();
+      load_d_sum<CPT>(t_d1, t_d2, c2);
+      if (ok && len == nsteps && len > 0) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const int c = CPT * cgp + 2 * i;
+          if (c < H) aggrow[c] = ldexpf(c2[i].x, -E);
+          if (c + 1 < H) aggrow[c + 1] = ldexpf(c2[i].y, -E);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // Head block of level 1: slot 0 holds the column-major aggregate M of the
 // head block's leaves (written by the fold above); replace it in place by the
 // vector M . seed (the head aggregate of the scan: a[C-1]...a[1] a[0]
 // with a[0] = the seed).  One CTA per sample; the matrix is read before the
 // vector overwrites its first column.
 __global__ void __launch_bounds__(TH) head_apply_kernel(float* __restrict__ lvl, long long bstride,
-                                                        const float* __restrict__ seed) {
+                                                        const float* __restrict__ seed, int H) {
   __shared__ float sd[TH];
   const int b = blockIdx.x, i = threadIdx.x;
   float* M = lvl + (long long)b * bstride;
-  sd[i] = seed[(long long)b * TH + i];
+  if (i < H) sd[i] = seed[(long long)b * H + i];
   __syncthreads();
   float v = 0.f;
-#pragma unroll 8
-  for (int j = 0; j < TH; ++j) v = fmaf(M[(long long)j * TH + i], sd[j], v);
+  if (i < H)
+    for (int j = 0; j < H; ++j) v = fmaf(M[(long long)j * H + i], sd[j], v);
   __syncthreads();
-  M[i] = v;
+  if (i < H) M[i] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -1302,8 +1567,8 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
 
 }  // namespace
 
-cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, cudaStream_t st) {
-  head_apply_kernel<<<B, TH, 0, st>>>(lvl, bstride, seed);
+cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, int H, cudaStream_t st) {
+  head_apply_kernel<<<B, TH, 0, st>>>(lvl, bstride, seed, H);
   return cudaGetLastError();
 }
 
@@ -1315,6 +1580,21 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
   const long long pairs = (ntiles + 1) / 2;
   const int grid = (int)std::min<long long>(pairs, num_sms);
   if (grid <= 0) return cudaSuccess;
+  if (a.seg.H != TH) {                             // 3xFP16, 16 <= H < 64: packed groups
+    const long long ngroups = (long long)a.seg.B * (n_out - q0);
+    const long long ntg = (ngroups + TM / a.seg.H - 1) / (TM / a.seg.H);
+    const int gridg = (int)std::min<long long>((ntg + 1) / 2, num_sms);
+    if (gridg <= 0) return cudaSuccess;
+    static bool attrg = false;
+    if (!attrg) {
+      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           F_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attrg = true;
+    }
+    tc_leaf_up_f16g_kernel<<<gridg, 512, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+    return cudaGetLastError();
+  }
   if (prec == 0) {                                 // 3xFP16, 8 epilogue warps per slot
     static bool attrf = false;
     if (!attrf) {

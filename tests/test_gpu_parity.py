@@ -79,6 +79,22 @@ def test_rnn_tensor_leaf_realistic(lib, T, blocks, impl):
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
 
 
+@pytest.mark.parametrize("H", [16, 20, 32, 48, 60])
+@pytest.mark.parametrize("T,B,blocks", [(1000, 16, (0, 0)), (3001, 5, (16, 4)), (700, 3, (64, 8)), (40, 7, (8, 2))])
+def test_rnn_tensor_leaf_small_H(lib, H, T, B, blocks):
+    """3xFP16 fold at 16 <= H < 64 (configs 1-2 have H = 20): W zero-padded to
+    64, G = 128 // H groups of H chains per tile, groups of different blocks
+    (head block, ragged last block) in one tile."""
+    w = W.rnn_workload(T, B, H, seed=T + H)
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=blocks[0], block=blocks[1], leaf_impl="tensor")
+    assert rel_pair(grad, ref, gi, ref_init) <= TOL
+    f = W.norm_preserving_rnn(T, B, H, seed=H)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1], leaf_impl="tensor")
+    assert rel_pair(gt, ref, it, ref_init) <= max(TOL, T * BIAS_PER_STEP)
+
+
 @pytest.mark.parametrize("wscale", [1e-20, 1e-3, 1.0])
 def test_rnn_tensor_leaf_scaling_range(lib, wscale):
     """The 3xFP16 fold rescales W once and every chain row at every step by
