@@ -140,6 +140,34 @@ __device__ __forceinline__ void matvec_multi(const float (&w)[NX<CELL>::v][NR][H
   }
 }
 
+// RNN, H <= 32 (one row per lane): x stored chain-minor, xb[k][j], so one
+// 16-byte broadcast read yields x_j[k] for four chains and the products run on
+// the paired fp32 pipe (FFMA2, W_ki broadcast to both halves): half the issue
+// slots of the scalar loop, and the x store is NC/4 vector stores per lane
+template <int HT, int NC>
+__device__ __forceinline__ void matvec_multi_t(const float (&w)[1][1][HT], const float* __restrict__ xb,
+                                               float (&acc)[NC][1]) {
+  static_assert(NC % 4 == 0, "chains in fours");
+  float2 a2[NC / 2];
+#pragma unroll
+  for (int p = 0; p < NC / 2; ++p) a2[p] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < HT; ++k) {
+    const float2 wk = make_float2(w[0][0][k], w[0][0][k]);
+#pragma unroll
+    for (int j4 = 0; j4 < NC / 4; ++j4) {
+      const float4 x4 = *reinterpret_cast<const float4*>(xb + k * NC + 4 * j4);
+      a2[2 * j4] = __ffma2_rn(make_float2(x4.x, x4.y), wk, a2[2 * j4]);
+      a2[2 * j4 + 1] = __ffma2_rn(make_float2(x4.z, x4.w), wk, a2[2 * j4 + 1]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < NC / 2; ++p) {
+    acc[2 * p][0] = a2[p].x;
+    acc[2 * p + 1][0] = a2[p].y;
+  }
+}
+
 template <int CELL, int HT, int NC>
 struct UpBounds { static constexpr int minb = (CELL == BPPSA_JAC_RNN_TANH && HT == 64) ? 3 : 1; };
 
@@ -206,21 +234,39 @@ __global__ void __launch_bounds__(128, UpBounds<CELL, HT, NC>::minb) leaf_up_ker
       }
     }
     float* xb = xs + buf * XW;
+    constexpr bool TRANS = CELL == BPPSA_JAC_RNN_TANH && NR == 1 && NC % 4 == 0;
+    if constexpr (TRANS) {
+      if (lane < HT) {                              // xb[i][j] = d_i c_j[i], four chains per store
 #pragma unroll
-    for (int j = 0; j < NC; ++j) {
+        for (int j4 = 0; j4 < NC / 4; ++j4) {
+          float4 v4;
+          v4.x = (4 * j4 + 0 < nc) ? cur[0].c[0] * c[4 * j4 + 0][0] : 0.f;
+          v4.y = (4 * j4 + 1 < nc) ? cur[0].c[0] * c[4 * j4 + 1][0] : 0.f;
+          v4.z = (4 * j4 + 2 < nc) ? cur[0].c[0] * c[4 * j4 + 2][0] : 0.f;
+          v4.w = (4 * j4 + 3 < nc) ? cur[0].c[0] * c[4 * j4 + 3][0] : 0.f;
+          *reinterpret_cast<float4*>(xb + lane * NC + 4 * j4) = v4;
+        }
+      }
+    } else {
 #pragma unroll
-      for (int m = 0; m < NR; ++m) {
-        const int i = lane + 32 * m;
-        if (i < HT) {
+      for (int j = 0; j < NC; ++j) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v) xb[(j * NV + v) * HT + i] = (j < nc) ? cur[m].c[v] * c[j][m] : 0.f;
+        for (int m = 0; m < NR; ++m) {
+          const int i = lane + 32 * m;
+          if (i < HT) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) xb[(j * NV + v) * HT + i] = (j < nc) ? cur[m].c[v] * c[j][m] : 0.f;
+          }
         }
       }
     }
     __syncwarp();
     {
       float acc[NC][NR];
-      matvec_multi<CELL, HT, NR, NC>(w, xb, acc);    // chains j >= nc compute on zeros
+      if constexpr (TRANS)
+        matvec_multi_t<HT, NC>(w, xb, acc);
+      else
+        matvec_multi<CELL, HT, NR, NC>(w, xb, acc);    // chains j >= nc compute on zeros
 #pragma unroll
       for (int j = 0; j < NC; ++j)
 #pragma unroll
