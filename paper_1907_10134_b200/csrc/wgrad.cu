@@ -18,8 +18,16 @@ namespace bppsa {
 namespace {
 
 constexpr int TA = 64, RR = 32, NT = 256, MAXE = 64;
-constexpr int PER_A = RR * TA / NT;   // 8 elements of A per thread per stage
-constexpr int PER_U = RR * TA / NT;   // 8 elements of U (hidden part) per thread per stage
+// tile shapes: <64, 64>: 64-wide A and U tiles, 256 threads (H up to 64);
+// <32, 16>: 32-wide tiles, 64 threads, up to 16 extra columns (H <= 32:
+// configs 1-3 have H = 20, where the 64-wide tile was 90 % padding)
+template <int TA_, int MAXE_>
+struct WT {
+  static constexpr int NT = (TA_ / 4) * (TA_ / 4);
+  static constexpr int PER = RR * TA_ / NT;       // A and U (hidden part) elements per thread per stage
+  static constexpr int PE = MAXE_ * RR / NT;      // extra-column elements per thread per stage
+  static constexpr int NEA = 16;                  // extra outputs per thread
+};
 
 struct WArgs {
   int T, B, H, I, kind;
@@ -58,25 +66,28 @@ __device__ __forceinline__ float valE(const WArgs& w, long long row, int c) {   
   return (c < w.I) ? w.x[row * w.I + c] : 1.f;
 }
 
-__global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __restrict__ ws) {
+template <int TA, int MAXE>
+__global__ void __launch_bounds__(WT<TA, MAXE>::NT) wgrad_partial_kernel(WArgs w, float* __restrict__ ws) {
+  constexpr int NT = WT<TA, MAXE>::NT, PER_A = WT<TA, MAXE>::PER, PER_U = WT<TA, MAXE>::PER;
+  constexpr int GI = TA / 4;
   __shared__ __align__(16) float As[2][RR][TA];
   __shared__ __align__(16) float Us[2][RR][TA];
   __shared__ float Es[2][RR][MAXE];
   const int part = blockIdx.x, ta = blockIdx.y;
   const long long r0 = (long long)part * w.rows_per_part;
   const long long r1 = min(r0 + w.rows_per_part, w.rows);
-  const int tid = threadIdx.x, ti = tid % 16, tj = tid / 16;
+  const int tid = threadIdx.x, ti = tid % GI, tj = tid / GI;
   const int nE = TA * w.E;                          // extra outputs of this A slice
   float acc[4][4];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
-  float eacc[16];
+  float eacc[WT<TA, MAXE>::NEA];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) eacc[u] = 0.f;
+  for (int u = 0; u < WT<TA, MAXE>::NEA; ++u) eacc[u] = 0.f;
 
-  float pa[PER_A], pu[PER_U], pe[MAXE * RR / NT];
+  float pa[PER_A], pu[PER_U], pe[WT<TA, MAXE>::PE];
   auto fetch = [&](long long rb) {
 #pragma unroll
     for (int u = 0; u < PER_A; ++u) {
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __res
       pu[u] = (row < r1) ? valU(w, row, col) : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < MAXE * RR / NT; ++u) {
+    for (int u = 0; u < WT<TA, MAXE>::PE; ++u) {
       const int e = tid + u * NT, rr = e / MAXE, col = e % MAXE;
       const long long row = rb + rr;
       pe[u] = (row < r1 && col < w.E) ? valE(w, row, col) : 0.f;
@@ -100,7 +111,7 @@ __global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __res
       Us[buf][rr][col] = pu[u];
     }
 #pragma unroll
-    for (int u = 0; u < MAXE * RR / NT; ++u) {
+    for (int u = 0; u < WT<TA, MAXE>::PE; ++u) {
       const int e = tid + u * NT;
       Es[buf][e / MAXE][e % MAXE] = pe[u];
     }
@@ -124,7 +135,7 @@ __global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __res
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(av[x], uv[y], acc[x][y]);
     }
-    for (int u = 0; u < 16; ++u) {                    // extra columns: x_t and the bias
+    for (int u = 0; u < WT<TA, MAXE>::NEA; ++u) {   // extra columns: x_t and the bias
       const int e = tid + u * NT;
       if (e >= nE) break;
       const int a = e / w.E, c = e % w.E;
@@ -148,7 +159,7 @@ __global__ void __launch_bounds__(NT) wgrad_partial_kernel(WArgs w, float* __res
       if (c < w.H) dst[(long long)a * NB + c] = acc[x][y];
     }
   }
-  for (int u = 0; u < 16; ++u) {
+  for (int u = 0; u < WT<TA, MAXE>::NEA; ++u) {
     const int e = tid + u * NT;
     if (e >= nE) break;
     const int a = ta * TA + e / w.E, c = e % w.E;
@@ -238,8 +249,13 @@ cudaError_t reduce_rnn(const float* ws, long long P, int H, int I, float* dW_ih,
 }
 
 cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream_t st) {
-  dim3 grid((unsigned)nparts, (unsigned)((w.NA + TA - 1) / TA));
-  wgrad_partial_kernel<<<grid, NT, 0, st>>>(w, ws);
+  if (w.H <= 32 && w.E <= 16 && 32 * w.E <= WT<32, 16>::NEA * WT<32, 16>::NT) {
+    dim3 grid((unsigned)nparts, (unsigned)((w.NA + 31) / 32));
+    wgrad_partial_kernel<32, 16><<<grid, WT<32, 16>::NT, 0, st>>>(w, ws);
+  } else {
+    dim3 grid((unsigned)nparts, (unsigned)((w.NA + TA - 1) / TA));
+    wgrad_partial_kernel<64, 64><<<grid, WT<64, 64>::NT, 0, st>>>(w, ws);
+  }
   return cudaGetLastError();
 }
 
