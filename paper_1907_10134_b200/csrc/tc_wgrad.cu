@@ -72,9 +72,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
                "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps in the barrier
+// unit instead of re-issuing the probe (256 converter threads spinning cost
+// ~25 % of the kernel's issued instructions: r01i ncu)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
-                   bar), "r"(parity) : "memory");
+  asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra W_%=;\n}\n" ::"r"(
+                   bar), "r"(parity), "r"(1000000u) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
@@ -162,15 +165,17 @@ struct Bars {
 // (h_prev hi or lo) of rows 16*grp .. 16*grp+15 (base = stage + column i +
 // 16*grp rows); rows >= n are zero, h_prev rows < nlow (before h_0 with no
 // h_init) are zero.  IX = number of input columns (hi threads only).
-template <bool LO, int IX, bool FULL>
+template <bool LO, int IX, bool FULL, bool SPLIT>
 __device__ __forceinline__ void convert_rows(uint32_t base, uint32_t xbase, int n, int nlow, float (&av)[16],
                                              float (&bv)[16], float& dbias, float (&dih)[MAXI], uint32_t hp_lo,
                                              uint32_t hp_hi, int nsplit) {
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
-    // h_prev row rr: rows < nsplit from hp_lo, the rest from hp_hi (see converters)
+    // h_prev row rr: rows < nsplit from hp_lo, the rest from hp_hi (see
+    // converters); !SPLIT: every row from hp_lo
     const float hv = lds(base + rr * ROW_BYTES), gv = lds(base + (KC + rr) * ROW_BYTES),
-                pv = lds(rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES);
+                pv = lds(!SPLIT ? hp_lo + rr * ROW_BYTES
+                                : (rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES));
     float d = (1.f - hv * hv) * gv, hp = pv;
     if (!FULL) {
       d = rr < n ? d : 0.f;
@@ -244,8 +249,14 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
         nsplit = 0;
       }
       float av[16], bv[16];
-      if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
-      else convert_rows<LO, IX, false>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
+      if (nsplit == 0 || nsplit >= 16) {               // my 16 h_prev rows are contiguous
+        const uint32_t hp = nsplit == 0 ? hp_hi : hp_lo;
+        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, false>(base, xbase, n, nlow, av, bv, dbias, dih, hp, hp, 16);
+        else convert_rows<LO, IX, false, false>(base, xbase, n, nlow, av, bv, dbias, dih, hp, hp, 16);
+      } else {
+        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, true>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
+        else convert_rows<LO, IX, false, true>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
+      }
       if (!reuse) {
         mbar_arrive(br.empty(s));
       } else {
