@@ -445,3 +445,16 @@ def test_streamed_backward_from_host(lib, chunks):
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
     for got, want in zip((dWih, dWhh, db), rW):
         assert rel(got, want) <= TOL
+
+
+@pytest.mark.parametrize("B", [9, 24, 130])
+def test_rnn_tensor_walk_group_shapes(lib, B):
+    """The TMA walk packs G = 128 // B whole groups of B chains per tile (9 ->
+    14 groups + 2 idle rows, 24 -> 5 groups + 8 idle); B > 128 falls back to
+    the per-row 3xTF32 walk.  T spans merged-box tiles, the block-0 tile and
+    per-group tail tiles."""
+    T = 4101
+    w = W.rnn_workload(T, B, 64, seed=B)
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=64, block=8, leaf_impl="tensor")
+    assert rel_pair(grad, ref, gi, ref_init) <= TOL
