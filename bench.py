@@ -448,6 +448,41 @@ def sweep_small(api, args):
     out["c3"] = {"set": "L (1034 x 12)", "B": 64, "H": 20, "bppsa_ms_eager": round(_time(bwd_gru), 4),
                  "cudnn_backward_ms": round(cudnn_backward_ms(1034, 64, 20, 12, reps=5, x=gw.x, gru=True), 4)}
     out["c5"] = sweep_csr(api)
+    out["train"] = sweep_train()
+    return out
+
+
+def sweep_train():
+    """End-to-end training iterations (cuDNN forward + backward + Adam) on the
+    paper's bitstream task, BPPSA backward vs torch autograd
+    (cuDNN backward); same model, data and optimizer (paper_1907_10134_b200/train.py)."""
+    import copy
+    import torch
+    import bppsa_workloads as W
+    from paper_1907_10134_b200.train import AutogradTrainer, BitstreamRnn, BppsaTrainer
+    out = {}
+    for name, (T, B, H, C0, C) in {"c1": (1000, 16, 20, 8, 8), "c2": (30000, 16, 20, 16, 16)}.items():
+        torch.manual_seed(0)
+        ma = BitstreamRnn(H=H).cuda()
+        mb = copy.deepcopy(ma)
+        mb.rnn.flatten_parameters()
+        ta, tb = BppsaTrainer(ma, lr=1e-5, block0=C0, block=C), AutogradTrainer(mb, lr=1e-5)
+        x, y = W.bitstreams(T, B, seed=7)
+        x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        res = {}
+        for tag, tr in (("bppsa_iter_ms", ta), ("autograd_iter_ms", tb)):
+            for _ in range(3):
+                tr.step(x, y)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                tr.step(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            res[tag] = round(e0.elapsed_time(e1) / 10, 4)
+        res["speedup"] = round(res["autograd_iter_ms"] / res["bppsa_iter_ms"], 2)
+        out[name] = {"T": T, "B": B, "H": H, **res}
     return out
 
 

@@ -1,0 +1,64 @@
+"""End-to-end training with the BPPSA backward: the same
+model, data and optimizer as torch autograd (cuDNN backward), only the
+backward differs, so the trajectories agree up to fp32 association."""
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import bppsa_workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("T,B,H", [(2000, 16, 20), (1500, 16, 64), (777, 5, 32)])
+def test_bppsa_training_matches_autograd(lib, T, B, H):
+    from paper_1907_10134_b200.train import AutogradTrainer, BitstreamRnn, BppsaTrainer
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.manual_seed(0)
+    ma = BitstreamRnn(H=H).cuda()
+    mb = copy.deepcopy(ma)
+    mb.rnn.flatten_parameters()
+    ta, tb = BppsaTrainer(ma, lr=1e-3, block0=64), AutogradTrainer(mb, lr=1e-3)
+    la, lb = [], []
+    for it in range(25):
+        x, y = W.bitstreams(T, B, seed=100 + it)
+        x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        la.append(ta.step(x, y))
+        lb.append(tb.step(x, y))
+        if it == 0:     # identical forward and head; the BPPSA gradients == autograd's
+            assert la[0] == pytest.approx(lb[0], rel=1e-6)
+    la, lb = np.array(la), np.array(lb)
+    assert np.abs(la - lb).max() <= 1e-3 * np.abs(lb).max(), (la, lb)
+    for pa, pb in zip(ma.parameters(), mb.parameters()):
+        d = (pa - pb).abs().max().item()
+        assert d <= 1e-3 * max(pb.abs().max().item(), 1e-3), d
+
+
+def test_bppsa_gradients_equal_autograd(lib):
+    """One backward, no update: every parameter gradient within 1e-4 (max-norm
+    relative) of torch autograd's."""
+    from paper_1907_10134_b200 import api
+    torch.backends.cudnn.allow_tf32 = False
+    T, B, H = 3000, 8, 64
+    torch.manual_seed(3)
+    from paper_1907_10134_b200.train import BitstreamRnn
+    m = BitstreamRnn(H=H).cuda()
+    x, y = W.bitstreams(T, B, seed=5)
+    x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    h, logits = m(x)
+    torch.nn.functional.cross_entropy(logits, y).backward()
+    ref = {n: p.grad.clone() for n, p in m.rnn.named_parameters()}
+    with torch.no_grad():
+        h, _ = m.rnn(x)
+    hl = h[-1].detach().requires_grad_(True)
+    torch.nn.functional.cross_entropy(m.head(hl), y).backward()
+    jac = api.jacobians_rnn(h.contiguous(), m.rnn.weight_hh_l0.detach().contiguous())
+    grad, _ = api.scan(jac, hl.grad.contiguous())
+    dWih, dWhh, db = api.weight_grads_rnn(x, h.contiguous(), grad)
+    got = {"weight_ih_l0": dWih, "weight_hh_l0": dWhh, "bias_ih_l0": db, "bias_hh_l0": db}
+    for n, g in got.items():
+        r = ref[n]
+        assert (g - r).abs().max().item() <= 1e-4 * r.abs().max().item(), n
