@@ -449,7 +449,49 @@ def sweep_small(api, args):
                  "cudnn_backward_ms": round(cudnn_backward_ms(1034, 64, 20, 12, reps=5, x=gw.x, gru=True), 4)}
     out["c5"] = sweep_csr(api)
     out["train"] = sweep_train()
+    out["hybrid"] = sweep_hybrid(api)
     return out
+
+
+def sweep_hybrid(api):
+    """the level-balanced hybrid on C1's
+    materialised leaves (T = 1000, B = 16, H = 20): scan ms per
+    (up_levels, down_levels), CUDA-graph replayed, next to the blocked
+    scan on the same DENSE descriptor."""
+    import torch
+    import bppsa_workloads as W
+    T, B, H = 1000, 16, 20
+    w = W.rnn_workload(T, B, H, seed=1)
+    JT = torch.empty((T, B, H, H), device="cuda")
+    api.jacobians_rnn(torch.from_numpy(w.h).cuda(), torch.from_numpy(w.W_hh).cuda(), JT_out=JT)
+    jac = api.jacobians_dense(JT)
+    g = torch.from_numpy(w.g).cuda()
+    grad = torch.empty((T, B, H), device="cuda")
+    L = T.bit_length()
+
+    def graph_ms(fn):
+        fn()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gr, stream=s, capture_error_mode="relaxed"):
+                fn()
+        torch.cuda.synchronize()
+        return round(_time(gr.replay, reps=20), 4)
+
+    res = {}
+    for u in range(0, L):
+        lv = (u, u + 1) if u + 1 <= L else (u, u)
+        ws = api.workspace(api.scan_workspace_size(jac, "hybrid", levels=lv))
+        res[f"u{lv[0]}_d{lv[1]}"] = graph_ms(
+            lambda ws=ws, lv=lv: api.scan(jac, g, grad_h=grad, ws=ws, mode="hybrid", levels=lv))
+    wsb = api.workspace(api.scan_workspace_size(jac, "blocked", 8, 8))
+    res["blocked_8_8"] = graph_ms(lambda: api.scan(jac, g, grad_h=grad, ws=wsb, block0=8, block=8))
+    return {"T": T, "B": B, "H": H, "leaves": "materialised J^T (DENSE)", "scan_ms_graph": res}
 
 
 def sweep_train():

@@ -110,7 +110,18 @@ typedef enum {
   BPPSA_SCAN_ALG1 = 1,
   /* The linear scan = sequential BP on the GPU (S_Linear = Theta(n)):
    * the comparator.                                                          */
-  BPPSA_SCAN_LINEAR = 2
+  BPPSA_SCAN_LINEAR = 2,
+  /* The level-balanced hybrid of P:472 (reading 19):
+   * the first `up_levels` = u up-sweep levels of Alg. 1 (d = 0..u-1), a
+   * serial bridge that folds the 2^u-block aggregates onto the seed (GEMVs)
+   * and deposits the exclusive prefix of every 2^dl-block at its right end,
+   * then the last `down_levels` = dl down-sweep levels (d = dl-1..0).  Needs
+   * 0 <= u <= max(L-1, 0), dl in {u, u+1}, dl <= L (L = ceil(log2(T+1)));
+   * (0, 0) is the linear scan, (L-1, L) is Alg. 1.  DENSE only, like ALG1;
+   * same association as the oracle's `hybrid`.  Fewer levels trade GEMMs
+   * for a longer serial GEMV bridge (the paper's tuning knob).  Invalid
+   * (u, dl): BPPSA_ERR_INVALID_ARGUMENT.                                     */
+  BPPSA_SCAN_HYBRID = 3
 } bppsa_scan_mode;
 
 typedef struct bppsa_scan_opts {
@@ -133,6 +144,8 @@ typedef struct bppsa_scan_opts {
   void** events;
   int n_events;
   int* launches;
+  int up_levels;    /* HYBRID: u                                              */
+  int down_levels;  /* HYBRID: dl                                             */
 } bppsa_scan_opts;   /* NULL opts = all defaults */
 
 /* Workspace bytes needed by bppsa_scan / the shard calls for this

@@ -19,8 +19,8 @@ _lib = C.CDLL(_LIB_PATH)
 # ----------------------------------------------------------------- ABI types
 OK = 0
 JAC_DENSE, JAC_RNN_TANH, JAC_GRU = 0, 1, 2
-SCAN_BLOCKED, SCAN_ALG1, SCAN_LINEAR = 0, 1, 2
-MODES = {"blocked": SCAN_BLOCKED, "alg1": SCAN_ALG1, "linear": SCAN_LINEAR}
+SCAN_BLOCKED, SCAN_ALG1, SCAN_LINEAR, SCAN_HYBRID = 0, 1, 2, 3
+MODES = {"blocked": SCAN_BLOCKED, "alg1": SCAN_ALG1, "linear": SCAN_LINEAR, "hybrid": SCAN_HYBRID}
 
 _vp, _i, _sz = C.c_void_p, C.c_int, C.c_size_t
 
@@ -32,7 +32,7 @@ class _Jac(C.Structure):
 
 class _Opts(C.Structure):
     _fields_ = [("mode", _i), ("block0", _i), ("block", _i), ("leaf_impl", _i), ("events", C.POINTER(_vp)),
-                ("n_events", _i), ("launches", C.POINTER(_i))]
+                ("n_events", _i), ("launches", C.POINTER(_i)), ("up_levels", _i), ("down_levels", _i)]
 
 
 EXPORTS = {
@@ -150,9 +150,10 @@ def jacobians_dense(JT: torch.Tensor) -> Jacobians:
 LEAF_IMPL = {"auto": 0, "ffma": 1, "tensor": 2, "tensor_tf32": 3}
 
 
-def _opts(mode="blocked", block0=0, block=0, trace=None, leaf_impl="auto") -> _Opts:
+def _opts(mode="blocked", block0=0, block=0, trace=None, leaf_impl="auto", levels=(0, 0)) -> _Opts:
     o = _Opts(MODES[mode] if isinstance(mode, str) else int(mode), int(block0), int(block),
               LEAF_IMPL[leaf_impl] if isinstance(leaf_impl, str) else int(leaf_impl))
+    o.up_levels, o.down_levels = int(levels[0]), int(levels[1])
     if trace is not None:
         o.events, o.n_events, o.launches = trace._arr, len(trace.events), C.pointer(trace._count)
     return o
@@ -178,9 +179,9 @@ class LaunchTrace:
         return self.events[2 * k].elapsed_time(self.events[2 * k + 1])
 
 
-def scan_workspace_size(jac: Jacobians, mode="blocked", block0=0, block=0) -> int:
+def scan_workspace_size(jac: Jacobians, mode="blocked", block0=0, block=0, levels=(0, 0)) -> int:
     n = _sz()
-    o = _opts(mode, block0, block)
+    o = _opts(mode, block0, block, levels=levels)
     _check(_lib.bppsa_scan_workspace_size(C.byref(jac.desc), C.byref(o), C.byref(n)), "bppsa_scan_workspace_size")
     return n.value
 
@@ -192,8 +193,9 @@ def workspace(nbytes: int, device=None) -> torch.Tensor:
 def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
          grad_h_init: torch.Tensor | bool | None = None, ws: torch.Tensor | None = None,
          mode="blocked", block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None,
-         leaf_impl="auto"):
-    """bppsa_scan: all grad_h[t] = dl/dh_t at once (and dl/dh_init if asked)."""
+         leaf_impl="auto", levels=(0, 0)):
+    """bppsa_scan: all grad_h[t] = dl/dh_t at once (and dl/dh_init if asked).
+    `levels` = (up_levels, down_levels) for mode="hybrid" (P:472)."""
     T, B, H = jac.T, jac.B, jac.H
     dev = seed.device
     if grad_h is None:
@@ -202,9 +204,9 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
         grad_h_init = torch.empty((B, H), dtype=torch.float32, device=dev)
     elif grad_h_init is False:
         grad_h_init = None
-    o = _opts(mode, block0, block, trace, leaf_impl)
+    o = _opts(mode, block0, block, trace, leaf_impl, levels)
     if ws is None:
-        ws = workspace(scan_workspace_size(jac, mode, block0, block), dev)
+        ws = workspace(scan_workspace_size(jac, mode, block0, block, levels), dev)
     _check(_lib.bppsa_scan(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(grad_h, "grad_h"),
                            _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
                            _stream(stream)), "bppsa_scan")

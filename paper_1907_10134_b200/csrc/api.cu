@@ -161,11 +161,19 @@ bppsa_status get_opts(const bppsa_jac& j, const bppsa_scan_opts* o, int* mode, i
   *mode = o ? o->mode : BPPSA_SCAN_BLOCKED;
   *C0 = (o && o->block0 > 0) ? o->block0 : default_block0(j);
   *C = (o && o->block > 0) ? o->block : default_block(j);
-  if (*mode != BPPSA_SCAN_BLOCKED && *mode != BPPSA_SCAN_ALG1 && *mode != BPPSA_SCAN_LINEAR)
+  if (*mode != BPPSA_SCAN_BLOCKED && *mode != BPPSA_SCAN_ALG1 && *mode != BPPSA_SCAN_LINEAR &&
+      *mode != BPPSA_SCAN_HYBRID)
     return fail(BPPSA_ERR_INVALID_ARGUMENT, "unknown scan mode");
   if (*C0 < 2 || *C < 2) return fail(BPPSA_ERR_INVALID_ARGUMENT, "block lengths must be >= 2");
-  if (*mode == BPPSA_SCAN_ALG1 && j.kind != BPPSA_JAC_DENSE)
-    return fail(BPPSA_ERR_NOT_SUPPORTED, "ALG1 mode runs on materialised (DENSE) leaves");
+  if ((*mode == BPPSA_SCAN_ALG1 || *mode == BPPSA_SCAN_HYBRID) && j.kind != BPPSA_JAC_DENSE)
+    return fail(BPPSA_ERR_NOT_SUPPORTED, "ALG1 and HYBRID modes run on materialised (DENSE) leaves");
+  if (*mode == BPPSA_SCAN_HYBRID) {
+    const int L = (int)(64 - __builtin_clzll((unsigned long long)j.T));   // ceil(log2(n+1)), n = T
+    const int u = o->up_levels, dl = o->down_levels;
+    if (u < 0 || u > std::max(L - 1, 0) || (dl != u && dl != u + 1) || dl > L)
+      return fail(BPPSA_ERR_INVALID_ARGUMENT,
+                  "HYBRID needs 0 <= up_levels <= L-1, down_levels in {u, u+1}, down_levels <= L");
+  }
   return BPPSA_OK;
 }
 
@@ -181,12 +189,13 @@ bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts
   if (p->leaf_impl >= 2 && !tensor_fold_ok(j, p->leaf_impl))
     return fail(BPPSA_ERR_NOT_SUPPORTED,
                 "tensor-core leaf fold: tanh RNN with 16 <= H <= 64, H % 4 == 0 (3xTF32: H = 64)");
-  p->has_dense = (j.kind == BPPSA_JAC_DENSE) && mode != BPPSA_SCAN_ALG1;
+  const bool tree = (mode == BPPSA_SCAN_ALG1 || mode == BPPSA_SCAN_HYBRID);
+  p->has_dense = (j.kind == BPPSA_JAC_DENSE) && !tree;
   if (p->has_dense) {
     p->dense_off = off;
     off = align_up(off + (size_t)j.T * B * HH * sizeof(float));
   }
-  if (mode == BPPSA_SCAN_ALG1) {
+  if (tree) {
     p->L = 0;
     p->dense_off = off;
     off = align_up(off + (size_t)(j.T + 1) * B * HH * sizeof(float));
@@ -476,21 +485,30 @@ bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h, 
   char* w = static_cast<char*>(ws);
   const int mode = opts ? opts->mode : BPPSA_SCAN_BLOCKED;
   Tracer tr = tracer_from(opts);
-  if (mode == BPPSA_SCAN_ALG1) {
+  if (mode == BPPSA_SCAN_ALG1 || mode == BPPSA_SCAN_HYBRID) {
     float* X = reinterpret_cast<float*>(w + p.dense_off);
     const long long n = j.T;
     const int L = (int)(64 - __builtin_clzll((unsigned long long)n));   // ceil(log2(n+1))
+    const bool hyb = (mode == BPPSA_SCAN_HYBRID);
+    const int up = hyb ? opts->up_levels : L - 1;    // up-sweep levels d = 0..up-1
+    const int down = hyb ? opts->down_levels : L;    // down-sweep levels d = down-1..0
     tr.begin(st);
     cudaError_t e = launch_alg1_init(j.JT, seed, X, j.T, j.B, j.H, st);
     tr.end(st);
     if (e != cudaSuccess) return cuda_status(e, "alg1 init");
-    for (int d = 0; d <= L - 2; ++d) {
+    for (int d = 0; d < up; ++d) {
       tr.begin(st);
       e = launch_alg1_up(X, j.B, j.H, n, d, st);
       tr.end(st);
       if (e != cudaSuccess) return cuda_status(e, "alg1 up-sweep level");
     }
-    for (int d = L - 1; d >= 0; --d) {   // a[n] <- I is symbolic (pair i = 0 rule)
+    if (hyb) {   // Alg. 1 proper: a[n] <- I is symbolic (pair i = 0 rule)
+      tr.begin(st);
+      e = launch_hybrid_bridge(X, j.B, j.H, n, up, down, st);
+      tr.end(st);
+      if (e != cudaSuccess) return cuda_status(e, "hybrid bridge");
+    }
+    for (int d = down - 1; d >= 0; --d) {
       tr.begin(st);
       e = launch_alg1_down(X, j.B, j.H, n, d, st);
       tr.end(st);

@@ -107,6 +107,7 @@ cudaError_t launch_alg1_init(const float* JT, const float* seed, float* X, int T
                              int H, cudaStream_t st);
 cudaError_t launch_alg1_up(float* X, int B, int H, long long n, int d, cudaStream_t st);
 cudaError_t launch_alg1_down(float* X, int B, int H, long long n, int d, cudaStream_t st);
+cudaError_t launch_hybrid_bridge(float* X, int B, int H, long long n, int u, int dl, cudaStream_t st);
 cudaError_t launch_alg1_extract(const float* X, const float* JT, float* grad_h,
                                 float* grad_init, int T, int B, int H, cudaStream_t st);
 

@@ -464,6 +464,72 @@ __global__ void alg1_extract_kernel(const float* __restrict__ X, const float* __
   }
 }
 
+// Level-balanced hybrid bridge (reading 19): after `u` up-sweep levels
+// a[s + 2^u - 1] holds the aggregate of the 2^u-block starting at slot s.  One
+// warp per sample folds those aggregates left to right onto the seed (every
+// prefix that contains slot 0 is a vector, so each fold is one GEMV
+// P <- a[slot] P) and deposits the exclusive prefix of every 2^dl-block at the
+// block's right end.  The deposit of block 0 is the identity, left symbolic
+// (the down-sweep's pair i = 0 never reads it).  A deposit's slot is read by
+// the fold at most once, at the same or the next iteration, so it is written
+// only after that read.
+__global__ void hybrid_bridge_kernel(float* __restrict__ X, int B, int H, long long n, int u, int dl) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const long long HH = (long long)H * H;
+  const long long bs = 1ll << u, D = 1ll << dl;
+  const long long last = (n / D) * D;   // start of the last 2^dl-block
+  float P[2] = {0.f, 0.f}, pv[2] = {0.f, 0.f};
+  bool ident = true;
+  long long pend = -1;                  // slot of a deposit not yet written
+  auto store = [&](long long slot, const float* v) {
+    __syncwarp();
+    float* dst = X + (slot * B + b) * HH;
+    for (int m = 0; m < 2; ++m) {
+      const int i = lane + 32 * m;
+      if (i < H) dst[i] = v[m];
+    }
+  };
+  for (long long s = 0; s <= last; s += bs) {
+    if (s % D == 0 && s > 0) {
+      const long long pos = min(s + D - 1, n);
+      if (s + D <= last) {   // the fold reads slot pos at iteration s + D - bs: write after it
+        pend = pos;
+        pv[0] = P[0];
+        pv[1] = P[1];
+      } else {
+        store(pos, P);
+      }
+    }
+    if (s + bs > last) continue;
+    const long long slot = s + bs - 1;
+    const float* A = X + (slot * B + b) * HH;
+    if (ident) {   // block 0's aggregate contains slot 0: a vector
+      for (int m = 0; m < 2; ++m) {
+        const int i = lane + 32 * m;
+        P[m] = (i < H) ? A[i] : 0.f;
+      }
+      ident = false;
+    } else {       // P <- P <> a[slot] = a[slot] P
+      float res[2] = {0.f, 0.f};
+      for (int k = 0; k < H; ++k) {
+        const float pk = __shfl_sync(0xffffffffu, P[k >> 5], k & 31);
+        for (int m = 0; m < 2; ++m) {
+          const int i = lane + 32 * m;
+          if (i < H) res[m] = fmaf(A[(long long)k * H + i], pk, res[m]);
+        }
+      }
+      P[0] = res[0];
+      P[1] = res[1];
+    }
+    if (slot == pend) {
+      store(pend, pv);
+      pend = -1;
+    }
+  }
+}
+
 // carry = M_{r+1} ... M_{G-2} V_{G-1}; aggregates column-major [G][B][H*H]
 __global__ void carry_combine_kernel(const float* __restrict__ gathered, int rank, int world, int B, int H,
                                      float* __restrict__ carry_out) {
@@ -577,6 +643,11 @@ cudaError_t launch_alg1_down(float* X, int B, int H, long long n, int d, cudaStr
 cudaError_t launch_alg1_extract(const float* X, const float* JT, float* grad_h, float* grad_init, int T, int B,
                                 int H, cudaStream_t st) {
   alg1_extract_kernel<<<grid_for((long long)T * B * H), 256, 0, st>>>(X, JT, grad_h, grad_init, T, B, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hybrid_bridge(float* X, int B, int H, long long n, int u, int dl, cudaStream_t st) {
+  hybrid_bridge_kernel<<<(unsigned)((B + 3) / 4), 128, 0, st>>>(X, B, H, n, u, dl);
   return cudaGetLastError();
 }
 

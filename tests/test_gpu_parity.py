@@ -241,6 +241,53 @@ def test_alg1_matches_oracle_alg1_tightly(lib):
     assert rel(grad, tree) <= 1e-5
 
 
+def _hybrid_splits(T):
+    L = int(T).bit_length()
+    return [(u, dl) for u in range(0, max(L - 1, 0) + 1) for dl in (u, u + 1) if dl <= L]
+
+
+@pytest.mark.parametrize("T,H", [(1, 20), (2, 20), (7, 20), (100, 20), (129, 64)])
+def test_hybrid_integer_bit_exact_all_splits(lib, T, H):
+    """HYBRID mode (reading 19) for every valid (up_levels, down_levels):
+    bit-exact on the integer family, including (0, 0) = linear and (L-1, L) =
+    Alg. 1."""
+    f = W.int_dense_family(T, 3, H, seed=T + 2 * H)
+    ref, ref_init = bp.bp_dense(f["JT"], f["g"])
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    for lv in _hybrid_splits(T):
+        grad, gi = lib.scan(jac, cu(f["g"]), grad_h_init=True, mode="hybrid", levels=lv)
+        torch.cuda.synchronize()
+        assert np.array_equal(grad.cpu().numpy(), ref), lv
+        assert np.array_equal(gi.cpu().numpy(), ref_init), lv
+
+
+@pytest.mark.parametrize("T,H", [(300, 20), (257, 64)])
+def test_hybrid_matches_oracle_hybrid_tightly(lib, T, H):
+    """Same association as the oracle's `hybrid`, so fp32 vs fp64 stays tight;
+    and the plain-BP gate on every split."""
+    f = W.random_dense_family(T, 2, H, seed=5)
+    ref, _ = bp.bp_dense(f["JT"], f["g"])
+    a = S.scan_array(f["g"], f["JT"])
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    for lv in _hybrid_splits(T):
+        grad, _ = lib.scan(jac, cu(f["g"]), mode="hybrid", levels=lv)
+        tree = S.grads_from_scan(S.hybrid(a, *lv))
+        assert rel(grad, tree) <= 1e-5, lv
+        assert rel(grad, ref) <= TOL, lv
+
+
+def test_hybrid_errors(lib):
+    f = W.int_dense_family(100, 2, 20, seed=1)          # L = 7
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    g = cu(f["g"])
+    for lv in [(-1, 0), (7, 7), (2, 4), (3, 2), (6, 8)]:
+        with pytest.raises(lib.BppsaError, match="INVALID_ARGUMENT"):
+            lib.scan(jac, g, mode="hybrid", levels=lv)
+    jr = lib.jacobians_rnn(torch.zeros((4, 2, 20), device="cuda"), torch.zeros((20, 20), device="cuda"))
+    with pytest.raises(lib.BppsaError, match="NOT_SUPPORTED"):
+        lib.scan(jr, torch.zeros((2, 20), device="cuda"), mode="hybrid", levels=(1, 1))
+
+
 def test_materialized_rnn_leaves(lib):
     T, B, H = 40, 3, 20
     w = W.rnn_workload(T, B, H, seed=9)
