@@ -450,7 +450,60 @@ def sweep_small(api, args):
     out["c5"] = sweep_csr(api)
     out["train"] = sweep_train()
     out["hybrid"] = sweep_hybrid(api)
+    out["jacgen"] = sweep_jacgen(api)
     return out
+
+
+def sweep_jacgen(api, sample_cols: int = 256):
+    """SURVEY 8(f) NEXT-3 / Table 1's last column: the
+    analytical device builders (pattern + data of J^T, one sample) vs
+    generating J^T through torch autograd one column at a time on the same
+    GPU.  The autograd side is timed on `sample_cols` columns and scaled to
+    all columns (one backward per output element; stated in the output)."""
+    import torch
+    torch.manual_seed(0)
+    res = {}
+    x = torch.randn(1, 3, 32, 32, device="cuda")
+    conv = torch.nn.Conv2d(3, 64, 3, padding=1, bias=False).cuda()
+    wflat = conv.weight.detach().reshape(-1).contiguous()
+    a = torch.randn(1, 64, 32, 32, device="cuda")
+    ws = api.workspace(api.csr_conv3x3_build_size(3, 64, 32, 32)[1])
+
+    def conv_build():
+        api.csr_conv3x3_build(3, 64, 32, 32, wflat, with_data=True, ws=ws)
+
+    def relu_build():
+        api.csr_identity_build(64 * 32 * 32)
+        api.csr_relu_data(a.reshape(1, -1))
+
+    _, pidx = torch.nn.functional.max_pool2d(a, 2, return_indices=True)
+
+    def pool_build():
+        api.csr_maxpool_build(64, 32, 32)
+        api.csr_maxpool_data(pidx, 64, 32, 32)
+
+    def autograd_ms(f, inp):
+        inp = inp.clone().requires_grad_(True)
+        y = f(inp).reshape(-1)
+        cols = y.numel()
+        idx = torch.randperm(cols, device="cuda")[:sample_cols].tolist()
+
+        def run():
+            for j in idx:
+                torch.autograd.grad(y[j], inp, retain_graph=True)
+
+        return _time(run, reps=2, warm=1) / len(idx) * cols, cols
+
+    cases = {"conv1 (3->64, 32x32)": (conv_build, lambda t: conv(t), x),
+             "relu1 (64x32x32)": (relu_build, torch.relu, a),
+             "pool1 (64x32x32, 2x2)": (pool_build, lambda t: torch.nn.functional.max_pool2d(t, 2), a)}
+    for name, (build, f, inp) in cases.items():
+        an = _time(build, reps=20)
+        ag, cols = autograd_ms(f, inp)
+        res[name] = {"analytical_ms": round(an, 4), "autograd_column_ms_extrapolated": round(ag, 1),
+                     "columns": cols, "speedup": round(ag / an, 1)}
+    return {"sample_cols": sample_cols, "device": "same B200 for both", "ops": res,
+            "paper_speedups_cpu_context": {"conv": 8.3e3, "relu": 1.2e6, "pool": 1.5e5}}
 
 
 def sweep_hybrid(api):
@@ -548,9 +601,19 @@ def sweep_csr(api):
         grads = [torch.empty((16, d), device="cuda") for d in plan.dims]
         ms = _time(lambda: api.csr_scan(plan, chain.data, chain.batched, seed, grads=grads, ws=ws), reps=10)
         info = plan.info()
-        res[f"u{sched[0]}_dl{sched[1]}"] = {"scan_ms": round(ms, 4), "plan_build_s": round(t_plan, 2),
-                                            "contributions": info["contributions"], "spmv_nnz": info["spmv_nnz"],
-                                            "kernels": info["kernels"], "ws_GB": round(ws.numel() / 1e9, 3)}
+        steps = api.csr_plan_steps(plan)       # fig:prune_symbolic static FLOP analysis
+        scan_st = [x for x in steps if x["phase"] != "bp"]
+        bp_st = [x for x in steps if x["phase"] == "bp"]
+        res[f"u{sched[0]}_dl{sched[1]}"] = {
+            "scan_ms": round(ms, 4), "plan_build_s": round(t_plan, 2),
+            "contributions": info["contributions"], "spmv_nnz": info["spmv_nnz"],
+            "kernels": info["kernels"], "ws_GB": round(ws.numel() / 1e9, 3),
+            "flops_per_sample": {"bppsa_total": sum(x["flops"] for x in scan_st),
+                                 "bppsa_critical_path": sum(x["flops"] for x in scan_st if x["critical"]),
+                                 "bppsa_max_step": max(x["flops"] for x in scan_st),
+                                 "bp_total": sum(x["flops"] for x in bp_st),
+                                 "bp_max_step": max(x["flops"] for x in bp_st),
+                                 "dense_equivalent_total": sum(x["dense_flops"] for x in scan_st)}}
         del ws, plan
         torch.cuda.empty_cache()
     res["note"] = ("paper schedule (u, dl) = (3, 4) (P:472) needs 9.1e10 contribution pairs on this pruned "

@@ -259,6 +259,26 @@ bppsa_status bppsa_csr_plan_workspace_size(const bppsa_csr_plan* plan, int B,
 bppsa_status bppsa_csr_plan_info(const bppsa_csr_plan* plan,
                                  long long* contributions, long long* spmv_nnz,
                                  int* n_kernels);
+/* Per-step static FLOP analysis of the schedule (fig:prune_symbolic, P:467,
+ * P:474).  One record per numeric op in schedule order — up-sweep SpGEMMs
+ * and SpMVs (phase UP, level d), bridge SpMVs (BRIDGE, level = fold index),
+ * down-sweep SpMVs (DOWN, level d), the inclusive extra J_1^T dl/dx_1
+ * (EXTRA) — then the BP baseline's n gradient operators (BP, level k = the
+ * operator J_k^T, k = n..1).  flops: per sample, 2 x contribution pairs (mm)
+ * or 2 x nnz (mv); dense_flops: the same op on dense operands (2 m k n / 2 m n,
+ * the figure's x-axis).  critical: the costliest op of each up-/down-sweep
+ * level, every bridge / extra / BP op (DESIGN reading 23).  Writes
+ * min(capacity, count) records; *n_steps = count.                          */
+enum { BPPSA_CSR_STEP_MM = 0, BPPSA_CSR_STEP_MV = 1 };
+enum { BPPSA_CSR_STEP_UP = 0, BPPSA_CSR_STEP_BRIDGE = 1, BPPSA_CSR_STEP_DOWN = 2,
+       BPPSA_CSR_STEP_EXTRA = 3, BPPSA_CSR_STEP_BP = 4 };
+typedef struct bppsa_csr_step {
+  int kind, phase, level, critical;
+  long long flops, dense_flops;
+} bppsa_csr_step;
+bppsa_status bppsa_csr_plan_steps(const bppsa_csr_plan* plan,
+                                  bppsa_csr_step* steps, int capacity,
+                                  int* n_steps);
 /* data[k]: device values of J_{k+1}^T (layout above; batched[k] != 0 for
  * per-sample data).  seed: dl/dx_n [B][cols(J_n^T)].  grads[k], k = 0..n
  * (n+1 pointers, NULL = not wanted): dl/dx_k [B][dim x_k]; grads[n] = seed;
@@ -295,6 +315,35 @@ bppsa_status bppsa_csr_maxpool_pattern(int c, int h, int w, long long* indptr,
 bppsa_status bppsa_csr_maxpool_data(int c, int h, int w, int B,
                                     const long long* pool_idx, float* data,
                                     void* stream);
+
+/* Device analytical builders (Algs. 2-4 and 8-9 on the GPU; SURVEY 8(f)
+ * NEXT-3; "generate the transposed Jacobian directly into the CSR
+ * format").  Same patterns, entry order and taps as the host builders above;
+ * every output array is a caller-owned DEVICE buffer; asynchronous on
+ * `stream`.
+ * bppsa_csr_conv3x3_build_size: *max_nnz = the structural nnz
+ * ci co (3h-2)(3w-2) (h, w >= 2; reading 17) = the capacity `indices`,
+ * `tap`, `data` need (the exact count when drop_zero = 0); *ws_bytes = the
+ * workspace of bppsa_csr_conv3x3_build (0 unless drop_zero).
+ * bppsa_csr_conv3x3_build: indptr [ci h w + 1] (Alg. 2 in closed form, or a
+ * row count + device scan when drop_zero drops pruned taps; the nnz is
+ * indptr[ci h w]), indices (Alg. 3), tap (nullable), data (nullable:
+ * data[p] = weights[tap[p]], Alg. 4).  weights: device [co][ci][3][3],
+ * required when drop_zero or data.                                          */
+bppsa_status bppsa_csr_conv3x3_build_size(int ci, int co, int h, int w,
+                                          int drop_zero, long long* max_nnz,
+                                          size_t* ws_bytes);
+bppsa_status bppsa_csr_conv3x3_build(int ci, int co, int h, int w,
+                                     const float* weights, int drop_zero,
+                                     long long* indptr, int* indices, int* tap,
+                                     float* data, void* ws, size_t ws_bytes,
+                                     void* stream);
+/* max-pool window pattern (as bppsa_csr_maxpool_pattern) and the ReLU
+ * identity pattern of size d, on the device.                                */
+bppsa_status bppsa_csr_maxpool_build(int c, int h, int w, long long* indptr,
+                                     int* indices, void* stream);
+bppsa_status bppsa_csr_identity_build(long long d, long long* indptr,
+                                      int* indices, void* stream);
 
 #ifdef __cplusplus
 }

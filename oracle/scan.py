@@ -236,3 +236,77 @@ def shard_local_grads(JT_time, lo, hi, carry):
         out[t - lo] = v
         v = np.einsum("bik,bk->bi", np.asarray(JT_time[t], D), v)
     return out, v
+
+
+def hybrid_steps(patterns, up_levels: int, down_levels: int):
+    """Static FLOP analysis of the hybrid schedule (fig:prune_symbolic, P:467,
+    P:474) over a CSR chain given by its patterns only.
+
+    `patterns[k]` = csr.CSR pattern of J_{k+1}^T in time order (data unused).
+    The scan array is [seed, J_n^T, ..., J_1^T] (reading 3); the schedule is
+    `hybrid` above step by step, each <> application recorded as one op:
+      mm  a[r] <- a[l] <> a[r] = a[r] a[l] with both matrices:
+          flops = 2 x the contribution pairs of the structural product
+          (csr.plan_product), dense_flops = 2 m k n;
+      mv  any product with a vector: flops = 2 nnz(matrix), dense = 2 m n.
+    Identities are symbolic (no op).  Then the inclusive extra
+    J_1^T dl/dx_1 (phase 'extra') and the BP baseline's n gradient operators
+    J_n^T .. J_1^T (phase 'bp', level k).  critical (reading 23): the costliest
+    op of each up/down level (first on ties); every bridge/extra/bp op."""
+    n = len(patterns)
+    u, dl = up_levels, down_levels
+    L = num_levels(n)
+    if not (0 <= u <= max(L - 1, 0) and dl in (u, u + 1) and dl <= L):
+        raise ValueError("need 0 <= up_levels <= L-1, down_levels in {u, u+1}, down_levels <= L")
+    VEC, ID = "v", "I"
+    a = [VEC] + [patterns[n - s] for s in range(1, n + 1)]      # slot s >= 1: J_{n-s+1}^T
+    steps = []
+
+    def op(phase, level, left, right):
+        """left <> right = right . left; returns the result (VEC or a pattern)."""
+        if left is ID:
+            return right
+        if right is ID:
+            return left
+        if left is VEC:
+            steps.append(dict(kind="mv", phase=phase, level=level, flops=2 * right.nnz,
+                              dense_flops=2 * right.rows * right.cols))
+            return VEC
+        pl = csr.plan_product(right, left)
+        steps.append(dict(kind="mm", phase=phase, level=level, flops=2 * len(pl.left_pos),
+                          dense_flops=2 * right.rows * right.cols * left.cols))
+        return pl.out
+
+    for d in range(0, u):
+        for i in range(0, n - 2 ** d + 1, 2 ** (d + 1)):
+            l, r = i + 2 ** d - 1, min(i + 2 ** (d + 1) - 1, n)
+            a[r] = op("up", d, a[l], a[r])
+    bs, D = 2 ** u, 2 ** dl
+    last = (n // D) * D
+    P, deposits = ID, []
+    for s in range(0, last + 1, bs):
+        if s % D == 0:
+            deposits.append((min(s + D - 1, n), P))
+        if s + bs <= last:
+            P = op("bridge", s // bs, P, a[min(s + bs - 1, n)])
+    for pos, val in deposits:
+        a[pos] = val
+    for d in range(dl - 1, -1, -1):
+        for i in range(0, n - 2 ** d + 1, 2 ** (d + 1)):
+            l, r = i + 2 ** d - 1, min(i + 2 ** (d + 1) - 1, n)
+            T = a[l]
+            a[l] = a[r]
+            a[r] = op("down", d, a[r], T)
+    assert all(x is VEC for x in a[1:]), "every output slot must be a vector"
+    op("extra", 0, VEC, patterns[0])
+    for st in steps:
+        st["critical"] = st["phase"] in ("bridge", "extra")
+    for ph in ("up", "down"):
+        for lv in {st["level"] for st in steps if st["phase"] == ph}:
+            grp = [st for st in steps if st["phase"] == ph and st["level"] == lv]
+            max(grp, key=lambda st: st["flops"])["critical"] = True     # max() keeps the first on ties
+    for k in range(n, 0, -1):
+        m = patterns[k - 1]
+        steps.append(dict(kind="mv", phase="bp", level=k, flops=2 * m.nnz, dense_flops=2 * m.rows * m.cols,
+                          critical=True))
+    return steps

@@ -67,7 +67,21 @@ EXPORTS.update({
     "bppsa_csr_relu_data": (_i, [_ll, _i, _vp, _vp, _vp]),
     "bppsa_csr_maxpool_pattern": (_i, [_i, _i, _i, _vp, _vp]),
     "bppsa_csr_maxpool_data": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
+    "bppsa_csr_plan_steps": (_i, [_vp, _vp, _i, C.POINTER(_i)]),
+    "bppsa_csr_conv3x3_build_size": (_i, [_i, _i, _i, _i, _i, C.POINTER(_ll), C.POINTER(_sz)]),
+    "bppsa_csr_conv3x3_build": (_i, [_i, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "bppsa_csr_maxpool_build": (_i, [_i, _i, _i, _vp, _vp, _vp]),
+    "bppsa_csr_identity_build": (_i, [_ll, _vp, _vp, _vp]),
 })
+
+
+class _CsrStep(C.Structure):
+    _fields_ = [("kind", _i), ("phase", _i), ("level", _i), ("critical", _i), ("flops", _ll),
+                ("dense_flops", _ll)]
+
+
+STEP_KIND = ("mm", "mv")
+STEP_PHASE = ("up", "bridge", "down", "extra", "bp")
 for _name, (_res, _args) in EXPORTS.items():
     _f = getattr(_lib, _name)
     _f.restype, _f.argtypes = _res, _args
@@ -298,6 +312,63 @@ class CsrPlan:
         n = _sz()
         _check(_lib.bppsa_csr_plan_workspace_size(self.h, B, arr, C.byref(n)), "bppsa_csr_plan_workspace_size")
         return n.value
+
+
+def csr_plan_steps(plan: "CsrPlan"):
+    """bppsa_csr_plan_steps: the per-step static FLOP analysis (fig:prune_symbolic)
+    as a list of dicts (kind, phase, level, critical, flops, dense_flops)."""
+    n = _i()
+    _check(_lib.bppsa_csr_plan_steps(plan.h, None, 0, C.byref(n)), "bppsa_csr_plan_steps")
+    arr = (_CsrStep * max(n.value, 1))()
+    _check(_lib.bppsa_csr_plan_steps(plan.h, arr, n.value, C.byref(n)), "bppsa_csr_plan_steps")
+    return [dict(kind=STEP_KIND[a.kind], phase=STEP_PHASE[a.phase], level=a.level, critical=bool(a.critical),
+                 flops=a.flops, dense_flops=a.dense_flops) for a in arr[:n.value]]
+
+
+def csr_conv3x3_build_size(ci, co, h, w, drop_zero=False):
+    """-> (max_nnz, workspace bytes) of bppsa_csr_conv3x3_build (host call)."""
+    nnz, ws = C.c_longlong(), _sz()
+    _check(_lib.bppsa_csr_conv3x3_build_size(ci, co, h, w, int(drop_zero), C.byref(nnz), C.byref(ws)),
+           "bppsa_csr_conv3x3_build_size")
+    return nnz.value, ws.value
+
+
+def csr_conv3x3_build(ci, co, h, w, weights: torch.Tensor | None = None, drop_zero=False, with_data=False,
+                      ws=None, stream=None):
+    """Device analytical conv J^T builder -> (indptr [ci h w + 1] int64, indices int32,
+    tap int32, data fp32 or None), trimmed to the nnz (one host read of indptr[-1]
+    when drop_zero)."""
+    dev = weights.device if weights is not None else torch.device("cuda")
+    cap, wsb = csr_conv3x3_build_size(ci, co, h, w, drop_zero)
+    ip = torch.empty(ci * h * w + 1, dtype=torch.int64, device=dev)
+    ix = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    tap = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    data = torch.empty(max(cap, 1), dtype=torch.float32, device=dev) if with_data else None
+    if ws is None:
+        ws = workspace(wsb, dev)
+    _check(_lib.bppsa_csr_conv3x3_build(ci, co, h, w, _ptr(weights, "weights"), int(drop_zero), ip.data_ptr(),
+                                        ix.data_ptr(), tap.data_ptr(), _ptr(data, "data"), ws.data_ptr(),
+                                        ws.numel(), _stream(stream)), "bppsa_csr_conv3x3_build")
+    nnz = int(ip[-1]) if drop_zero else cap
+    return ip, ix[:nnz], tap[:nnz], None if data is None else data[:nnz]
+
+
+def csr_maxpool_build(c, h, w, device=None, stream=None):
+    dev = device or torch.device("cuda")
+    ip = torch.empty(c * h * w + 1, dtype=torch.int64, device=dev)
+    ix = torch.empty(c * h * w, dtype=torch.int32, device=dev)
+    _check(_lib.bppsa_csr_maxpool_build(c, h, w, ip.data_ptr(), ix.data_ptr(), _stream(stream)),
+           "bppsa_csr_maxpool_build")
+    return ip, ix
+
+
+def csr_identity_build(d, device=None, stream=None):
+    dev = device or torch.device("cuda")
+    ip = torch.empty(d + 1, dtype=torch.int64, device=dev)
+    ix = torch.empty(d, dtype=torch.int32, device=dev)
+    _check(_lib.bppsa_csr_identity_build(d, ip.data_ptr(), ix.data_ptr(), _stream(stream)),
+           "bppsa_csr_identity_build")
+    return ip, ix
 
 
 def csr_plan_create(patterns, up_levels: int, down_levels: int, max_contributions: int = 0) -> CsrPlan:

@@ -15,6 +15,8 @@
 #include <thread>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 
 namespace bppsa {
@@ -67,6 +69,7 @@ struct bppsa_csr_plan {
   std::vector<int> out_buf;   // out_buf[k] = buffer holding dl/dx_k (k = 0..n)
   int seed_buf = -1;
   long long contributions = 0, spmv_nnz = 0;
+  std::vector<bppsa_csr_step> steps;   // one per op (schedule order), then the BP baseline
   ~bppsa_csr_plan() {
     for (auto& p : plans) {
       cudaFree(p.cptr);
@@ -266,6 +269,103 @@ __global__ void maxpool_data_kernel(const long long* __restrict__ pidx, float* _
   data[t] = (sel == rem) ? 1.f : 0.f;
 }
 
+// ---- device analytical builders (Algs. 2-4 on the GPU) ----
+// Conv 3x3 / pad 1 / stride 1 transposed Jacobian, rows = input pixels
+// (c, y, x), entries in ascending output index (o, y+oy, x+ox) — candidate
+// q = o*9 + (oy+1)*3 + (ox+1) enumerates them in that order — weight tap
+// W[o][c][1-oy][1-ox] (the exact pattern, reading 17: no wrap-around).
+__device__ __forceinline__ int conv_ny(int y, int h) { return min(y + 1, h - 1) - max(y - 1, 0) + 1; }
+
+// Alg. 2 (reading 15) in closed form: rows before (c, y, x) hold
+// c*co*NY*NX + co*SY(y)*NX + co*ny(y)*SX(x) entries, SY(y) = sum_{y'<y} ny(y').
+__global__ void conv_indptr_kernel(int ci, int co, int h, int w, long long* __restrict__ indptr) {
+  const long long rows = (long long)ci * h * w;
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r > rows) return;
+  const long long NY = (h == 1) ? 1 : 3ll * h - 2, NX = (w == 1) ? 1 : 3ll * w - 2;
+  if (r == rows) {
+    indptr[r] = (long long)ci * co * NY * NX;
+    return;
+  }
+  const int c = (int)(r / ((long long)h * w)), rem = (int)(r % ((long long)h * w)), y = rem / w, x = rem % w;
+  long long SY = 0, SX = 0;
+  for (int t = 0; t < y; ++t) SY += conv_ny(t, h);
+  for (int t = 0; t < x; ++t) SX += conv_ny(t, w);
+  indptr[r] = (long long)c * co * NY * NX + (long long)co * SY * NX + (long long)co * conv_ny(y, h) * SX;
+}
+
+// pruned taps leave the pattern: entries per row by ballot over the candidates
+__global__ void conv_count_kernel(int ci, int co, int h, int w, const float* __restrict__ wts,
+                                  long long* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long rows = (long long)ci * h * w;
+  if (r >= rows) return;
+  const int c = (int)(r / ((long long)h * w)), rem = (int)(r % ((long long)h * w)), y = rem / w, x = rem % w;
+  long long n = 0;
+  for (int q0 = 0; q0 < co * 9; q0 += 32) {
+    const int q = q0 + lane;
+    bool v = false;
+    if (q < co * 9) {
+      const int o = q / 9, oy = (q % 9) / 3 - 1, ox = q % 3 - 1;
+      const int yo = y + oy, xo = x + ox;
+      v = yo >= 0 && yo < h && xo >= 0 && xo < w && wts[((o * ci + c) * 3 + (1 - oy)) * 3 + (1 - ox)] != 0.f;
+    }
+    n += __popc(__ballot_sync(0xffffffffu, v));
+  }
+  if (lane == 0) cnt[r] = n;
+}
+
+// Alg. 3 (indices) + Alg. 4 (data) with the row offsets from indptr
+__global__ void conv_fill_kernel(int ci, int co, int h, int w, const float* __restrict__ wts, int drop,
+                                 const long long* __restrict__ indptr, int* __restrict__ indices,
+                                 int* __restrict__ tap, float* __restrict__ data) {
+  const int lane = threadIdx.x & 31;
+  const long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long rows = (long long)ci * h * w;
+  if (r >= rows) return;
+  const int c = (int)(r / ((long long)h * w)), rem = (int)(r % ((long long)h * w)), y = rem / w, x = rem % w;
+  long long p = indptr[r];
+  for (int q0 = 0; q0 < co * 9; q0 += 32) {
+    const int q = q0 + lane;
+    bool v = false;
+    int t = 0, col = 0;
+    if (q < co * 9) {
+      const int o = q / 9, oy = (q % 9) / 3 - 1, ox = q % 3 - 1;
+      const int yo = y + oy, xo = x + ox;
+      t = ((o * ci + c) * 3 + (1 - oy)) * 3 + (1 - ox);
+      col = (o * h + yo) * w + xo;
+      v = yo >= 0 && yo < h && xo >= 0 && xo < w && (!drop || wts[t] != 0.f);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, v);
+    if (v) {
+      const long long e = p + __popc(m & ((1u << lane) - 1u));
+      indices[e] = col;
+      if (tap) tap[e] = t;
+      if (data) data[e] = wts[t];
+    }
+    p += __popc(m);
+  }
+}
+
+// 2x2 / stride-2 max-pool window pattern (reading 18) and the identity (ReLU)
+__global__ void pool_pattern_kernel(int c, int h, int w, long long* __restrict__ indptr, int* __restrict__ indices) {
+  const long long d = (long long)c * h * w;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > d) return;
+  indptr[i] = i;
+  if (i == d) return;
+  const int cc = (int)(i / ((long long)h * w)), rem = (int)(i % ((long long)h * w)), y = rem / w, x = rem % w;
+  indices[i] = (cc * (h / 2) + y / 2) * (w / 2) + x / 2;
+}
+
+__global__ void identity_pattern_kernel(long long d, long long* __restrict__ indptr, int* __restrict__ indices) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > d) return;
+  indptr[i] = i;
+  if (i < d) indices[i] = (int)i;
+}
+
 unsigned blocks_for(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -365,15 +465,18 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
     P->bufs.push_back(b);
     return (int)P->bufs.size() - 1;
   };
+  int phase = BPPSA_CSR_STEP_UP, level = 0;   // where the next op sits (static analysis)
   auto spmv = [&](int mat, int vec) {   // returns new vector buffer = mat * vec
     const HCSR& m = P->pats[P->bufs[mat].pat];
     const int out = new_vec(m.rows);
     P->ops.push_back(Op{OP_SPMV, out, mat, vec, -1});
     P->spmv_nnz += m.nnz();
+    P->steps.push_back(bppsa_csr_step{BPPSA_CSR_STEP_MV, phase, level, 0, 2 * m.nnz(), 2ll * m.rows * m.cols});
     return out;
   };
   // up-sweep levels d < u (Alg. 1 lines 1-5): a[r] <- a[r] a[l]
   for (int d = 0; d < u; ++d) {
+    level = d;
     for (long long i = 0; i <= (long long)n - (1ll << d); i += (1ll << (d + 1))) {
       const int l = (int)(i + (1ll << d) - 1), r = (int)std::min<long long>(i + (1ll << (d + 1)) - 1, n);
       if (is_vec(slot[l])) {
@@ -394,6 +497,12 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
         P->plans.push_back(dp);
         if (e != cudaSuccess) return cuda_status(e, "plan upload");
         P->contributions += dp.contrib;
+        {
+          const HCSR& A = P->pats[bl.pat];
+          const HCSR& Bm = P->pats[br.pat];
+          P->steps.push_back(bppsa_csr_step{BPPSA_CSR_STEP_MM, phase, level, 0, 2 * dp.contrib,
+                                            2ll * A.rows * A.cols * Bm.cols});
+        }
         P->pats.push_back(std::move(hp.out));
         Buf pb;
         pb.kind = B_PROD;
@@ -414,9 +523,11 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
     const long long last = (n / bd) * bd;
     int Pv = IDENT;
     std::vector<std::pair<int, int>> deposits;
+    phase = BPPSA_CSR_STEP_BRIDGE;
     for (long long s = 0; s <= last; s += bs) {
       if (s % bd == 0) deposits.push_back({(int)std::min<long long>(s + bd - 1, n), Pv});
       if (s + bs <= last) {
+        level = (int)(s / bs);
         const int agg = slot[(int)std::min<long long>(s + bs - 1, n)];
         Pv = (Pv == IDENT) ? agg : spmv(agg, Pv);
       }
@@ -424,7 +535,9 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
     for (auto& dp : deposits) slot[dp.first] = dp.second;
   }
   // down-sweep levels d < dl with the operand reversal (Alg. 1 line 13)
+  phase = BPPSA_CSR_STEP_DOWN;
   for (int d = dl - 1; d >= 0; --d) {
+    level = d;
     for (long long i = 0; i <= (long long)n - (1ll << d); i += (1ll << (d + 1))) {
       const int l = (int)(i + (1ll << d) - 1), r = (int)std::min<long long>(i + (1ll << (d + 1)) - 1, n);
       const int T = slot[l];
@@ -438,7 +551,31 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
     if (!is_vec(slot[s])) return fail(BPPSA_ERR_PLAN, "internal: slot " + std::to_string(s) + " is not a vector");
     P->out_buf[n - s + 1] = slot[s];
   }
+  phase = BPPSA_CSR_STEP_EXTRA;
+  level = 0;
   P->out_buf[0] = spmv(0, P->out_buf[1]);   // inclusive extra J_1^T dl/dx_1
+  // critical path of the level-synchronous schedule (DESIGN reading 23): the
+  // costliest op of every up-/down-sweep level; every bridge op and the extra
+  // (serial)
+  for (size_t a = 0; a < P->steps.size(); ++a) {
+    bppsa_csr_step& st = P->steps[a];
+    if (st.phase == BPPSA_CSR_STEP_BRIDGE || st.phase == BPPSA_CSR_STEP_EXTRA) {
+      st.critical = 1;
+      continue;
+    }
+    bool top = true;
+    for (size_t b = 0; b < P->steps.size() && top; ++b) {
+      const bppsa_csr_step& o = P->steps[b];
+      if (b == a || o.phase != st.phase || o.level != st.level) continue;
+      if (o.flops > st.flops || (o.flops == st.flops && b < a)) top = false;
+    }
+    st.critical = top ? 1 : 0;
+  }
+  // the BP baseline: one gradient operator J_k^T per element, serial
+  for (int k = n; k >= 1; --k) {
+    const HCSR& m = P->pats[k - 1];
+    P->steps.push_back(bppsa_csr_step{BPPSA_CSR_STEP_MV, BPPSA_CSR_STEP_BP, k, 1, 2 * m.nnz(), 2ll * m.rows * m.cols});
+  }
   // device copies of every pattern used by an SpMV
   P->dpats.resize(P->pats.size());
   for (const Op& op : P->ops) {
@@ -468,6 +605,15 @@ bppsa_status bppsa_csr_plan_info(const bppsa_csr_plan* plan, long long* contribu
   if (contributions) *contributions = plan->contributions;
   if (spmv_nnz) *spmv_nnz = plan->spmv_nnz;
   if (n_kernels) *n_kernels = (int)plan->ops.size() + 1 + (plan->n + 1);
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_csr_plan_steps(const bppsa_csr_plan* plan, bppsa_csr_step* steps, int capacity, int* n_steps) {
+  if (!plan || !n_steps || capacity < 0 || (capacity > 0 && !steps))
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad arguments");
+  *n_steps = (int)plan->steps.size();
+  const int c = std::min(capacity, *n_steps);
+  for (int a = 0; a < c; ++a) steps[a] = plan->steps[a];
   return BPPSA_OK;
 }
 
@@ -562,6 +708,71 @@ bppsa_status bppsa_csr_relu_data(long long d, int B, const float* x, float* data
   relu_data_kernel<<<blocks_for(d * B), 256, 0, (cudaStream_t)stream>>>(x, data, d, B);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "relu data");
+}
+
+bppsa_status bppsa_csr_conv3x3_build_size(int ci, int co, int h, int w, int drop_zero, long long* max_nnz,
+                                          size_t* ws_bytes) {
+  if (ci < 1 || co < 1 || h < 1 || w < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad conv spec");
+  const long long NY = (h == 1) ? 1 : 3ll * h - 2, NX = (w == 1) ? 1 : 3ll * w - 2;
+  const long long rows = (long long)ci * h * w;
+  if (max_nnz) *max_nnz = (long long)ci * co * NY * NX;
+  if (ws_bytes) {
+    size_t tmp = 0;
+    if (drop_zero) {
+      cudaError_t e = cub::DeviceScan::InclusiveSum(nullptr, tmp, (const long long*)nullptr, (long long*)nullptr,
+                                                    (int)rows);
+      if (e != cudaSuccess) return cuda_status(e, "cub scan size");
+      tmp = align256(tmp) + align256((size_t)rows * sizeof(long long));
+    }
+    *ws_bytes = tmp;
+  }
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_csr_conv3x3_build(int ci, int co, int h, int w, const float* weights, int drop_zero,
+                                     long long* indptr, int* indices, int* tap, float* data, void* ws,
+                                     size_t ws_bytes, void* stream) {
+  if (ci < 1 || co < 1 || h < 1 || w < 1 || !indptr || !indices) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad conv spec");
+  if ((drop_zero || data) && !weights) return fail(BPPSA_ERR_INVALID_ARGUMENT, "drop_zero / data need weights");
+  if ((long long)co * h * w > (1ll << 31) - 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "column index exceeds int32");
+  size_t need = 0;
+  bppsa_status s = bppsa_csr_conv3x3_build_size(ci, co, h, w, drop_zero, nullptr, &need);
+  if (s != BPPSA_OK) return s;
+  if (ws_bytes < need || (need && !ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long rows = (long long)ci * h * w;
+  cudaError_t e;
+  if (!drop_zero) {
+    conv_indptr_kernel<<<blocks_for(rows + 1), 256, 0, st>>>(ci, co, h, w, indptr);
+  } else {
+    long long* cnt = reinterpret_cast<long long*>(static_cast<char*>(ws));
+    void* tmp = static_cast<char*>(ws) + align256((size_t)rows * sizeof(long long));
+    size_t tmp_bytes = need - align256((size_t)rows * sizeof(long long));
+    conv_count_kernel<<<blocks_for(rows * 32), 256, 0, st>>>(ci, co, h, w, weights, cnt);
+    e = cudaMemsetAsync(indptr, 0, sizeof(long long), st);
+    if (e != cudaSuccess) return cuda_status(e, "indptr[0]");
+    e = cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, cnt, indptr + 1, (int)rows, st);
+    if (e != cudaSuccess) return cuda_status(e, "row-count scan");
+  }
+  conv_fill_kernel<<<blocks_for(rows * 32), 256, 0, st>>>(ci, co, h, w, weights, drop_zero, indptr, indices, tap, data);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "conv build");
+}
+
+bppsa_status bppsa_csr_maxpool_build(int c, int h, int w, long long* indptr, int* indices, void* stream) {
+  if (c < 1 || h < 2 || w < 2 || (h & 1) || (w & 1) || !indptr || !indices)
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad max-pool spec (even h, w >= 2)");
+  const long long d = (long long)c * h * w;
+  pool_pattern_kernel<<<blocks_for(d + 1), 256, 0, (cudaStream_t)stream>>>(c, h, w, indptr, indices);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "maxpool build");
+}
+
+bppsa_status bppsa_csr_identity_build(long long d, long long* indptr, int* indices, void* stream) {
+  if (d < 1 || d > (1ll << 31) - 1 || !indptr || !indices) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad size");
+  identity_pattern_kernel<<<blocks_for(d + 1), 256, 0, (cudaStream_t)stream>>>(d, indptr, indices);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "identity build");
 }
 
 bppsa_status bppsa_csr_maxpool_pattern(int c, int h, int w, long long* indptr, int* indices) {

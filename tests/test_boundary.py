@@ -80,3 +80,13 @@ def test_product_never_imports_oracle():
     for f in glob.glob(os.path.join(ROOT, "paper_1907_10134_b200", "**", "*.py"), recursive=True):
         src = open(f).read()
         assert "oracle" not in re.sub(r"#.*|\"\"\".*?\"\"\"", "", src, flags=re.S), f
+
+
+def test_conv_build_size_host_call(built):
+    """bppsa_csr_conv3x3_build_size (host): the structural nnz in closed form
+    matches the oracle's exact stencil and Table 1's conv1 (1,696,512)."""
+    from paper_1907_10134_b200 import api
+    from oracle import csr as C
+    assert api.csr_conv3x3_build_size(3, 64, 32, 32)[0] == 1_696_512
+    for ci, co, h, w in [(1, 1, 1, 1), (2, 3, 1, 5), (3, 2, 2, 2), (4, 5, 7, 3)]:
+        assert api.csr_conv3x3_build_size(ci, co, h, w) == (C.conv_tjac_exact(ci, co, h, w).nnz, 0)

@@ -177,3 +177,60 @@ def test_vgg11_config5(lib, sched):
         for i in range(2, n, 2):
             tot += len(C.plan_product(a[i + 1].pattern(), a[i].pattern()).left_pos)
         assert info["contributions"] == tot
+
+
+# ------------------------------------------------------------------ NEXT-3: device builders, static FLOPs
+@pytest.mark.parametrize("ci,co,h,w,density", [(3, 64, 32, 32, 1.0), (64, 128, 16, 16, 0.03), (5, 7, 1, 6, 1.0),
+                                                (4, 3, 2, 2, 0.5), (2, 5, 7, 3, 0.3), (512, 512, 2, 2, 0.03)])
+def test_device_conv_builder_matches_host_and_oracle(lib, ci, co, h, w, density):
+    """bppsa_csr_conv3x3_build (Algs. 2-4 on the GPU) == the host builder and
+    the oracle's exact stencil, bit for bit (indptr, indices, tap, data)."""
+    rng = np.random.default_rng(ci + co + h)
+    wt = rng.standard_normal((co, ci, 3, 3)).astype(np.float32)
+    drop = density < 1
+    if drop:
+        wt[rng.random(wt.shape) >= density] = 0.0
+    wdev = torch.from_numpy(wt.reshape(-1)).cuda()
+    ip, ix, tap, data = lib.csr_conv3x3_build(ci, co, h, w, wdev, drop_zero=drop, with_data=True)
+    torch.cuda.synchronize()
+    hip, hix, htap = lib.csr_conv3x3_pattern(ci, co, h, w, wt, drop_zero=drop)
+    assert np.array_equal(ip.cpu().numpy(), hip)
+    assert np.array_equal(ix.cpu().numpy(), hix)
+    assert np.array_equal(tap.cpu().numpy(), htap)
+    assert np.array_equal(data.cpu().numpy(), wt.reshape(-1)[htap])
+    if ci * co * h * w <= 64 * 128 * 16 * 16:
+        m = C.conv_tjac_exact(ci, co, h, w, wt, drop_zero_weights=drop)
+        assert np.array_equal(ip.cpu().numpy(), m.indptr) and np.array_equal(ix.cpu().numpy(), m.indices)
+        assert np.array_equal(data.cpu().numpy().astype(np.float64), m.data)
+
+
+def test_device_pool_and_identity_builders(lib):
+    for c, h, w in [(64, 32, 32), (3, 2, 2), (5, 6, 4)]:
+        ip, ix = lib.csr_maxpool_build(c, h, w)
+        hip, hix = lib.csr_maxpool_pattern(c, h, w)
+        assert np.array_equal(ip.cpu().numpy(), hip) and np.array_equal(ix.cpu().numpy(), hix)
+    ip, ix = lib.csr_identity_build(65536)
+    assert np.array_equal(ip.cpu().numpy(), np.arange(65537)) and np.array_equal(ix.cpu().numpy(), np.arange(65536))
+
+
+def _steps_equal(got, want):
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g == {k: w[k] for k in g}, (g, w)
+
+
+@pytest.mark.parametrize("n", [1, 3, 8, 13])
+def test_plan_steps_match_oracle_random(lib, n):
+    """bppsa_csr_plan_steps == oracle.scan.hybrid_steps on every split."""
+    chain, pats, *_ = random_chain(n, 2, seed=40 + n, int_data=True)
+    for lv in [(u, dl) for u in range(0, S.num_levels(n)) for dl in (u, u + 1) if dl <= S.num_levels(n)]:
+        got = lib.csr_plan_steps(lib.csr_plan_create(pats, *lv))
+        _steps_equal(got, S.hybrid_steps([m.pattern() for m in chain], *lv))
+
+
+def test_plan_steps_small_vgg(lib):
+    cfg, B, hw = [4, "M", 6, 6, "M", 8, "M"], 2, 8
+    ws, recs, s = vgg_case(cfg, B, hw, seed=7, density=0.5)
+    dev, chain = build_both(lib, cfg, ws, recs, B, hw)
+    for lv in [(0, 0), (2, 3), (3, 4)]:
+        _steps_equal(lib.csr_plan_steps(dev.plan(*lv)), S.hybrid_steps([m.pattern() for m in chain], *lv))
