@@ -100,6 +100,41 @@ def bp_gru(tape, W_hh3, seed):
 
 
 # ---------------------------------------------------------------------------
+# Per-step losses: the affine recurrence (reading 8 notes
+# the paper covers the last-step loss only).  With l = sum_t l_t(h_t)
+# and e_t = dl_t/dh_t (partial), the total derivative obeys
+#     grad_h[T-1] = seed + e_{T-1},   grad_h[t-1] = J_t^T grad_h[t] + e_{t-1},
+# and dl/dh_init = J_0^T grad_h[0] (no e_{-1}).  As a scan: elements (J^T, e)
+# composed by (A, a) <> (B, b) = (BA, Ba + b).
+# ---------------------------------------------------------------------------
+
+def bp_affine(jt, T, seed, e):
+    """Sequential affine BP; jt(t) -> J_t^T [B,H,H]; e: [T,B,H]."""
+    e = _d(e)
+    v = _d(seed) + e[T - 1]
+    out = np.empty((T,) + v.shape, D)
+    for t in range(T - 1, -1, -1):
+        out[t] = v
+        v = np.einsum("bik,bk->bi", jt(t), v)
+        if t >= 1:
+            v = v + e[t - 1]
+    return out, v
+
+
+def bp_rnn_affine(h, W_hh, seed, e):
+    return bp_affine(lambda t: rnn_jt(h[t], W_hh), len(h), seed, e)
+
+
+def bp_dense_affine(JT, seed, e):
+    return bp_affine(lambda t: _d(JT[t]), len(JT), seed, e)
+
+
+def bp_gru_affine(tape, W_hh3, seed, e):
+    return bp_affine(lambda t: gru_jt(tape["h_prev"][t], tape["r"][t], tape["z"][t], tape["n"][t],
+                                      tape["M"][t], W_hh3), len(tape["r"]), seed, e)
+
+
+# ---------------------------------------------------------------------------
 # Parameter gradients, eqn:update_param (P:81-85) with tied weights summed over
 # time (S:345): each time step is a layer sharing theta.
 # ---------------------------------------------------------------------------
