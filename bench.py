@@ -240,6 +240,15 @@ def run_ours(args):
         result["e2e"] = e2e_ours(api, w, args)
         result["sequential_bp"] = sequential_baselines(api, w, args)
         result["sweep"] = sweep_small(api, args)
+        # NEXT-4: the affine scan (a loss on every step) on the same C4 inputs
+        gen = torch.Generator(device=dev).manual_seed(args.seed)
+        e_steps = torch.randn((T, B, H), device=dev, generator=gen) * 0.01
+        aff = _time(lambda: api.scan_affine(jac, g, e_steps, grad_h=grad, ws=ws, block0=C4_BLOCK0,
+                                            block=C4_BLOCK), reps=5, warm=2)
+        plain = _time(lambda: api.scan(jac, g, grad_h=grad, ws=ws, block0=C4_BLOCK0, block=C4_BLOCK), reps=5, warm=2)
+        result["affine"] = {"workload": "C4 shapes, per-step losses e ~ 0.01 N(0,1) (synthetic)",
+                            "scan_affine_ms": round(aff, 3), "scan_ms": round(plain, 3)}
+        del e_steps
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -704,6 +713,7 @@ def main():
         sb["speedup_vs_cudnn"] = None if sb["cudnn_backward_ms"] is None else round(sb["cudnn_backward_ms"] / r["ms"], 2)
         line["sequential_bp"] = sb
         line["sweep"] = r["sweep"]
+        line["sweep"]["affine_c4"] = r["affine"]
         line["cpu_baseline"] = oracle_sample()
     print(json.dumps(line), flush=True)
 

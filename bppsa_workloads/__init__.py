@@ -108,6 +108,15 @@ def rnn_workload(T: int, B: int, H: int, seed: int = 0, I: int = 1) -> RnnWorklo
     return RnnWorkload(x, labels, p, h, g)
 
 
+def per_step_seeds(w: RnnWorkload, seed: int = 0) -> np.ndarray:
+    """Per-step losses: a label y_t ~ U{0..9} per step and the
+    same head on every h_t; e[t] = dl_t/dh_t [T, B, H] (the head's derivative
+    at each step, an input of the affine scan like the seed)."""
+    T, B, _ = w.h.shape
+    ys = _rng(seed + 7).integers(0, 10, size=(T, B))
+    return np.stack([head_seed(w.h[t], w.params["W_out"], w.params["b_out"], ys[t]) for t in range(T)])
+
+
 def norm_preserving_rnn(T: int, B: int, H: int, seed: int = 0):
     """W_hh = c Q (Q seeded orthogonal), h_t ~ U(-0.01, 0.01), c = 1/(1 - 0.01^2/3).
 

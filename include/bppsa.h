@@ -162,6 +162,22 @@ bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h,
                         float* grad_h_init, void* ws, size_t ws_bytes,
                         const bppsa_scan_opts* opts, void* stream);
 
+/* Per-step losses (not in the paper, whose loss sits on
+ * the last step, P:317 / reading 8): l = sum_t l_t(h_t), e [T][B][H] device,
+ * e[t] = the partial dl_t/dh_t.  The recurrence becomes affine,
+ *   grad_h[T-1] = seed + e[T-1],  grad_h[t-1] = J_t^T grad_h[t] + e[t-1],
+ *   dl/dh_init = J_0^T grad_h[0],
+ * scanned with elements (J^T, e) and (A, a) <> (B, b) = (BA, Ba + b): the
+ * block aggregates keep their matrix parts (same kernels, tensor-core fold
+ * included) and gain a vector part from one extra GEMV pass per level; the
+ * level-0 walk adds e (CUDA-core walk).  BLOCKED and LINEAR modes (others:
+ * BPPSA_ERR_NOT_SUPPORTED); same workspace as bppsa_scan; e = 0 gives
+ * bppsa_scan's result.                                                      */
+bppsa_status bppsa_scan_affine(const bppsa_jac* jac, const float* seed,
+                               const float* e, float* grad_h,
+                               float* grad_h_init, void* ws, size_t ws_bytes,
+                               const bppsa_scan_opts* opts, void* stream);
+
 /* Multi-GPU: contiguous time shards, rank order = time order.
  * `jac` describes this rank's T_local steps.  The rank holding t = T-1 (the
  * last rank) passes its seed and is the "head" shard.

@@ -43,6 +43,7 @@ EXPORTS = {
     "bppsa_jacobians_gru": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_Jac), _vp]),
     "bppsa_scan_workspace_size": (_i, [C.POINTER(_Jac), C.POINTER(_Opts), C.POINTER(_sz)]),
     "bppsa_scan": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_scan_affine": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_scan_shard_up": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_scan_shard_down": (_i, [C.POINTER(_Jac), _vp, _vp, _i, _i, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_weight_grads_workspace_size": (_i, [_i, _i, _i, _i, C.POINTER(_sz)]),
@@ -224,6 +225,28 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
     _check(_lib.bppsa_scan(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(grad_h, "grad_h"),
                            _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
                            _stream(stream)), "bppsa_scan")
+    return grad_h, grad_h_init
+
+
+def scan_affine(jac: Jacobians, seed: torch.Tensor, e: torch.Tensor, grad_h: torch.Tensor | None = None,
+                grad_h_init: torch.Tensor | bool | None = None, ws: torch.Tensor | None = None,
+                mode="blocked", block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None,
+                leaf_impl="auto"):
+    """bppsa_scan_affine: per-step losses, e [T,B,H] = dl_t/dh_t (partial)."""
+    T, B, H = jac.T, jac.B, jac.H
+    dev = seed.device
+    if grad_h is None:
+        grad_h = torch.empty((T, B, H), dtype=torch.float32, device=dev)
+    if grad_h_init is True:
+        grad_h_init = torch.empty((B, H), dtype=torch.float32, device=dev)
+    elif grad_h_init is False:
+        grad_h_init = None
+    o = _opts(mode, block0, block, trace, leaf_impl)
+    if ws is None:
+        ws = workspace(scan_workspace_size(jac, mode, block0, block), dev)
+    _check(_lib.bppsa_scan_affine(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(e, "e"), _ptr(grad_h, "grad_h"),
+                                  _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
+                                  _stream(stream)), "bppsa_scan_affine")
     return grad_h, grad_h_init
 
 

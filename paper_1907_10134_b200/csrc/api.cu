@@ -122,7 +122,8 @@ struct Plan {
   long long n[kMaxLevels + 2] = {};
   int C[kMaxLevels + 2] = {};
   size_t agg_off[kMaxLevels + 2] = {}, out_off[kMaxLevels + 2] = {};
-  size_t dense_off = 0, carry_off = 0, total = 0;
+  size_t vec_off[kMaxLevels + 2] = {};   // affine vector parts [B][n_l][H] (l >= 1)
+  size_t dense_off = 0, carry_off = 0, aseed_off = 0, total = 0;
   bool has_dense = false;
 };
 
@@ -223,8 +224,12 @@ bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts
     off = align_up(off + B * (size_t)p->n[k] * HH * sizeof(float));
     p->out_off[k] = off;
     off = align_up(off + B * (size_t)p->n[k] * j.H * sizeof(float));
+    p->vec_off[k] = off;
+    off = align_up(off + B * (size_t)p->n[k] * j.H * sizeof(float));
   }
   p->carry_off = off;
+  off = align_up(off + B * j.H * sizeof(float));
+  p->aseed_off = off;
   off = align_up(off + B * j.H * sizeof(float));
   p->total = off;
   return BPPSA_OK;
@@ -274,14 +279,30 @@ MatAcc level_acc(const Plan& p, char* ws, int l, int H) {
 }
 
 float* level_out(const Plan& p, char* ws, int l) { return reinterpret_cast<float*>(ws + p.out_off[l]); }
+float* level_vec(const Plan& p, char* ws, int l) { return reinterpret_cast<float*>(ws + p.vec_off[l]); }
+VecAcc level_addv(const Plan& p, char* ws, int l, int H) {   // vector parts of level l (affine)
+  VecAcc v;
+  v.base = level_vec(p, ws, l);
+  v.slot_stride = H;
+  v.batch_stride = p.n[l] * (long long)H;
+  v.time_mode = 0;
+  return v;
+}
+VecAcc leaf_addv(const float* e) {
+  VecAcc v;
+  v.base = e;
+  v.time_mode = 1;
+  return v;
+}
 float* level_agg(const Plan& p, char* ws, int l) { return reinterpret_cast<float*>(ws + p.agg_off[l]); }
 
 // Up-sweep: levels 0 .. L-1 fold into levels 1 .. L.  `top_out` (nullable)
 // replaces the storage of level L (used by shard_up to write the aggregate
 // straight into the caller's buffer).
 bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan& p, char* ws, float* top_out,
-                    cudaStream_t st, Tracer& tr) {
+                    cudaStream_t st, Tracer& tr, const float* e_aff = nullptr) {
   const int H = j.H, B = j.B;
+  const Seg seg{j.T, j.B, j.H, head};
   for (int l = 0; l < p.L; ++l) {
     float* dst = (l + 1 == p.L && top_out) ? top_out : level_agg(p, ws, l + 1);
     cudaError_t e;
@@ -314,6 +335,24 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
     }
     tr.end(st);
     if (e != cudaSuccess) return cuda_status(e, "up-sweep launch");
+    if (e_aff) {
+      // affine vector parts m of the level-(l+1) elements (the matrix parts
+      // above are unchanged); the head block's vector replaces its slot
+      tr.begin(st);
+      const long long hb = p.n[l + 1] * (long long)H * H;
+      if (l == 0 && j.kind != BPPSA_JAC_DENSE)
+        e = launch_leaf_down(leaf_args(j, head, seed), p.C[0], nullptr, p.n[1], nullptr, nullptr, st, e_aff,
+                             level_vec(p, ws, 1), dst, hb);
+      else if (l == 0)
+        e = launch_walk_down(dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed), H, B, p.n[0],
+                             p.C[0], head, nullptr, p.n[1], nullptr, 1, seg, nullptr, st, leaf_addv(e_aff),
+                             level_vec(p, ws, 1), dst, hb);
+      else
+        e = launch_walk_down(level_acc(p, ws, l, H), H, B, p.n[l], p.C[l], head, nullptr, p.n[l + 1], nullptr, 0,
+                             seg, nullptr, st, level_addv(p, ws, l, H), level_vec(p, ws, l + 1), dst, hb);
+      tr.end(st);
+      if (e != cudaSuccess) return cuda_status(e, "affine up-sweep launch");
+    }
   }
   return BPPSA_OK;
 }
@@ -322,7 +361,7 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
 // the symbolic identity for a head segment) to the leaves.
 bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Plan& p, char* ws, int ltop,
                       long long ltop_C, const float* carry_top, float* grad_h, float* grad_init,
-                      cudaStream_t st, Tracer& tr) {
+                      cudaStream_t st, Tracer& tr, const float* e_aff = nullptr) {
   const int H = j.H, B = j.B;
   const Seg seg{j.T, j.B, j.H, head};
   for (int l = ltop; l >= 0; --l) {
@@ -334,16 +373,17 @@ bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Pla
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
       // tcgen05 walk: many short chains (the linear scan's single long chain per
       // sample stays on the CUDA cores; so do single-block segments)
-      if (use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8)
+      if (!e_aff && use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8)
         e = launch_tc_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st);
       else
-        e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st);
+        e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st, e_aff);
     } else if (l == 0) {
       const MatAcc A = dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed);
-      e = launch_walk_down(A, H, B, p.n[0], Cl, head, carry, nblk, grad_h, 1, seg, grad_init, st);
+      e = launch_walk_down(A, H, B, p.n[0], Cl, head, carry, nblk, grad_h, 1, seg, grad_init, st,
+                           e_aff ? leaf_addv(e_aff) : VecAcc{});
     } else {
       e = launch_walk_down(level_acc(p, ws, l, H), H, B, p.n[l], Cl, head, carry, nblk, level_out(p, ws, l), 0,
-                           seg, nullptr, st);
+                           seg, nullptr, st, e_aff ? level_addv(p, ws, l, H) : VecAcc{});
     }
     tr.end(st);
     if (e != cudaSuccess) return cuda_status(e, "down-sweep launch");
@@ -468,8 +508,9 @@ bppsa_status bppsa_scan_workspace_size(const bppsa_jac* jac, const bppsa_scan_op
   return BPPSA_OK;
 }
 
-bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h, float* grad_h_init, void* ws,
-                        size_t ws_bytes, const bppsa_scan_opts* opts, void* stream) {
+static bppsa_status scan_impl(const bppsa_jac* jac, const float* seed, const float* e_aff, float* grad_h,
+                              float* grad_h_init, void* ws, size_t ws_bytes, const bppsa_scan_opts* opts,
+                              void* stream) {
   bppsa_status s = check_jac(jac);
   if (s != BPPSA_OK) return s;
   REQUIRE_DEV(seed, "seed");
@@ -521,14 +562,37 @@ bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h, 
     report_launches(opts, tr);
     return BPPSA_OK;
   }
+  if (e_aff) {   // head element seed + e_{T-1} (reading 8 / NEXT-4)
+    float* aseed = reinterpret_cast<float*>(w + p.aseed_off);
+    tr.begin(st);
+    cudaError_t e = launch_affine_seed(seed, e_aff, j.T, j.B, j.H, aseed, st);
+    tr.end(st);
+    if (e != cudaSuccess) return cuda_status(e, "affine seed");
+    seed = aseed;
+  }
   s = prepare_dense(j, p, w, st, tr);
   if (s != BPPSA_OK) return s;
-  s = run_up(j, 1, seed, p, w, nullptr, st, tr);
+  s = run_up(j, 1, seed, p, w, nullptr, st, tr, e_aff);
   if (s != BPPSA_OK) return s;
   // top level: one block walked from the symbolic identity (head segment)
-  s = run_down(j, 1, seed, p, w, p.L, p.n[p.L], nullptr, grad_h, grad_h_init, st, tr);
+  s = run_down(j, 1, seed, p, w, p.L, p.n[p.L], nullptr, grad_h, grad_h_init, st, tr, e_aff);
   report_launches(opts, tr);
   return s;
+}
+
+bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h, float* grad_h_init, void* ws,
+                        size_t ws_bytes, const bppsa_scan_opts* opts, void* stream) {
+  return scan_impl(jac, seed, nullptr, grad_h, grad_h_init, ws, ws_bytes, opts, stream);
+}
+
+bppsa_status bppsa_scan_affine(const bppsa_jac* jac, const float* seed, const float* e, float* grad_h,
+                               float* grad_h_init, void* ws, size_t ws_bytes, const bppsa_scan_opts* opts,
+                               void* stream) {
+  REQUIRE_DEV(e, "e");
+  const int mode = opts ? opts->mode : BPPSA_SCAN_BLOCKED;
+  if (mode != BPPSA_SCAN_BLOCKED && mode != BPPSA_SCAN_LINEAR)
+    return fail(BPPSA_ERR_NOT_SUPPORTED, "the affine scan runs in the BLOCKED and LINEAR modes");
+  return scan_impl(jac, seed, e, grad_h, grad_h_init, ws, ws_bytes, opts, stream);
 }
 
 bppsa_status bppsa_scan_shard_up(const bppsa_jac* jac, const float* seed, float* aggregate, void* ws,

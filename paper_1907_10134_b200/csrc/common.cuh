@@ -56,6 +56,23 @@ struct MatAcc {
   }
 };
 
+// Additive vector term of the affine scan (per-step losses):
+// element s is (A_s, m_s), out[s+1] = A_s out[s] + m_s.  time_mode 0: m_s at
+// base + s*slot_stride + b*batch_stride (an upper level's vector parts);
+// time_mode 1: base = e [T][B][H] and slot s (holding J_t^T, t = time_of(s))
+// adds e_{t-1} (nothing at t = 0).  base == nullptr: no additive term.
+struct VecAcc {
+  const float* base = nullptr;
+  long long slot_stride = 0, batch_stride = 0;
+  int time_mode = 0;
+  __device__ __forceinline__ const float* at(int b, long long s, const Seg& seg, int B, int H) const {
+    if (base == nullptr) return nullptr;
+    if (time_mode == 0) return base + s * slot_stride + (long long)b * batch_stride;
+    const int t = seg.time_of(s) - 1;
+    return t < 0 ? nullptr : base + ((long long)t * B + b) * H;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Kernel launchers (defined in the .cu files).
 // ---------------------------------------------------------------------------
@@ -80,18 +97,30 @@ cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, 
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                                 float* grad_init, int num_sms, cudaStream_t st);
 // level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable
+// Affine (e != nullptr): v <- J_t^T v + e_{t-1}.  vec_out != nullptr: the
+// block's vector part instead of a walk — from 0 (or the head's seed) through
+// every element of the block, stored at vec_out[b][q][H]; the head block's
+// value also at head_out + b*head_bstride.
 cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry,
                              long long nblk, float* grad_h, float* grad_init,
-                             cudaStream_t st);
+                             cudaStream_t st, const float* e = nullptr,
+                             float* vec_out = nullptr, float* head_out = nullptr,
+                             long long head_bstride = 0);
 
 // explicit level fold / walk
 cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, int head,
                            float* agg_out, long long n_out, cudaStream_t st);
 // out_mode 0: out[b][s][H] (carry array with n slots); 1: grad_h via seg time map
+// addv / vec_out / head_out: the affine terms as for launch_leaf_down
 cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, int head,
                              const float* carry_in, long long nblk, float* out,
                              int out_mode, const Seg& seg, float* total_out,
-                             cudaStream_t st);
+                             cudaStream_t st, const VecAcc& addv = VecAcc{},
+                             float* vec_out = nullptr, float* head_out = nullptr,
+                             long long head_bstride = 0);
+// dst[b][i] = seed[b][i] + e[T-1][b][i] (the affine head, reading 8)
+cudaError_t launch_affine_seed(const float* seed, const float* e, int T, int B, int H, float* dst,
+                               cudaStream_t st);
 
 // DENSE helpers
 cudaError_t launch_transpose_dense(const float* JT, float* JTc, long long mats, int H,

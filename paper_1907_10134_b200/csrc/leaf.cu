@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(128, UpBounds<CELL, HT, NC>::minb) leaf_up_ker
 template <int CELL, int HT>
 __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const float* __restrict__ carry,
                                                         long long nblk, float* __restrict__ grad_h,
-                                                        float* __restrict__ grad_init) {
+                                                        float* __restrict__ grad_init, const float* __restrict__ e,
+                                                        float* __restrict__ vec_out, float* __restrict__ head_out,
+                                                        long long head_bstride) {
   constexpr int NR = (HT + 31) / 32;
   constexpr int NV = NX<CELL>::v;
   constexpr int XW = NV * HT;
@@ -310,6 +312,7 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
   const long long S = a.seg.S();
   const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
   const bool vec = a.seg.head && q == 0;
+  const bool vonly = vec_out != nullptr;     // affine vector part of the block
 
   float w[NV][NR][HT];
   load_w<CELL, HT, NR>(a, H, lane, w);
@@ -319,7 +322,12 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
   for (int m = 0; m < NR; ++m) {
     const int i = lane + 32 * m;
     v[m] = 0.f;
-    if (i < H) v[m] = vec ? __ldg(a.seed + (long long)b * H + i) : __ldg(carry + (q + (long long)b * nblk) * H + i);
+    if (i < H) {
+      if (vec)
+        v[m] = __ldg(a.seed + (long long)b * H + i);
+      else if (!vonly)
+        v[m] = __ldg(carry + (q + (long long)b * nblk) * H + i);
+    }
   }
   const long long rowB = (long long)B * H;
   long long s = vec ? 1 : s0;
@@ -335,14 +343,16 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
   int buf = 0;
   for (; s < s1; ++s) {
     const long long t = a.seg.time_of(s);
+    if (!vonly) {
 #pragma unroll
-    for (int m = 0; m < NR; ++m) {
-      const int i = lane + 32 * m;
-      if (i < H) grad_h[t * rowB + (long long)b * H + i] = v[m];
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H) grad_h[t * rowB + (long long)b * H + i] = v[m];
+      }
     }
     const bool last = (s + 1 == s1);
-    const bool total = last && s1 == S && grad_init != nullptr;
-    if (last && !total) break;
+    const bool total = !vonly && last && s1 == S && grad_init != nullptr;
+    if (last && !total && !vonly) break;
     Coef<CELL> cur[NR];
 #pragma unroll
     for (int m = 0; m < NR; ++m) cur[m] = nxt[m];
@@ -353,6 +363,12 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
         const int i = lane + 32 * m;
         nxt[m] = load_coef<CELL>(a, tn * rowB + (long long)b * H + i, i < H);
       }
+    }
+    float ev[NR];                                   // e_{t-1}, loaded ahead of the GEMV
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      ev[m] = (e != nullptr && t >= 1 && i < H) ? __ldg(e + (t - 1) * rowB + (long long)b * H + i) : 0.f;
     }
     float* xb = xs + buf * XW;
 #pragma unroll
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
 #pragma unroll
     for (int m = 0; m < NR; ++m) {
       if (CELL == BPPSA_JAC_GRU) acc[m] = fmaf(cur[m].c[3], v[m], acc[m]);
-      v[m] = acc[m];
+      v[m] = acc[m] + ev[m];
     }
     buf ^= 1;
     if (total) {
@@ -377,6 +393,16 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
       for (int m = 0; m < NR; ++m) {
         const int i = lane + 32 * m;
         if (i < H) grad_init[(long long)b * H + i] = v[m];
+      }
+    }
+  }
+  if (vonly) {
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      if (i < H) {
+        vec_out[((long long)b * nblk + q) * H + i] = v[m];
+        if (vec && head_out != nullptr) head_out[(long long)b * head_bstride + i] = v[m];
       }
     }
   }
@@ -401,14 +427,20 @@ cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, l
   return cudaGetLastError();
 }
 
+struct DownX {   // the affine extras of the level-0 walk
+  const float* e;
+  float *vec_out, *head_out;
+  long long head_bstride;
+};
+
 template <int CELL, int HT>
 cudaError_t down_impl(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
-                      float* grad_init, cudaStream_t st) {
+                      float* grad_init, cudaStream_t st, const DownX& x) {
   const long long tasks = (long long)a.seg.B * nblk;
   const long long grid = (tasks + kWarpsPerCta - 1) / kWarpsPerCta;
   const size_t smem = (size_t)kWarpsPerCta * 2 * NX<CELL>::v * HT * sizeof(float);
-  leaf_down_kernel<CELL, HT><<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(a, C, carry, nblk,
-                                                                           grad_h, grad_init);
+  leaf_down_kernel<CELL, HT><<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(
+      a, C, carry, nblk, grad_h, grad_init, x.e, x.vec_out, x.head_out, x.head_bstride);
   return cudaGetLastError();
 }
 
@@ -427,15 +459,17 @@ cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n
 }
 
 cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk,
-                             float* grad_h, float* grad_init, cudaStream_t st) {
+                             float* grad_h, float* grad_init, cudaStream_t st, const float* e, float* vec_out,
+                             float* head_out, long long head_bstride) {
   const int H = a.seg.H;
+  const DownX x{e, vec_out, head_out, head_bstride};
   if (a.kind == BPPSA_JAC_RNN_TANH) {
-    if (H == 20) return down_impl<BPPSA_JAC_RNN_TANH, 20>(a, C, carry, nblk, grad_h, grad_init, st);
-    if (H <= 32) return down_impl<BPPSA_JAC_RNN_TANH, 32>(a, C, carry, nblk, grad_h, grad_init, st);
-    return down_impl<BPPSA_JAC_RNN_TANH, 64>(a, C, carry, nblk, grad_h, grad_init, st);
+    if (H == 20) return down_impl<BPPSA_JAC_RNN_TANH, 20>(a, C, carry, nblk, grad_h, grad_init, st, x);
+    if (H <= 32) return down_impl<BPPSA_JAC_RNN_TANH, 32>(a, C, carry, nblk, grad_h, grad_init, st, x);
+    return down_impl<BPPSA_JAC_RNN_TANH, 64>(a, C, carry, nblk, grad_h, grad_init, st, x);
   }
-  if (H == 20) return down_impl<BPPSA_JAC_GRU, 20>(a, C, carry, nblk, grad_h, grad_init, st);
-  return down_impl<BPPSA_JAC_GRU, 32>(a, C, carry, nblk, grad_h, grad_init, st);
+  if (H == 20) return down_impl<BPPSA_JAC_GRU, 20>(a, C, carry, nblk, grad_h, grad_init, st, x);
+  return down_impl<BPPSA_JAC_GRU, 32>(a, C, carry, nblk, grad_h, grad_init, st, x);
 }
 
 }  // namespace bppsa

@@ -177,9 +177,12 @@ template <int HP>
 __global__ void __launch_bounds__(128) walk_down_kernel(MatAcc A, int H, int B, long long n, int C, int head,
                                                         const float* __restrict__ carry_in, long long nblk,
                                                         float* __restrict__ out, int out_mode, Seg seg,
-                                                        float* __restrict__ total_out) {
+                                                        float* __restrict__ total_out, VecAcc addv,
+                                                        float* __restrict__ vec_out, float* __restrict__ head_out,
+                                                        long long head_bstride) {
   constexpr int NR = (HP + 31) / 32;
   constexpr int WS = 2 * HP * HP + HP;   // floats per warp
+  const bool vonly = vec_out != nullptr;   // affine vector part of the block (from 0 / the head vector)
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float* As[2] = {smem + wib * WS, smem + wib * WS + HP * HP};
@@ -199,26 +202,35 @@ __global__ void __launch_bounds__(128) walk_down_kernel(MatAcc A, int H, int B, 
   for (int m = 0; m < NR; ++m) {
     const int i = lane + 32 * m;
     v[m] = 0.f;
-    if (i < H) v[m] = vec ? A.vec(b)[i] : carry_in[(q + (long long)b * nblk) * H + i];
+    if (i < H) v[m] = vec ? A.vec(b)[i] : (vonly ? 0.f : carry_in[(q + (long long)b * nblk) * H + i]);
   }
   long long s = vec ? 1 : s0;
   int buf = 0;
   if (s < s1) stage_matrix<HP>(As[0], A.mat(b, s), H, lane);
   cp_commit();
   for (; s < s1; ++s) {
+    if (!vonly) {
 #pragma unroll
-    for (int m = 0; m < NR; ++m) {
-      const int i = lane + 32 * m;
-      if (i < H) {
-        if (out_mode == 0)
-          out[((long long)b * n + s) * H + i] = v[m];
-        else
-          out[((long long)seg.time_of(s) * B + b) * H + i] = v[m];
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H) {
+          if (out_mode == 0)
+            out[((long long)b * n + s) * H + i] = v[m];
+          else
+            out[((long long)seg.time_of(s) * B + b) * H + i] = v[m];
+        }
       }
     }
     const bool last = (s + 1 == s1);
-    const bool total = last && s1 == n && total_out != nullptr;
-    if (last && !total) break;
+    const bool total = !vonly && last && s1 == n && total_out != nullptr;
+    if (last && !total && !vonly) break;
+    const float* ap = addv.at(b, s, seg, B, H);
+    float av[NR];
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      av[m] = (ap != nullptr && i < H) ? ap[i] : 0.f;
+    }
     if (!last) stage_matrix<HP>(As[buf ^ 1], A.mat(b, s + 1), H, lane);
     cp_commit();
 #pragma unroll
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(128) walk_down_kernel(MatAcc A, int H, int B, 
       }
     }
 #pragma unroll
-    for (int m = 0; m < NR; ++m) v[m] = (part[m][0] + part[m][1]) + (part[m][2] + part[m][3]);
+    for (int m = 0; m < NR; ++m) v[m] = ((part[m][0] + part[m][1]) + (part[m][2] + part[m][3])) + av[m];
     __syncwarp();
     buf ^= 1;
     if (total) {
@@ -260,6 +272,16 @@ __global__ void __launch_bounds__(128) walk_down_kernel(MatAcc A, int H, int B, 
     }
   }
   cp_wait<0>();
+  if (vonly) {
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const int i = lane + 32 * m;
+      if (i < H) {
+        vec_out[((long long)b * nblk + q) * H + i] = v[m];
+        if (vec && head_out != nullptr) head_out[(long long)b * head_bstride + i] = v[m];
+      }
+    }
+  }
 }
 
 constexpr int kWarps = 4;
@@ -282,7 +304,7 @@ cudaError_t fold_impl(const MatAcc& A, int H, int B, long long n, int C, int hea
 template <int HP>
 cudaError_t walk_impl(const MatAcc& A, int H, int B, long long n, int C, int head, const float* carry_in,
                       long long nblk, float* out, int out_mode, const Seg& seg, float* total_out,
-                      cudaStream_t st) {
+                      cudaStream_t st, const VecAcc& addv, float* vec_out, float* head_out, long long head_bstride) {
   const size_t smem = (size_t)kWarps * (2 * HP * HP + HP) * sizeof(float);
   auto k = walk_down_kernel<HP>;
   if (smem > 48 * 1024) {
@@ -291,7 +313,8 @@ cudaError_t walk_impl(const MatAcc& A, int H, int B, long long n, int C, int hea
   }
   const long long tasks = (long long)B * nblk;
   k<<<(unsigned)((tasks + kWarps - 1) / kWarps), 32 * kWarps, smem, st>>>(A, H, B, n, C, head, carry_in, nblk,
-                                                                          out, out_mode, seg, total_out);
+                                                                          out, out_mode, seg, total_out, addv,
+                                                                          vec_out, head_out, head_bstride);
   return cudaGetLastError();
 }
 
@@ -572,10 +595,27 @@ cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, in
 
 cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, int head,
                              const float* carry_in, long long nblk, float* out, int out_mode, const Seg& seg,
-                             float* total_out, cudaStream_t st) {
-  if (H == 20) return walk_impl<20>(A, H, B, n, C, head, carry_in, nblk, out, out_mode, seg, total_out, st);
-  if (H <= 32) return walk_impl<32>(A, H, B, n, C, head, carry_in, nblk, out, out_mode, seg, total_out, st);
-  return walk_impl<64>(A, H, B, n, C, head, carry_in, nblk, out, out_mode, seg, total_out, st);
+                             float* total_out, cudaStream_t st, const VecAcc& addv, float* vec_out,
+                             float* head_out, long long head_bstride) {
+  if (H == 20)
+    return walk_impl<20>(A, H, B, n, C, head, carry_in, nblk, out, out_mode, seg, total_out, st, addv, vec_out,
+                         head_out, head_bstride);
+  if (H <= 32)
+    return walk_impl<32>(A, H, B, n, C, head, carry_in, nblk, out, out_mode, seg, total_out, st, addv, vec_out,
+                         head_out, head_bstride);
+  return walk_impl<64>(A, H, B, n, C, head, carry_in, nblk, out, out_mode, seg, total_out, st, addv, vec_out,
+                       head_out, head_bstride);
+}
+
+__global__ void affine_seed_kernel(const float* __restrict__ seed, const float* __restrict__ e, int T, int B,
+                                   int H, float* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B * H) dst[i] = seed[i] + e[(long long)(T - 1) * B * H + i];
+}
+
+cudaError_t launch_affine_seed(const float* seed, const float* e, int T, int B, int H, float* dst, cudaStream_t st) {
+  affine_seed_kernel<<<(B * H + 255) / 256, 256, 0, st>>>(seed, e, T, B, H, dst);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_transpose_dense(const float* JT, float* JTc, long long mats, int H, cudaStream_t st) {

@@ -1,0 +1,123 @@
+"""GPU parity of bppsa_scan_affine (per-step losses)
+against the oracle's affine BP (oracle.bp.bp_*_affine), through the C-ABI.
+Gates as for bppsa_scan: <= 1e-4 max-norm relative (reading 12), bit-exact
+on integer families."""
+import numpy as np
+import pytest
+import torch
+
+import bppsa_workloads as W
+from oracle import bp
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def rel_pair(grad, gi, ref, ref_init):
+    s = float(np.abs(ref).max())
+    g = grad.cpu().numpy().astype(np.float64)
+    i = gi.cpu().numpy().astype(np.float64)
+    return max(np.abs(g - ref).max(), np.abs(i - ref_init).max()) / s
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 17, 100, 257, 1000, 4097])
+@pytest.mark.parametrize("H", [20, 64])
+@pytest.mark.parametrize("leaf_impl", ["auto", "ffma"])
+def test_rnn_affine_realistic(lib, T, H, leaf_impl):
+    w = W.rnn_workload(T, 4, H, seed=T + H)
+    e = W.per_step_seeds(w, seed=T)
+    ref, ref_init = bp.bp_rnn_affine(w.h, w.W_hh, w.g, e)
+    jac = lib.jacobians_rnn(cu(w.h), cu(w.W_hh))
+    grad, gi = lib.scan_affine(jac, cu(w.g), cu(e), grad_h_init=True, leaf_impl=leaf_impl)
+    torch.cuda.synchronize()
+    assert rel_pair(grad, gi, ref, ref_init) <= TOL
+
+
+@pytest.mark.parametrize("H", [5, 20, 33, 64])
+@pytest.mark.parametrize("blocks", [(2, 2), (3, 5), (7, 4), (512, 32)])
+def test_rnn_affine_blocks_norm_preserving(lib, H, blocks):
+    # T = 1500: with block (2, 2) the tree is ~10 levels of fp32 64 x 64
+    # products, whose rounding on this family grows with depth (reading 12)
+    T, B = 1500, 3
+    f = W.norm_preserving_rnn(T, B, H, seed=H)
+    e = (np.random.default_rng(H).standard_normal((T, B, H)) * 0.1).astype(np.float32)
+    ref, ref_init = bp.bp_rnn_affine(f["h"], f["W_hh"], f["g"], e)
+    jac = lib.jacobians_rnn(cu(f["h"]), cu(f["W_hh"]))
+    grad, gi = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, block0=blocks[0], block=blocks[1])
+    torch.cuda.synchronize()
+    assert rel_pair(grad, gi, ref, ref_init) <= TOL
+
+
+def test_rnn_affine_tensor_fold_c4_block(lib):
+    """The tcgen05 3xFP16 fold (H = 64, block0 = 512, as at C4) keeps the matrix
+    parts: realistic workload with per-step losses at the 1e-4 gate; the
+    norm-preserving family at the fold's bias bound (16 ulp per step, as for
+    bppsa_scan, DESIGN "Precision")."""
+    T, B, H = 20000, 16, 64
+    w = W.rnn_workload(T, B, H, seed=11)
+    e = W.per_step_seeds(w, seed=11)
+    ref, ref_init = bp.bp_rnn_affine(w.h, w.W_hh, w.g, e)
+    jac = lib.jacobians_rnn(cu(w.h), cu(w.W_hh))
+    grad, gi = lib.scan_affine(jac, cu(w.g), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl="tensor")
+    torch.cuda.synchronize()
+    assert rel_pair(grad, gi, ref, ref_init) <= TOL
+    f = W.norm_preserving_rnn(T, B, H, seed=1)
+    e = (np.random.default_rng(2).standard_normal((T, B, H)) * 0.05).astype(np.float32)
+    ref, ref_init = bp.bp_rnn_affine(f["h"], f["W_hh"], f["g"], e)
+    jac = lib.jacobians_rnn(cu(f["h"]), cu(f["W_hh"]))
+    grad, gi = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl="tensor")
+    gf, i_f = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl="ffma")
+    torch.cuda.synchronize()
+    assert rel_pair(gf, i_f, ref, ref_init) <= TOL
+    assert rel_pair(grad, gi, ref, ref_init) <= T * 16 * 2.0 ** -24
+
+
+@pytest.mark.parametrize("mode", ["blocked", "linear"])
+@pytest.mark.parametrize("T,H", [(1, 20), (7, 20), (300, 20), (129, 64)])
+def test_dense_affine_integer_bit_exact(lib, mode, T, H):
+    f = W.int_dense_family(T, 3, H, seed=T + H)
+    e = np.random.default_rng(T).integers(-2, 3, (T, 3, H)).astype(np.float32)
+    ref, ref_init = bp.bp_dense_affine(f["JT"], f["g"], e)
+    assert np.abs(ref).max() < 2 ** 20
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    grad, gi = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, mode=mode)
+    torch.cuda.synchronize()
+    assert np.array_equal(grad.cpu().numpy(), ref)
+    assert np.array_equal(gi.cpu().numpy(), ref_init)
+
+
+@pytest.mark.parametrize("T", [1, 50, 1034])
+def test_gru_affine(lib, T):
+    gw = W.gru_workload("L", 4, seed=3)
+    tape = {k: v[:T] for k, v in gw.tape.items()}
+    H = tape["r"].shape[2]
+    e = (np.random.default_rng(T).standard_normal((T, 4, H)) * 0.1).astype(np.float32)
+    ref, ref_init = bp.bp_gru_affine(tape, gw.params["W_hh3"], gw.g, e)
+    jac = lib.jacobians_gru(*[cu(tape[k]) for k in ("h_prev", "r", "z", "n", "M")], cu(gw.params["W_hh3"]))
+    grad, gi = lib.scan_affine(jac, cu(gw.g), cu(e), grad_h_init=True)
+    torch.cuda.synchronize()
+    assert rel_pair(grad, gi, ref, ref_init) <= TOL
+
+
+def test_affine_zero_e_is_the_plain_scan(lib):
+    w = W.rnn_workload(5000, 8, 20, seed=4)
+    jac = lib.jacobians_rnn(cu(w.h), cu(w.W_hh))
+    a, _ = lib.scan_affine(jac, cu(w.g), torch.zeros((5000, 8, 20), device="cuda"))
+    b, _ = lib.scan(jac, cu(w.g))
+    torch.cuda.synchronize()
+    ref, _ = bp.bp_rnn(w.h, w.W_hh, w.g)
+    assert np.abs(a.cpu().numpy() - b.cpu().numpy()).max() <= 1e-6 * np.abs(ref).max()
+
+
+def test_affine_errors(lib):
+    f = W.int_dense_family(10, 2, 20, seed=1)
+    jac = lib.jacobians_dense(cu(f["JT"]))
+    e = torch.zeros((10, 2, 20), device="cuda")
+    with pytest.raises(lib.BppsaError, match="NOT_SUPPORTED"):
+        lib.scan_affine(jac, cu(f["g"]), e, mode="alg1")
+    with pytest.raises(ValueError):
+        lib.scan_affine(jac, cu(f["g"]), torch.zeros((10, 2, 20)))       # host e
