@@ -170,7 +170,8 @@ bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h,
  * scanned with elements (J^T, e) and (A, a) <> (B, b) = (BA, Ba + b): the
  * block aggregates keep their matrix parts (same kernels, tensor-core fold
  * included) and gain a vector part from one extra GEMV pass per level; the
- * level-0 walk adds e (CUDA-core walk).  BLOCKED and LINEAR modes (others:
+ * level-0 walk adds e (the TMA walk at H = 64, B <= 128).  BLOCKED and
+ * LINEAR modes (others:
  * BPPSA_ERR_NOT_SUPPORTED); same workspace as bppsa_scan; e = 0 gives
  * bppsa_scan's result.                                                      */
 bppsa_status bppsa_scan_affine(const bppsa_jac* jac, const float* seed,

@@ -340,7 +340,11 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
       // above are unchanged); the head block's vector replaces its slot
       tr.begin(st);
       const long long hb = p.n[l + 1] * (long long)H * H;
-      if (l == 0 && j.kind != BPPSA_JAC_DENSE)
+      if (l == 0 && j.kind != BPPSA_JAC_DENSE && use_tensor_walk(j, p.leaf_impl) && j.B <= 128 && p.n[1] >= 2 &&
+          p.C[0] >= 8)
+        e = launch_tc_leaf_down(leaf_args(j, head, seed), p.C[0], nullptr, p.n[1], nullptr, nullptr, num_sms(), st,
+                                e_aff, level_vec(p, ws, 1), dst, hb);
+      else if (l == 0 && j.kind != BPPSA_JAC_DENSE)
         e = launch_leaf_down(leaf_args(j, head, seed), p.C[0], nullptr, p.n[1], nullptr, nullptr, st, e_aff,
                              level_vec(p, ws, 1), dst, hb);
       else if (l == 0)
@@ -373,8 +377,8 @@ bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Pla
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
       // tcgen05 walk: many short chains (the linear scan's single long chain per
       // sample stays on the CUDA cores; so do single-block segments)
-      if (!e_aff && use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8)
-        e = launch_tc_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st);
+      if (use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8 && (!e_aff || j.B <= 128))
+        e = launch_tc_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st, e_aff);
       else
         e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st, e_aff);
     } else if (l == 0) {

@@ -94,8 +94,10 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
                               int num_sms, cudaStream_t st, int prec);
 // level-1 head slot: column-major H = 64 matrix at lvl + b*bstride -> M . seed_b (in place)
 cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, int H, cudaStream_t st);
+// e / vec_out / head_out: the affine terms as for launch_leaf_down (B <= 128)
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
-                                float* grad_init, int num_sms, cudaStream_t st);
+                                float* grad_init, int num_sms, cudaStream_t st, const float* e = nullptr,
+                                float* vec_out = nullptr, float* head_out = nullptr, long long head_bstride = 0);
 // level-0 walk: carries [B][nblk][H] (or head I) -> grad_h; grad_init nullable
 // Affine (e != nullptr): v <- J_t^T v + e_{t-1}.  vec_out != nullptr: the
 // block's vector part instead of a walk — from 0 (or the head's seed) through

@@ -1234,19 +1234,26 @@ constexpr int W_NST = 3;                                    // ring stages
 constexpr int W_STAGE = 2 * TM * 128;                       // [half][128 rows][128 B] = 32 KB
 constexpr int W_OFF_RING = F_B_BYTES;                       // [slot][stage]
 constexpr int W_OFF_RED = W_OFF_RING + NSLOT * W_NST * W_STAGE;   // [slot][parity][128 rows][2] u32
-constexpr int W_OFF_BAR = W_OFF_RED + NSLOT * 2 * TM * 8;
+constexpr int W_OFF_XRED = W_OFF_RED + NSLOT * 2 * TM * 8;        // affine: the same, for max|v + e|
+constexpr int W_OFF_BAR = W_OFF_XRED + NSLOT * 2 * TM * 8;
 constexpr int W_SMEM_BYTES = W_OFF_BAR + 128 + 1024;
 constexpr int W_WPS = 8, W_EPI = 32 * W_WPS, W_NT = 2 * W_EPI;
 
 
+template <bool AFF>
 __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, const __grid_constant__ CUtensorMap h3,
                                                                      const __grid_constant__ CUtensorMap h5,
                                                                      const __grid_constant__ CUtensorMap g3,
                                                                      const __grid_constant__ CUtensorMap g5,
                                                                      int C, const float* __restrict__ carry,
                                                                      long long nblk, float* __restrict__ grad_h,
-                                                                     float* __restrict__ grad_init, int G) {
+                                                                     float* __restrict__ grad_init, int G,
+                                                                     const float* __restrict__ e_aff,
+                                                                     float* __restrict__ vec_out,
+                                                                     float* __restrict__ head_out,
+                                                                     long long head_bstride) {
   extern __shared__ uint8_t smem_raw[];
+  const bool vonly = AFF && vec_out != nullptr;   // affine vector part of each block (no grad_h stores)
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + W_OFF_BAR);
   uint64_t* h_full = d_full + NSLOT;                                    // [slot][stage]
@@ -1309,6 +1316,8 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
   const uint32_t hrow_off = (uint32_t)(row * 256 + cgp * 128);          // this thread's row half in a stage
   const int swz = (2 * row + cgp) & 7;                                    // its 128-byte line's swizzle
   const uint32_t red0 = su32(smem + W_OFF_RED) + (uint32_t)((g * 2 * TM + row) * 8);
+  const uint32_t xred0 = su32(smem + W_OFF_XRED) + (uint32_t)((g * 2 * TM + row) * 8);
+  uint32_t xpar = 0;
   const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
   uint64_t bdesc[4];
 #pragma unroll
@@ -1349,10 +1358,11 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
     float2 v[16];                                          // this thread's 32 columns of the chain (true scale)
     {
       const float* src = head ? a.seed + (long long)bsm * TH : carry + ((long long)bsm * nblk + q) * TH;
+      const bool from_src = valid && (head || !vonly);     // a vector part starts from 0
 #pragma unroll
       for (int k4 = 0; k4 < 8; ++k4) {
-        const float4 f = valid ? __ldg(reinterpret_cast<const float4*>(src + 32 * cgp) + k4)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 f = from_src ? __ldg(reinterpret_cast<const float4*>(src + 32 * cgp) + k4)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
         v[2 * k4] = make_float2(f.x, f.y);
         v[2 * k4 + 1] = make_float2(f.z, f.w);
       }
@@ -1451,8 +1461,23 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
       named_bar(5 + g, W_EPI);                              // the exchange words may be reused
     }
     int s_prev = 0;
+    // affine: e rows of the step's own time (t(s) - 1 = t(s+1): the step that
+    // consumes J_t(s-1) adds e at the time of slot s)
+    auto load_e = [&](long long slot, float2 (&ef)[16]) {
+      const float* src = e_aff + ((long long)a.seg.time_of(slot) * B + bsm) * TH + 32 * cgp;
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(src) + k4);
+        ef[2 * k4] = make_float2(f.x, f.y);
+        ef[2 * k4 + 1] = make_float2(f.z, f.w);
+      }
+    };
     for (int st = 0; st < C; ++st, ++gs) {
       WTRACE(0);
+      float2 ef[16];
+      // (a vector part also takes its last element's e: slot s1, when it exists)
+      const bool add_e = AFF && e_aff != nullptr && valid && st > 0 && (st < len || (vonly && st == len && s1 < S));
+      if (add_e) load_e(s_start + st, ef);                 // in flight during the waits below
       if (issuer) {                                         // D of step st-1 and h of step st
         if (lane == 0) {
           if (st > 0) mbar_wait_s(dbar, dph);
@@ -1470,10 +1495,42 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
         const float f = __int_as_float((127 - s_prev - sw) << 23);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __fmul2_rn(t[i], make_float2(f, f));
-        if (total && st == len) {                           // inclusive extra: J_0^T grad_h[0]
+        if (total && !vonly && st == len) {                 // inclusive extra: J_0^T grad_h[0]
           float4* dst = reinterpret_cast<float4*>(grad_init + (long long)bsm * TH + 32 * cgp);
 #pragma unroll
           for (int k4 = 0; k4 < 8; ++k4) dst[k4] = make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+        }
+        if (add_e) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __fadd2_rn(v[i], ef[i]);
+        }
+        if (AFF && e_aff != nullptr) {
+          // e is outside the step's bound G M 2^-(s+sw): the scale of x^ comes
+          // from the exact row maximum of v + e instead (two threads per row)
+          float pv = 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pv = fmaxf(pv, fmaxf(fabsf(v[i].x), fabsf(v[i].y)));
+          const uint32_t xp = xred0 + xpar * (TM * 8);
+          asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(xp + 4u * cgp), "r"(__float_as_uint(pv)) : "memory");
+          named_bar(7 + g, W_EPI);
+          uint32_t m2[2];
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(xp) : "memory");
+          const int eMv = (int)(max(m2[0], m2[1]) >> 23) - 127;
+          s_cur = max(-127 - sw, min(126 - sw, 14 - eMv));
+          xpar ^= 1;
+        }
+        if (vonly && valid && st == len) {                  // the block's vector part (a short block)
+          float* dst = vec_out + ((long long)bsm * nblk + q) * TH;
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4)
+            reinterpret_cast<float4*>(dst + 32 * cgp)[k4] =
+                make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+          if (head && head_out != nullptr) {
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4)
+              reinterpret_cast<float4*>(head_out + (long long)bsm * head_bstride + 32 * cgp)[k4] =
+                  make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+          }
         }
       }
       WTRACE(2);
@@ -1517,7 +1574,8 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
       if (issuer) {
         tc_fence_after();
         mma8_f16_commit(slot_base, bdesc, dbar);
-        issue_stores(st, gs);
+        if (!vonly) issue_stores(st, gs);
+        else asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         if (st + 2 < C) {
           // stage (gs+2) % 3 was stored from at step st-1: its reads must be done
           asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
@@ -1547,12 +1605,26 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
     {
       float2 t[16];
       load_d_sum<32>(t_d1, t_d2, t);
-      if (total && len == C) {
+      if ((total || vonly) && valid && len == C) {
         const float f = __int_as_float((127 - s_prev - sw) << 23);
-        float4* dst = reinterpret_cast<float4*>(grad_init + (long long)bsm * TH + 32 * cgp);
+        float2 ef[16];
+        const bool add_e = AFF && vonly && e_aff != nullptr && s1 < S;   // the last element's e_{t-1}
+        if (add_e) load_e(s1, ef);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          t[i] = __fmul2_rn(t[i], make_float2(f, f));
+          if (add_e) t[i] = __fadd2_rn(t[i], ef[i]);
+        }
+        float* dst = vonly ? vec_out + ((long long)bsm * nblk + q) * TH : grad_init + (long long)bsm * TH;
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4)
-          dst[k4] = make_float4(t[2 * k4].x * f, t[2 * k4].y * f, t[2 * k4 + 1].x * f, t[2 * k4 + 1].y * f);
+          reinterpret_cast<float4*>(dst + 32 * cgp)[k4] = make_float4(t[2 * k4].x, t[2 * k4].y, t[2 * k4 + 1].x, t[2 * k4 + 1].y);
+        if (vonly && head && head_out != nullptr) {
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4)
+            reinterpret_cast<float4*>(head_out + (long long)bsm * head_bstride + 32 * cgp)[k4] =
+                make_float4(t[2 * k4].x, t[2 * k4].y, t[2 * k4 + 1].x, t[2 * k4 + 1].y);
+        }
       }
     }
   }
@@ -1660,8 +1732,13 @@ static cudaError_t make_walk_map(const float* base, int T, int B, int C, long lo
 // Level-0 down-walk of an RNN H = 64 segment on the tensor cores: the 3xFP16
 // walk with per-run TMA loads (B <= 128), else the 3xTF32 per-row walk.
 cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
-                                float* grad_init, int num_sms, cudaStream_t st) {
-  if (a.seg.B <= TM && !std::getenv("BPPSA_WALK_TF32")) {
+                                float* grad_init, int num_sms, cudaStream_t st, const float* e_aff, float* vec_out,
+                                float* head_out, long long head_bstride) {
+  if (e_aff != nullptr || vec_out != nullptr) {    // affine terms: the TMA walk only
+    if (a.seg.B > TM) return cudaErrorNotSupported;
+    if (grad_h == nullptr) grad_h = const_cast<float*>(a.h);   // vector parts store no grad_h (maps unused)
+  }
+  if (a.seg.B <= TM && (e_aff != nullptr || vec_out != nullptr || !std::getenv("BPPSA_WALK_TF32"))) {
     const int B = a.seg.B, G = TM / B;
     const long long Tm = (long long)a.seg.T - 1 + a.seg.head;
     CUtensorMap maps[4];
@@ -1672,14 +1749,18 @@ cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, lo
     const long long A = Tm / C, nfull = A > 1 ? (A - 1) / G : 0, rem0 = 1 + nfull * G;
     const long long nt = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
     const int gridw = (int)std::min<long long>((nt + 1) / 2, num_sms);
-    static bool attrw = false;
-    if (!attrw) {
-      e = cudaFuncSetAttribute(tc_leaf_down_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
+    const bool aff = e_aff != nullptr || vec_out != nullptr;
+    static bool attrw[2] = {false, false};
+    if (!attrw[aff]) {
+      e = cudaFuncSetAttribute(aff ? tc_leaf_down_f16_kernel<true> : tc_leaf_down_f16_kernel<false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
       if (e != cudaSuccess) return e;
-      attrw = true;
+      attrw[aff] = true;
     }
-    tc_leaf_down_f16_kernel<<<gridw, W_NT, W_SMEM_BYTES, st>>>(a, maps[0], maps[1], maps[2], maps[3], C, carry, nblk,
-                                                               grad_h, grad_init, G);
+    auto kern = aff ? tc_leaf_down_f16_kernel<true> : tc_leaf_down_f16_kernel<false>;
+    kern<<<gridw, W_NT, W_SMEM_BYTES, st>>>(a, maps[0], maps[1], maps[2], maps[3], C, carry, nblk,
+                                           vec_out ? nullptr : grad_h, vec_out ? nullptr : grad_init, G, e_aff,
+                                           vec_out, head_out, head_bstride);
     return cudaGetLastError();
   }
   const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
