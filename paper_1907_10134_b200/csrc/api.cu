@@ -16,7 +16,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 
@@ -29,6 +32,19 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 bppsa_status fail(bppsa_status s, const std::string& msg) {
   g_last_error = msg;
   return s;
+}
+
+cudaError_t smem_attr_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kernel, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev});
+  return e;
 }
 
 bppsa_status cuda_status(cudaError_t e, const char* where) {

@@ -18,6 +18,11 @@ void set_error(const std::string& msg);
 bppsa_status fail(bppsa_status s, const std::string& msg);
 bppsa_status cuda_status(cudaError_t e, const char* where);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device context, so a process that drives several GPUs
+// (or switches device) must set it on each.  Thread-safe.
+cudaError_t smem_attr_once(const void* kernel, int bytes);
+
 #define BPPSA_CHECK_LAUNCH(where)                                         \
   do {                                                                    \
     cudaError_t _e = cudaGetLastError();                                  \

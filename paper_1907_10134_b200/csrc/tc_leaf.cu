@@ -1657,34 +1657,19 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
     const long long ntg = (ngroups + TM / a.seg.H - 1) / (TM / a.seg.H);
     const int gridg = (int)std::min<long long>((ntg + 1) / 2, num_sms);
     if (gridg <= 0) return cudaSuccess;
-    static bool attrg = false;
-    if (!attrg) {
-      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           F_SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-      attrg = true;
-    }
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_up_f16g_kernel), F_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     tc_leaf_up_f16g_kernel<<<gridg, 512, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
     return cudaGetLastError();
   }
   if (prec == 0) {                                 // 3xFP16, 8 epilogue warps per slot
-    static bool attrf = false;
-    if (!attrf) {
-      cudaError_t e = cudaFuncSetAttribute(tc_leaf_up_f16_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           F_SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-      attrf = true;
-    }
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_up_f16_kernel<8>), F_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     tc_leaf_up_f16_kernel<8><<<grid, 64 * 8, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
     return cudaGetLastError();
   }
-  static bool attr16 = false;
-  if (!attr16) {
-    cudaError_t e = cudaFuncSetAttribute(tc_leaf_up16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES16);
-    if (e != cudaSuccess) return e;
-    attr16 = true;
-  }
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_up16_kernel), SMEM_BYTES16);
+  if (e != cudaSuccess) return e;
   tc_leaf_up16_kernel<<<grid, NTHREADS16, SMEM_BYTES16, st>>>(a, C, agg_out, n_out, q0);
   return cudaGetLastError();
 }
@@ -1750,14 +1735,9 @@ cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, lo
     const long long nt = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
     const int gridw = (int)std::min<long long>((nt + 1) / 2, num_sms);
     const bool aff = e_aff != nullptr || vec_out != nullptr;
-    static bool attrw[2] = {false, false};
-    if (!attrw[aff]) {
-      e = cudaFuncSetAttribute(aff ? tc_leaf_down_f16_kernel<true> : tc_leaf_down_f16_kernel<false>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, W_SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-      attrw[aff] = true;
-    }
     auto kern = aff ? tc_leaf_down_f16_kernel<true> : tc_leaf_down_f16_kernel<false>;
+    e = smem_attr_once(reinterpret_cast<const void*>(kern), W_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     kern<<<gridw, W_NT, W_SMEM_BYTES, st>>>(a, maps[0], maps[1], maps[2], maps[3], C, carry, nblk,
                                            vec_out ? nullptr : grad_h, vec_out ? nullptr : grad_init, G, e_aff,
                                            vec_out, head_out, head_bstride);
@@ -1765,13 +1745,8 @@ cudaError_t launch_tc_leaf_down(const LeafArgs& a, int C, const float* carry, lo
   }
   const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
   const int grid = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
-  static bool attr16 = false;
-  if (!attr16) {
-    cudaError_t e = cudaFuncSetAttribute(tc_leaf_down16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES_D16);
-    if (e != cudaSuccess) return e;
-    attr16 = true;
-  }
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_down16_kernel), SMEM_BYTES_D16);
+  if (e != cudaSuccess) return e;
   tc_leaf_down16_kernel<<<grid, NTHREADS16, SMEM_BYTES_D16, st>>>(a, C, carry, nblk, grad_h, grad_init);
   return cudaGetLastError();
 }

@@ -424,12 +424,8 @@ bool tc_wgrad_applies(int H_, int I, long long rows) {
 
 cudaError_t launch_tc_wgrad_partials(int B, int I, const float* x, const float* h, const float* h_init,
                                      const float* grad_h, long long rows, float* ws, int num_sms, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_wgrad_kernel), SMEM);
+  if (e != cudaSuccess) return e;
   TWArgs a{B, I, x, h, h_init, grad_h, rows, ws, (rows + PART_ROWS - 1) / PART_ROWS};
   const int grid = (int)std::min<long long>(a.nparts, num_sms);
   tc_wgrad_kernel<<<grid, NTH, SMEM, st>>>(a);
