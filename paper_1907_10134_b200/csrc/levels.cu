@@ -57,15 +57,17 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
                                                                        long long n_out) {
   using Tl = Tile<HP, TM, TN>;
   extern __shared__ __align__(16) float smem[];
-  float* Ab[2] = {smem, smem + HP * HP};
-  float* Pb[2] = {smem + 2 * HP * HP, smem + 3 * HP * HP};
+  // one A buffer (the next A_s waits in registers) and two P buffers: 48 KB
+  // at H = 64, so four CTAs fit an SM (64 KB with two A buffers allowed three)
+  float* Ab[1] = {smem};
+  float* Pb[2] = {smem + HP * HP, smem + 2 * HP * HP};
   const int tid = threadIdx.x;
   const long long q = blockIdx.x;
   const int b = blockIdx.y;
   const long long s0 = q * C, s1 = min(s0 + (long long)C, n);
   const bool vec = head && q == 0;
   const int HH = H * H;
-  for (int e = tid; e < 4 * HP * HP; e += Tl::NT) smem[e] = 0.f;
+  for (int e = tid; e < 3 * HP * HP; e += Tl::NT) smem[e] = 0.f;
   __syncthreads();
   long long s;
   if (vec) {
@@ -80,7 +82,8 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
     }
     s = s0 + 1;
   }
-  int pc = 0, ac = 0;
+  int pc = 0;
+  constexpr int ac = 0;
   if (HP == 64 && H == 64 && Tl::NT == 256) {
     // H = 64: the next A_s (16 KB, column-major = A[k][i] rows of 64) is
     // prefetched as four coalesced float4 per thread (scalar loads made this
@@ -101,8 +104,8 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
       }
       __syncthreads();
       gemm_step<HP, TM, TN>(Ab[ac], Pb[pc], Pb[pc ^ 1], tid);
+      __syncthreads();                            // A is rewritten next step
       pc ^= 1;
-      ac ^= 1;
     }
   } else {
     float pre[Tl::PER];
@@ -130,8 +133,8 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
       }
       __syncthreads();
       gemm_step<HP, TM, TN>(Ab[ac], Pb[pc], Pb[pc ^ 1], tid);
+      __syncthreads();                            // A is rewritten next step
       pc ^= 1;
-      ac ^= 1;
     }
   }
   __syncthreads();
@@ -290,7 +293,7 @@ template <int HP, int TM, int TN>
 cudaError_t fold_impl(const MatAcc& A, int H, int B, long long n, int C, int head, float* agg_out,
                       long long n_out, cudaStream_t st) {
   using Tl = Tile<HP, TM, TN>;
-  const size_t smem = 4ull * HP * HP * sizeof(float);
+  const size_t smem = 3ull * HP * HP * sizeof(float);
   auto k = fold_up_kernel<HP, TM, TN>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -15,7 +15,9 @@ CFG = {"c4": (1 << 20, 16, 64, 128, 32), "c1": (1000, 16, 20, 8, 8), "c2": (3000
        "c4s": (1 << 18, 16, 64, 128, 32), "c4b128": (1 << 20, 16, 64, 128, 32), "c4b128c64": (1 << 20, 16, 64, 128, 64),
        "c4c64": (1 << 20, 16, 64, 64, 64), "c4b256": (1 << 20, 16, 64, 256, 32), "c4b512": (1 << 20, 16, 64, 512, 32),
        "c4b256c64": (1 << 20, 16, 64, 256, 64), "c4b512c16": (1 << 20, 16, 64, 512, 16),
-       "c4b512c64": (1 << 20, 16, 64, 512, 64), "c4b384": (1 << 20, 16, 64, 384, 32)}
+       "c4b512c64": (1 << 20, 16, 64, 512, 64), "c4b384": (1 << 20, 16, 64, 384, 32),
+       "c4b1024": (1 << 20, 16, 64, 1024, 32), "c4b1024c16": (1 << 20, 16, 64, 1024, 16),
+       "c4b768": (1 << 20, 16, 64, 768, 32)}
 
 
 def run(name, reps=5):
