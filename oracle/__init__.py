@@ -12,11 +12,13 @@ The product path (paper_1907_10134_b200) never imports it.
 Modules
   bp    — definitions: sequential BP (eqn:backprop) for the tanh RNN
           and the GRU, leaf transposed Jacobians (eqn:rnn, eqn:gru_jcb), the
-          fp64 forward and loss used by the finite-difference pins, and the
-          parameter gradients of eqn:update_param.
+          fp64 forward and loss used by the finite-difference pins, the
+          parameter gradients of eqn:update_param, and the affine
+          recurrence of per-step losses (not in the paper).
   scan  — the operator A<>B = BA, the exclusive scan definition
           (eqn:scan_input), Alg. 1 executed literally,
-          the level-balanced hybrid scan, and the contiguous-shard
+          the level-balanced hybrid scan, its per-step static FLOP
+          analysis (fig:prune_symbolic), and the contiguous-shard
           emulation of the multi-GPU carry protocol.
   csr   — CSR matrices, the analytical transposed-Jacobian builders of
           Algs. 2-10, the exact guaranteed-zero stencil pattern,
