@@ -587,6 +587,30 @@ def sweep_train():
             res[tag] = round(e0.elapsed_time(e1) / 10, 4)
         res["speedup"] = round(res["autograd_iter_ms"] / res["bppsa_iter_ms"], 2)
         out[name] = {"T": T, "B": B, "H": H, **res}
+    # config 3: GRU on the IRMAS-shaped L set (F = 1034, C = 12), B = 64, lr 3e-4;
+    # the BPPSA iteration includes the gate recompute "FO"
+    from paper_1907_10134_b200.train import BppsaGruTrainer, IrmasGru
+    torch.manual_seed(0)
+    ma = IrmasGru(12).cuda()
+    mb = copy.deepcopy(ma)
+    mb.rnn.flatten_parameters()
+    ta, tb = BppsaGruTrainer(ma, lr=3e-4, block0=16, block=16), AutogradTrainer(mb, lr=3e-4)
+    x, y = W.irmas_like(1034, 12, 64, 7)
+    x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    res = {}
+    for tag, tr in (("bppsa_iter_ms", ta), ("autograd_iter_ms", tb)):
+        for _ in range(3):
+            tr.step(x, y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            tr.step(x, y)
+        e1.record()
+        torch.cuda.synchronize()
+        res[tag] = round(e0.elapsed_time(e1) / 10, 4)
+    res["speedup"] = round(res["autograd_iter_ms"] / res["bppsa_iter_ms"], 2)
+    out["c3_gru"] = {"F": 1034, "C": 12, "B": 64, "H": 20, **res}
     return out
 
 

@@ -95,6 +95,24 @@ bppsa_status bppsa_jacobians_gru(int T, int B, int H, const float* h_prev,
                                  const float* M, const float* W_hh3,
                                  float* JT_out, bppsa_jac* desc, void* stream);
 
+/* GRU forward overhead "FO" (DESIGN reading 10): a forward
+ * that hides its gates (cuDNN) leaves only h; this recomputes the tape the
+ * GRU leaf needs from x [T][B][I], h [T][B][H] (= h_0..h_{T-1}), h_init
+ * [B][H] (nullable => 0) and torch's GRU parameters W_ih3 [3H][I], W_hh3
+ * [3H][H], b_ih3, b_hh3 [3H] (gate order r, z, n), eqn:gru:
+ *   h_prev[t] = h[t-1] (h_init at t = 0), r = sigma(W_ir x + b_ir + W_hr
+ *   h_prev + b_hr), z = sigma(W_iz x + b_iz + W_hz h_prev + b_hz),
+ *   M = W_hn h_prev + b_hn, n = tanh(W_in x + b_in + r M);
+ * outputs [T][B][H] each (device, caller-owned).  No recurrence: every
+ * (t, b) row at once, fp32 (expf / tanhf, no fast math).  1 <= H <= 32,
+ * 1 <= I <= 64 (else BPPSA_ERR_NOT_SUPPORTED).                              */
+bppsa_status bppsa_gru_gates(int T, int B, int H, int I, const float* x,
+                             const float* h, const float* h_init,
+                             const float* W_ih3, const float* W_hh3,
+                             const float* b_ih3, const float* b_hh3,
+                             float* h_prev, float* r, float* z, float* n,
+                             float* M, void* stream);
+
 /* ---------------------------------------------------------------------------
  * The scan (Alg. 1).
  * ------------------------------------------------------------------------- */

@@ -247,3 +247,24 @@ def gru_forward64(x, p, h0=None, t_start=0, h_start=None):
         h = (1 - z) * n + z * h
         tape["r"][t], tape["z"][t], tape["n"][t], tape["M"][t], tape["h"][t] = r, z, n, M, h
     return tape
+
+
+def gru_gates64(x, h, p, h_init=None):
+    """The GRU 'forward overhead' (FO; reading 10): the tape of
+    P:826-831 recomputed from given h_0..h_{T-1} — eqn:gru's gate formulas at
+    h_prev[t] = h[t-1] (h_init, default 0, at t = 0), no recurrence."""
+    x, h = _d(x), _d(h)
+    T, B, _ = x.shape
+    Wih, Whh = _d(p["W_ih3"]), _d(p["W_hh3"])
+    bih, bhh = _d(p["b_ih3"]), _d(p["b_hh3"])
+    H = Whh.shape[1]
+    hp = np.concatenate([(np.zeros((1, B, H), D) if h_init is None else _d(h_init)[None]), h[:-1]], axis=0)
+    gi = x @ Wih.T + bih
+    gh = hp @ Whh.T + bhh
+    sig = lambda v: 1.0 / (1.0 + np.exp(-v))
+    r = sig(gi[..., :H] + gh[..., :H])
+    z = sig(gi[..., H:2 * H] + gh[..., H:2 * H])
+    M = gh[..., 2 * H:]
+    n = np.tanh(gi[..., 2 * H:] + r * M)
+    return {"h_prev": hp, "r": r, "z": z, "n": n, "M": M}
+

@@ -43,6 +43,7 @@ EXPORTS = {
     "bppsa_jacobians_gru": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_Jac), _vp]),
     "bppsa_scan_workspace_size": (_i, [C.POINTER(_Jac), C.POINTER(_Opts), C.POINTER(_sz)]),
     "bppsa_scan": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_gru_gates": (_i, [_i, _i, _i, _i] + [_vp] * 12 + [_vp]),
     "bppsa_scan_affine": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_scan_shard_up": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_scan_shard_down": (_i, [C.POINTER(_Jac), _vp, _vp, _i, _i, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
@@ -226,6 +227,20 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
                            _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
                            _stream(stream)), "bppsa_scan")
     return grad_h, grad_h_init
+
+
+def gru_gates(x: torch.Tensor, h: torch.Tensor, W_ih3: torch.Tensor, W_hh3: torch.Tensor, b_ih3: torch.Tensor,
+              b_hh3: torch.Tensor, h_init: torch.Tensor | None = None, out=None, stream=None) -> dict:
+    """bppsa_gru_gates (FO): the GRU tape {h_prev, r, z, n, M} recomputed from x and h."""
+    T, B, I = x.shape
+    H = h.shape[2]
+    if out is None:
+        out = {k: torch.empty((T, B, H), dtype=torch.float32, device=h.device) for k in ("h_prev", "r", "z", "n", "M")}
+    _check(_lib.bppsa_gru_gates(T, B, H, I, _ptr(x, "x"), _ptr(h, "h"), _ptr(h_init, "h_init"), _ptr(W_ih3, "W_ih3"),
+                                _ptr(W_hh3, "W_hh3"), _ptr(b_ih3, "b_ih3"), _ptr(b_hh3, "b_hh3"),
+                                *[_ptr(out[k], k) for k in ("h_prev", "r", "z", "n", "M")], _stream(stream)),
+           "bppsa_gru_gates")
+    return out
 
 
 def scan_affine(jac: Jacobians, seed: torch.Tensor, e: torch.Tensor, grad_h: torch.Tensor | None = None,

@@ -17,7 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
-#include <set>
+#include <map>
 #include <string>
 #include <utility>
 
@@ -35,15 +35,19 @@ bppsa_status fail(bppsa_status s, const std::string& msg) {
 }
 
 cudaError_t smem_attr_once(const void* kernel, int bytes) {
+  // the default allows 48 KB; never LOWER a limit set earlier (a smaller value
+  // would make later, larger launches of the same kernel fail)
+  if (bytes <= 48 * 1024) return cudaSuccess;
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, int> done;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(mu);
-  if (done.count({kernel, dev})) return cudaSuccess;
+  auto it = done.find({kernel, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done.insert({kernel, dev});
+  if (e == cudaSuccess) done[{kernel, dev}] = bytes;
   return e;
 }
 
@@ -504,6 +508,29 @@ bppsa_status bppsa_jacobians_gru(int T, int B, int H, const float* h_prev, const
   if (s != BPPSA_OK) return s;
   *desc = j;
   return BPPSA_OK;
+}
+
+bppsa_status bppsa_gru_gates(int T, int B, int H, int I, const float* x, const float* h, const float* h_init,
+                             const float* W_ih3, const float* W_hh3, const float* b_ih3, const float* b_hh3,
+                             float* h_prev, float* r, float* z, float* n, float* M, void* stream) {
+  if (T < 1 || B < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "T and B must be >= 1");
+  if (H < 1 || H > 32 || I < 1 || I > 64)
+    return fail(BPPSA_ERR_NOT_SUPPORTED, "GRU gate recompute: 1 <= H <= 32, 1 <= I <= 64");
+  REQUIRE_DEV(x, "x");
+  REQUIRE_DEV(h, "h");
+  if (h_init) REQUIRE_DEV(h_init, "h_init");
+  REQUIRE_DEV(W_ih3, "W_ih3");
+  REQUIRE_DEV(W_hh3, "W_hh3");
+  REQUIRE_DEV(b_ih3, "b_ih3");
+  REQUIRE_DEV(b_hh3, "b_hh3");
+  REQUIRE_DEV(h_prev, "h_prev");
+  REQUIRE_DEV(r, "r");
+  REQUIRE_DEV(z, "z");
+  REQUIRE_DEV(n, "n");
+  REQUIRE_DEV(M, "M");
+  cudaError_t e = launch_gru_gates(T, B, H, I, x, h, h_init, W_ih3, W_hh3, b_ih3, b_hh3, h_prev, r, z, n, M,
+                                   num_sms(), (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "gru gates launch");
 }
 
 bppsa_status bppsa_scan_workspace_size(const bppsa_jac* jac, const bppsa_scan_opts* opts, size_t* bytes) {

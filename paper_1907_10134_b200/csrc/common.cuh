@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../include/bppsa.h"
@@ -128,6 +129,11 @@ cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, 
 // dst[b][i] = seed[b][i] + e[T-1][b][i] (the affine head, reading 8)
 cudaError_t launch_affine_seed(const float* seed, const float* e, int T, int B, int H, float* dst,
                                cudaStream_t st);
+
+// GRU forward overhead (FO): the tape from (x, h) (gates.cu)
+cudaError_t launch_gru_gates(int T, int B, int H, int I, const float* x, const float* h, const float* h_init,
+                             const float* Wih, const float* Whh, const float* bih, const float* bhh, float* hp,
+                             float* r, float* z, float* n, float* M, int num_sms, cudaStream_t st);
 
 // DENSE helpers
 cudaError_t launch_transpose_dense(const float* JT, float* JTc, long long mats, int H,

@@ -79,6 +79,63 @@ class BppsaTrainer:
         return float(loss.detach())
 
 
+class IrmasGru(torch.nn.Module):
+    """The paper's GRU model: nn.GRU(C, H) + Linear(H, classes)
+    on the last hidden state (H = 20, 11 classes: reading 21)."""
+
+    def __init__(self, C: int, H: int = 20, classes: int = 11):
+        super().__init__()
+        self.rnn = torch.nn.GRU(C, H)
+        self.head = torch.nn.Linear(H, classes)
+
+    def forward(self, x):
+        h, _ = self.rnn(x)
+        return h, self.head(h[-1])
+
+
+class BppsaGruTrainer:
+    """GRU training with the BPPSA backward: cuDNN forward (gates hidden), the
+    gate recompute "FO" (bppsa_gru_gates), the eqn:gru_jcb leaves,
+    the scan, the GRU weight gradients, Adam (lr 3e-4 in the paper's runs)."""
+
+    def __init__(self, model: IrmasGru, lr: float, block0: int = 0, block: int = 0):
+        self.model, self.block0, self.block = model, block0, block
+        self.opt = torch.optim.Adam(model.parameters(), lr=lr)
+        self._shape = None
+
+    def step(self, x: torch.Tensor, labels: torch.Tensor) -> float:
+        m = self.model
+        T, B, I = x.shape
+        H = m.rnn.hidden_size
+        if self._shape != (T, B, H, I):
+            self.grad = torch.empty((T, B, H), device=x.device)
+            self.ws_w = api.workspace(api.weight_grads_workspace_size(T, B, H, I), x.device)
+            self.ws = None
+            self._shape = (T, B, H, I)
+        self.opt.zero_grad(set_to_none=True)
+        with torch.no_grad():
+            h, _ = m.rnn(x)
+        h = h.contiguous()
+        hl = h[-1].detach().requires_grad_(True)
+        loss = torch.nn.functional.cross_entropy(m.head(hl), labels)
+        loss.backward()
+        seed = hl.grad.contiguous()
+        r = m.rnn
+        W_hh3 = r.weight_hh_l0.detach().contiguous()
+        xc = x.contiguous()
+        tape = api.gru_gates(xc, h, r.weight_ih_l0.detach().contiguous(), W_hh3, r.bias_ih_l0.detach().contiguous(),
+                             r.bias_hh_l0.detach().contiguous())
+        jac = api.jacobians_gru(tape["h_prev"], tape["r"], tape["z"], tape["n"], tape["M"], W_hh3)
+        if self.ws is None:
+            self.ws = api.workspace(api.scan_workspace_size(jac, "blocked", self.block0, self.block), x.device)
+        api.scan(jac, seed, grad_h=self.grad, ws=self.ws, block0=self.block0, block=self.block)
+        dWih, dWhh, dbih, dbhh = api.weight_grads_gru(xc, tape, self.grad, ws=self.ws_w)
+        r.weight_ih_l0.grad, r.weight_hh_l0.grad = dWih, dWhh
+        r.bias_ih_l0.grad, r.bias_hh_l0.grad = dbih, dbhh
+        self.opt.step()
+        return float(loss.detach())
+
+
 class AutogradTrainer:
     """The baseline: the same iteration with torch's backward (cuDNN)."""
 

@@ -62,3 +62,61 @@ def test_bppsa_gradients_equal_autograd(lib):
     for n, g in got.items():
         r = ref[n]
         assert (g - r).abs().max().item() <= 1e-4 * r.abs().max().item(), n
+
+
+# ------------------------------------------------------------------ GRU (FO + BPPSA backward)
+def test_gru_gates_recompute_vs_oracle(lib):
+    """bppsa_gru_gates (FO) against the oracle's gru_gates64 on the same
+    fp32 h (gates are O(1): 1e-5 absolute)."""
+    from oracle import bp
+    from paper_1907_10134_b200 import api
+    gw = W.gru_workload("M", 16, seed=4)
+    p, tape = gw.params, gw.tape
+    h0 = np.random.default_rng(1).standard_normal((16, 20)).astype(np.float32) * 0.2
+    for hi in (None, h0):
+        ref = bp.gru_gates64(gw.x, tape["h"], p, h_init=hi)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        got = api.gru_gates(cu(gw.x), cu(tape["h"]), cu(p["W_ih3"]), cu(p["W_hh3"]), cu(p["b_ih3"]), cu(p["b_hh3"]),
+                            h_init=None if hi is None else cu(hi))
+        torch.cuda.synchronize()
+        for k in ("h_prev", "r", "z", "n", "M"):
+            assert np.abs(got[k].cpu().numpy() - ref[k]).max() < 1e-5, k
+
+
+@pytest.mark.parametrize("F,C,B", [(259, 38, 16), (1034, 12, 64)])
+def test_gru_bppsa_gradients_equal_autograd(lib, F, C, B):
+    """cuDNN GRU forward + FO + BPPSA backward: every GRU parameter gradient
+    within 1e-4 (max-norm relative) of torch autograd's."""
+    from paper_1907_10134_b200.train import BppsaGruTrainer, IrmasGru
+    torch.backends.cudnn.allow_tf32 = False
+    torch.manual_seed(7)
+    m = IrmasGru(C).cuda()
+    x, y = W.irmas_like(F, C, B, 3)
+    x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    _, logits = m(x)
+    torch.nn.functional.cross_entropy(logits, y).backward()
+    ref = {n: p.grad.clone() for n, p in m.rnn.named_parameters()}
+    t = BppsaGruTrainer(m, lr=0.0)
+    t.step(x, y)
+    for n, p in m.rnn.named_parameters():
+        e = ((p.grad - ref[n]).abs().max() / ref[n].abs().max()).item()
+        assert e <= 1e-4, (n, e)
+
+
+def test_gru_bppsa_training_matches_autograd(lib):
+    from paper_1907_10134_b200.train import AutogradTrainer, BppsaGruTrainer, IrmasGru
+    torch.backends.cudnn.allow_tf32 = False
+    torch.manual_seed(0)
+    ma = IrmasGru(24).cuda()
+    mb = copy.deepcopy(ma)
+    mb.rnn.flatten_parameters()
+    ta, tb = BppsaGruTrainer(ma, lr=3e-4), AutogradTrainer(mb, lr=3e-4)
+    la, lb = [], []
+    for it in range(20):
+        x, y = W.irmas_like(517, 24, 16, 50 + it)
+        x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        la.append(ta.step(x, y))
+        lb.append(tb.step(x, y))
+    la, lb = np.array(la), np.array(lb)
+    assert abs(la[0] - lb[0]) <= 1e-6 * abs(lb[0])
+    assert np.abs(la - lb).max() <= 1e-3 * np.abs(lb).max(), (la, lb)

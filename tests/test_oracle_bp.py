@@ -331,3 +331,17 @@ def test_generator_forward_matches_fp64_forward():
     t64 = bp.gru_forward64(gw.x, gw.params)
     for k in ("h_prev", "r", "z", "n", "M", "h"):
         assert np.abs(t64[k] - gw.tape[k]).max() < 1e-4
+
+
+def test_gru_gates_recompute_equals_the_forward_tape():
+    """FO (reading 10): the gates recomputed from the forward's own h equal the
+    tape the sequential fp64 forward recorded (gru_forward64, itself pinned by
+    torch.autograd above), with and without h_init."""
+    T, B, H, C = 30, 3, 20, 12
+    p = _gru_params64(H, C, 11, RNG)
+    x = RNG.standard_normal((T, B, C))
+    for h0 in (None, RNG.standard_normal((B, H)) * 0.3):
+        tape = bp.gru_forward64(x, p, h0=h0)
+        g = bp.gru_gates64(x, tape["h"], p, h_init=h0)
+        for k in ("h_prev", "r", "z", "n", "M"):
+            assert np.abs(g[k] - tape[k]).max() < 1e-14, k
