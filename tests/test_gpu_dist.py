@@ -1,0 +1,71 @@
+"""The multi-rank CUDA path of dist.py (CudaShardBackend + sharded_scan, the
+bench's N > 1 step) on ONE GPU: two processes share cuda:0 and talk over gloo
+(NCCL refuses two ranks on one device).  Exercises bppsa_scan_shard_up /
+_down with real device tensors, the all-gather of aggregates and the carry
+combine, and the weight-gradient all-reduce, against the fp64 oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, T, B, H, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bppsa_workloads as W
+        from paper_1907_10134_b200 import api
+        from paper_1907_10134_b200.dist import CudaShardBackend, shard_bounds, sharded_scan
+        w = W.rnn_workload(T, B, H, seed=21)
+        lo, hi = shard_bounds(T, world)[rank]
+        h = torch.from_numpy(w.h[lo:hi]).cuda()
+        x = torch.from_numpy(w.x[lo:hi]).cuda()
+        jac = api.jacobians_rnn(h, torch.from_numpy(w.W_hh).cuda())
+        be = CudaShardBackend(jac, 512, 32)
+        seed = torch.from_numpy(w.g).cuda() if rank == world - 1 else None
+        grad, init = sharded_scan(be, seed, want_init=(rank == 0))
+        h_init = torch.from_numpy(w.h[lo - 1]).cuda() if lo > 0 else None
+        dWih, dWhh, db = api.weight_grads_rnn(x, h, grad, h_init=h_init)
+        for t in (dWih, dWhh, db):
+            dist.all_reduce(t)
+        torch.cuda.synchronize()
+        parts = [None] * world
+        dist.all_gather_object(parts, (lo, grad.cpu().numpy(), None if init is None else init.cpu().numpy()))
+        if rank == 0:
+            from oracle import bp
+            ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+            got = np.concatenate([p[1] for p in sorted(parts, key=lambda p: p[0])])
+            s = np.abs(ref).max()
+            rw = bp.weight_grads_rnn(w.x, w.h, ref)
+            ew = max(float(np.abs(a.cpu().numpy() - b).max() / np.abs(b).max()) for a, b in zip((dWih, dWhh, db), rw))
+            q.put((float(np.abs(got - ref).max() / s), float(np.abs(parts[0][2] - ref_init).max() / s), ew))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cuda_path_one_gpu(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 30000, 16, 64, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    e_grad, e_init, e_w = q.get(timeout=5)
+    assert e_grad <= 1e-4 and e_init <= 1e-4 and e_w <= 1e-4, (e_grad, e_init, e_w)
