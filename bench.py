@@ -35,6 +35,15 @@ sys.path.insert(0, ROOT)
 METRIC = "BPPSA backward ms vs sequential BP (1/2/4/8 GPU); % HBM/tensor roofline"
 C4 = dict(T=1 << 20, B=16, H=64, I=1)
 C4_BLOCK0, C4_BLOCK = 512, 32
+
+
+def c4_block0(world: int) -> int:
+    """Level-0 block per rank for time shards of 2^20 / world steps: the walk's
+    time is ~block0 dependent steps (its tiles fit one wave), the level-1 fold
+    scales with the number of blocks, so the block shrinks as the shard does
+    (a model of the single-GPU kernel times, DESIGN "Multi-GPU"; 512 at N = 1
+    is measured)."""
+    return {1: 512, 2: 256, 4: 256}.get(world, 128)
 SMALL = {   # secondary configs (N = 1 sweep): (T, B, H, block0, block)
     "c1": dict(T=1000, B=16, H=20, block0=8, block=8),
     "c2": dict(T=30000, B=16, H=20, block0=16, block=16),
@@ -184,7 +193,8 @@ def run_ours(args):
     grad = torch.empty((Tl, B, H), device=dev)
     wout = (torch.empty((H, I), device=dev), torch.empty((H, H), device=dev), torch.empty((H,), device=dev))
     ws_w = api.workspace(api.weight_grads_workspace_size(Tl, B, H, I), dev)
-    backend = CudaShardBackend(jac, C4_BLOCK0, C4_BLOCK) if world > 1 else None
+    b0 = c4_block0(world)
+    backend = CudaShardBackend(jac, b0, C4_BLOCK) if world > 1 else None
     ws = api.workspace(api.scan_workspace_size(jac, "blocked", C4_BLOCK0, C4_BLOCK), dev) if world == 1 else None
 
     def step(trace=None):
@@ -227,7 +237,7 @@ def run_ours(args):
                   launches=launches_scan + 2, clocks=clk.summary(), Tl=Tl, head=head)
     if rank == 0:
         pk = peaks()
-        flops = level0_flops(Tl, B, H, C4_BLOCK0, head)
+        flops = level0_flops(Tl, B, H, b0, head)
         achieved = flops / (k0m * 1e-3) / 1e12
         # the level-0 fold runs on tcgen05 as 3xFP16 (x = x1 + x2, W = W1 + W2 in
         # fp16 with power-of-two row scaling; kind::f16, fp32 accumulate): every
@@ -736,7 +746,7 @@ def main():
             "data": "synthetic (seeded bitstreams x~Bernoulli(0.05+0.1c), torch-default init, fp32 forward)",
             "config": {"workload": "C4: tanh RNN, H=64, B=16, T=1048576 — full backward (fused leaves + "
                                    "blocked Blelloch scan + weight grads)",
-                       "T": C4["T"], "B": C4["B"], "H": C4["H"], "block0": C4_BLOCK0, "block": C4_BLOCK,
+                       "T": C4["T"], "B": C4["B"], "H": C4["H"], "block0": c4_block0(world), "block": C4_BLOCK,
                        "parallelism": f"contiguous time shards x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (h = 4.3 GB, grad_h = 4.3 GB)"},
             "roofline": r["roofline"], "gpu_launches": r["launches"] * args.steps,
