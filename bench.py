@@ -195,13 +195,19 @@ def run_ours(args):
     ws_w = api.workspace(api.weight_grads_workspace_size(Tl, B, H, I), dev)
     b0 = c4_block0(world)
     backend = CudaShardBackend(jac, b0, C4_BLOCK) if world > 1 else None
+    # carry exchange: NCCL all-gather (default) or BPPSA_EXCHANGE=peer, the
+    # peer-memory mailboxes of bppsa_exchange_publish / _wait
+    exchange = None
+    if world > 1 and os.environ.get("BPPSA_EXCHANGE", "nccl") == "peer":
+        from paper_1907_10134_b200.dist import PeerExchange
+        exchange = PeerExchange(B, H)
     ws = api.workspace(api.scan_workspace_size(jac, "blocked", C4_BLOCK0, C4_BLOCK), dev) if world == 1 else None
 
     def step(trace=None):
         if world == 1:
             api.scan(jac, g, grad_h=grad, ws=ws, block0=C4_BLOCK0, block=C4_BLOCK, trace=trace)
         else:
-            sharded_scan(_Traced(backend, trace), g, grad_h=grad)
+            sharded_scan(_Traced(backend, trace), g, grad_h=grad, exchange=exchange)
         dWih, dWhh, db = api.weight_grads_rnn(x, h, grad, h_init=h_init, ws=ws_w, out=wout)
         if world > 1:
             for t_ in (dWih, dWhh, db):
@@ -747,7 +753,9 @@ def main():
             "config": {"workload": "C4: tanh RNN, H=64, B=16, T=1048576 — full backward (fused leaves + "
                                    "blocked Blelloch scan + weight grads)",
                        "T": C4["T"], "B": C4["B"], "H": C4["H"], "block0": c4_block0(world), "block": C4_BLOCK,
-                       "parallelism": f"contiguous time shards x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"contiguous time shards x{world}, "
+                                       f"{os.environ.get('BPPSA_EXCHANGE', 'nccl')} carry exchange")
+                                      if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (h = 4.3 GB, grad_h = 4.3 GB)"},
             "roofline": r["roofline"], "gpu_launches": r["launches"] * args.steps,
             "clocks": r["clocks"], "kernels_ms": [round(k, 4) for k in r["kernels_ms"]]}

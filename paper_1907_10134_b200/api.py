@@ -43,6 +43,8 @@ EXPORTS = {
     "bppsa_jacobians_gru": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_Jac), _vp]),
     "bppsa_scan_workspace_size": (_i, [C.POINTER(_Jac), C.POINTER(_Opts), C.POINTER(_sz)]),
     "bppsa_scan": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_exchange_publish": (_i, [_vp, C.c_longlong, _i, _i, _vp, _vp, _vp, C.c_uint, _vp]),
+    "bppsa_exchange_wait": (_i, [_vp, _i, _i, C.c_uint, _vp]),
     "bppsa_gru_gates": (_i, [_i, _i, _i, _i] + [_vp] * 12 + [_vp]),
     "bppsa_scan_affine": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_scan_shard_up": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
@@ -227,6 +229,19 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
                            _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
                            _stream(stream)), "bppsa_scan")
     return grad_h, grad_h_init
+
+
+def exchange_publish(aggregate: torch.Tensor, rank: int, world: int, peer_mailboxes: torch.Tensor,
+                     peer_flags: torch.Tensor, counter: torch.Tensor, epoch: int, stream=None):
+    """bppsa_exchange_publish: aggregate -> every rank's mailbox, then the flags
+    (peer_mailboxes / peer_flags: int64 device arrays of device pointers)."""
+    _check(_lib.bppsa_exchange_publish(_ptr(aggregate, "aggregate"), aggregate.numel(), rank, world,
+                                       peer_mailboxes.data_ptr(), peer_flags.data_ptr(), counter.data_ptr(),
+                                       epoch, _stream(stream)), "bppsa_exchange_publish")
+
+
+def exchange_wait(flags: torch.Tensor, rank: int, world: int, epoch: int, stream=None):
+    _check(_lib.bppsa_exchange_wait(flags.data_ptr(), rank, world, epoch, _stream(stream)), "bppsa_exchange_wait")
 
 
 def gru_gates(x: torch.Tensor, h: torch.Tensor, W_ih3: torch.Tensor, W_hh3: torch.Tensor, b_ih3: torch.Tensor,

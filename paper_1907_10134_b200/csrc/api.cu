@@ -702,6 +702,28 @@ bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed, cons
   return s;
 }
 
+bppsa_status bppsa_exchange_publish(const float* aggregate, long long n, int rank, int world,
+                                    float* const* peer_mailboxes, unsigned* const* peer_flags, unsigned* counter,
+                                    unsigned epoch, void* stream) {
+  if (n < 1 || world < 1 || rank < 0 || rank >= world || epoch == 0)
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "need n >= 1, 0 <= rank < world, epoch >= 1");
+  REQUIRE_DEV(aggregate, "aggregate");
+  REQUIRE_DEV(peer_mailboxes, "peer_mailboxes");
+  REQUIRE_DEV(peer_flags, "peer_flags");
+  REQUIRE_DEV(counter, "counter");
+  cudaError_t e = launch_exchange_publish(aggregate, n, rank, world, peer_mailboxes, peer_flags, counter, epoch,
+                                          num_sms(), (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "exchange publish");
+}
+
+bppsa_status bppsa_exchange_wait(const unsigned* flags, int rank, int world, unsigned epoch, void* stream) {
+  if (world < 1 || rank < 0 || rank >= world || epoch == 0)
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "need 0 <= rank < world, epoch >= 1");
+  REQUIRE_DEV(flags, "flags");
+  cudaError_t e = launch_exchange_wait(flags, rank, world, epoch, (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "exchange wait");
+}
+
 // A fixed function of the row count only (deterministic results): parts of
 // at least 64 rows, at most 16 CTAs per SM of partial tiles.
 static long long wgrad_parts(long long rows) {

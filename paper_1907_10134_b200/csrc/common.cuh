@@ -130,6 +130,12 @@ cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, 
 cudaError_t launch_affine_seed(const float* seed, const float* e, int T, int B, int H, float* dst,
                                cudaStream_t st);
 
+// peer-memory carry exchange (exchange.cu)
+cudaError_t launch_exchange_publish(const float* src, long long n, int rank, int world, float* const* peers,
+                                    unsigned* const* peer_flags, unsigned* counter, unsigned epoch, int num_sms,
+                                    cudaStream_t st);
+cudaError_t launch_exchange_wait(const unsigned* flags, int rank, int world, unsigned epoch, cudaStream_t st);
+
 // GRU forward overhead (FO): the tape from (x, h) (gates.cu)
 cudaError_t launch_gru_gates(int T, int B, int H, int I, const float* x, const float* h, const float* h_init,
                              const float* Wih, const float* Whh, const float* bih, const float* bhh, float* hp,

@@ -59,7 +59,53 @@ class CudaShardBackend:
         return grad_h, gi
 
 
-def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None):
+class PeerExchange:
+    """The carry exchange over peer memory (bppsa_exchange_publish / _wait)
+    instead of an NCCL all-gather: this rank's mailbox [2][world][B][H*H] and
+    flags [world] are mapped into every other rank with CUDA IPC (handles
+    swapped once through torch.distributed), so the up-sweep aggregate is
+    stored straight into every peer's memory over NVLink and the down-sweep
+    waits on the flags of the later ranks only.  One instance per (rank,
+    shape); every call of `exchange` is a new epoch."""
+
+    def __init__(self, B: int, H: int, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        from . import api
+        self.api, self.group = api, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.n = B * H * H
+        self.mail = torch.zeros((2, self.world, B, H * H), dtype=torch.float32, device="cuda")
+        self.flags = torch.zeros(self.world, dtype=torch.int32, device="cuda")
+        self.counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        mine = (self.rank, reduce_tensor(self.mail), reduce_tensor(self.flags))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._peers = []                                   # keep the mappings alive
+        mail_ptrs, flag_ptrs = [0] * self.world, [0] * self.world
+        for r, (fm, am), (ff, af) in allh:
+            if r == self.rank:
+                m, f = self.mail, self.flags
+            else:
+                m, f = fm(*am), ff(*af)
+                self._peers.append((m, f))
+            mail_ptrs[r], flag_ptrs[r] = m.data_ptr(), f.data_ptr()
+        self.mail_ptrs = torch.tensor(mail_ptrs, dtype=torch.int64, device="cuda")
+        self.flag_ptrs = torch.tensor(flag_ptrs, dtype=torch.int64, device="cuda")
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def exchange(self, agg: torch.Tensor) -> torch.Tensor:
+        """Publish this rank's aggregate, wait for the later ranks'; returns the
+        gathered [world, B, H*H] view (valid for kernels after this call)."""
+        self.epoch += 1
+        self.api.exchange_publish(agg.contiguous(), self.rank, self.world, self.mail_ptrs, self.flag_ptrs,
+                                  self.counter, self.epoch)
+        self.api.exchange_wait(self.flags, self.rank, self.world, self.epoch)
+        return self.mail[self.epoch & 1]
+
+
+def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None, exchange=None):
     """Run the 3-step protocol on this rank.  `seed` must be given on the last
     rank only (it holds t = T-1).  Returns (local grad_h, J_lo^T grad_h[lo])."""
     rank = dist.get_rank(group)
@@ -68,7 +114,9 @@ def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None
     if head != (seed is not None):
         raise ValueError("exactly the last rank passes the seed")
     agg = backend.up(seed)
-    if world > 1:
+    if world > 1 and exchange is not None:               # peer-memory exchange (no NCCL)
+        gathered = exchange.exchange(agg).view((world,) + tuple(agg.shape))
+    elif world > 1:
         flat = torch.empty((world * agg.shape[0],) + tuple(agg.shape[1:]), dtype=agg.dtype, device=agg.device)
         dist.all_gather_into_tensor(flat, agg.contiguous(), group=group)    # concat form (NCCL and gloo)
         gathered = flat.view((world,) + tuple(agg.shape))

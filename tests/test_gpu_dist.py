@@ -21,14 +21,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, T, B, H, q):
+def _worker(rank, world, port, T, B, H, q, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import bppsa_workloads as W
         from paper_1907_10134_b200 import api
-        from paper_1907_10134_b200.dist import CudaShardBackend, shard_bounds, sharded_scan
+        from paper_1907_10134_b200.dist import CudaShardBackend, PeerExchange, shard_bounds, sharded_scan
         w = W.rnn_workload(T, B, H, seed=21)
         lo, hi = shard_bounds(T, world)[rank]
         h = torch.from_numpy(w.h[lo:hi]).cuda()
@@ -36,7 +36,10 @@ def _worker(rank, world, port, T, B, H, q):
         jac = api.jacobians_rnn(h, torch.from_numpy(w.W_hh).cuda())
         be = CudaShardBackend(jac, 512, 32)
         seed = torch.from_numpy(w.g).cuda() if rank == world - 1 else None
-        grad, init = sharded_scan(be, seed, want_init=(rank == 0))
+        ex = PeerExchange(B, H) if peer else None
+        for _ in range(3 if peer else 1):       # several epochs through the double-buffered mailboxes
+            grad, init = sharded_scan(be, seed, want_init=(rank == 0), exchange=ex)
+            dist.barrier()
         h_init = torch.from_numpy(w.h[lo - 1]).cuda() if lo > 0 else None
         dWih, dWhh, db = api.weight_grads_rnn(x, h, grad, h_init=h_init)
         for t in (dWih, dWhh, db):
@@ -56,12 +59,14 @@ def _worker(rank, world, port, T, B, H, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_cuda_path_one_gpu(world):
+@pytest.mark.parametrize("world,peer", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_cuda_path_one_gpu(world, peer):
+    """peer=True: the aggregates travel through bppsa_exchange_publish / _wait
+    (CUDA IPC mailboxes, here on one device) instead of the all-gather."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 30000, 16, 64, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 30000, 16, 64, q, peer)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
