@@ -168,6 +168,45 @@ __device__ __forceinline__ void matvec_multi_t(const float (&w)[1][1][HT], const
   }
 }
 
+// asynchronous 4-byte global -> shared copies for the walk's h ring
+__device__ __forceinline__ void cpa4(float* smem_dst, const float* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// The arrays one walk step reads per row: RNN h; GRU r, z, n, M, h_prev.
+template <int CELL>
+struct NArr { static constexpr int v = (CELL == BPPSA_JAC_GRU) ? 5 : 1; };
+template <int CELL>
+__device__ __forceinline__ const float* arr_ptr(const LeafArgs& a, int k) {
+  if (CELL == BPPSA_JAC_RNN_TANH) return a.h;
+  return k == 0 ? a.r : k == 1 ? a.z : k == 2 ? a.n : k == 3 ? a.M : a.hp;
+}
+// coefficients from one staged step (ring slot: [NArr][HT] floats)
+template <int CELL>
+__device__ __forceinline__ Coef<CELL> coef_from(const float* slot, int i, bool valid) {
+  Coef<CELL> k;
+  k.c[0] = k.c[1] = k.c[2] = k.c[3] = 0.f;
+  if (!valid) return k;
+  if (CELL == BPPSA_JAC_RNN_TANH) {
+    const float hv = slot[i];
+    k.c[0] = 1.f - hv * hv;
+  } else {
+    constexpr int HTX = 32;   // GRU tiles are HT = 32 (or 20 padded into 32 slots)
+    const float r = slot[0 * HTX + i], z = slot[1 * HTX + i], n = slot[2 * HTX + i];
+    const float M = slot[3 * HTX + i], hp = slot[4 * HTX + i];
+    const float omn2 = 1.f - n * n, omz = 1.f - z;
+    k.c[0] = r * (1.f - r) * M * omn2 * omz;
+    k.c[1] = r * omn2 * omz;
+    k.c[2] = z * (1.f - z) * (hp - n);
+    k.c[3] = z;
+  }
+  return k;
+}
+
 template <int CELL, int HT, int NC>
 struct UpBounds { static constexpr int minb = (CELL == BPPSA_JAC_RNN_TANH && HT == 64) ? 3 : 1; };
 
@@ -331,71 +370,93 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
   }
   const long long rowB = (long long)B * H;
   long long s = vec ? 1 : s0;
-  Coef<CELL> nxt[NR];
-  if (s < s1) {
-    const long long t = a.seg.time_of(s);
+  // the walk is a dependent GEMV chain: the h rows of the next PF steps are in
+  // flight as asynchronous copies into a per-warp shared-memory ring (one step
+  // of register prefetch left a lone chain bound by HBM latency, ~700 ns per
+  // step in the linear scan; a register ring stalls on its own loads)
+  constexpr int PF = 8, NA = NArr<CELL>::v, SLOT = NA * 32;   // slot: [NA][32] floats (HT <= 32 per row group)
+  float* ring = smem + (blockDim.x >> 5) * 2 * XW + wib * PF * SLOT * NR;   // after every warp's x buffers
+  auto stage = [&](long long sp) {                              // step sp -> ring slot sp % PF
+    if (sp < s1) {
+      const long long t = a.seg.time_of(sp);
+      float* dst = ring + (int)(sp % PF) * SLOT * NR;
 #pragma unroll
-    for (int m = 0; m < NR; ++m) {
-      const int i = lane + 32 * m;
-      nxt[m] = load_coef<CELL>(a, t * rowB + (long long)b * H + i, i < H);
+      for (int m = 0; m < NR; ++m) {
+        const int i = lane + 32 * m;
+        if (i < H)
+#pragma unroll
+          for (int k = 0; k < NA; ++k) cpa4(dst + (m * NA + k) * 32 + lane, arr_ptr<CELL>(a, k) + (t * B + b) * H + i);
+      }
     }
-  }
+    cpa_commit();                                               // one group per step, empty or not
+  };
+#pragma unroll 1
+  for (int u = 0; u < PF; ++u) stage(s + u);
   int buf = 0;
-  for (; s < s1; ++s) {
-    const long long t = a.seg.time_of(s);
-    if (!vonly) {
+  bool done = false;
+  for (; s < s1 && !done; s += PF) {
+#pragma unroll 1
+    for (int u = 0; u < PF; ++u) {                // not unrolled: one copy of the GEMV body (i-cache)
+      const long long su = s + u;
+      if (su >= s1 || done) break;
+      const long long t = a.seg.time_of(su);
+      if (!vonly) {
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+          const int i = lane + 32 * m;
+          if (i < H) grad_h[t * rowB + (long long)b * H + i] = v[m];
+        }
+      }
+      const bool last = (su + 1 == s1);
+      const bool total = !vonly && last && s1 == S && grad_init != nullptr;
+      if (last && !total && !vonly) {
+        done = true;
+        break;
+      }
+      cpa_wait<PF - 1>();                         // step su's group has landed (this lane's copies)
+      __syncwarp();
+      Coef<CELL> cur[NR];
+      {
+        const float* slot = ring + (int)(su % PF) * SLOT * NR;
+#pragma unroll
+        for (int m = 0; m < NR; ++m) cur[m] = coef_from<CELL>(slot + m * NA * 32, lane, lane + 32 * m < H);
+      }
+      __syncwarp();                               // every lane has read the slot before it is refilled
+      stage(su + PF);
+      float ev[NR];                               // e_{t-1}, loaded ahead of the GEMV
 #pragma unroll
       for (int m = 0; m < NR; ++m) {
         const int i = lane + 32 * m;
-        if (i < H) grad_h[t * rowB + (long long)b * H + i] = v[m];
+        ev[m] = (e != nullptr && t >= 1 && i < H) ? __ldg(e + (t - 1) * rowB + (long long)b * H + i) : 0.f;
       }
-    }
-    const bool last = (s + 1 == s1);
-    const bool total = !vonly && last && s1 == S && grad_init != nullptr;
-    if (last && !total && !vonly) break;
-    Coef<CELL> cur[NR];
-#pragma unroll
-    for (int m = 0; m < NR; ++m) cur[m] = nxt[m];
-    if (!last) {
-      const long long tn = a.seg.time_of(s + 1);
+      float* xb = xs + buf * XW;
 #pragma unroll
       for (int m = 0; m < NR; ++m) {
         const int i = lane + 32 * m;
-        nxt[m] = load_coef<CELL>(a, tn * rowB + (long long)b * H + i, i < H);
+        if (i < HT) {
+#pragma unroll
+          for (int vv = 0; vv < NV; ++vv) xb[vv * HT + i] = cur[m].c[vv] * v[m];
+        }
       }
-    }
-    float ev[NR];                                   // e_{t-1}, loaded ahead of the GEMV
-#pragma unroll
-    for (int m = 0; m < NR; ++m) {
-      const int i = lane + 32 * m;
-      ev[m] = (e != nullptr && t >= 1 && i < H) ? __ldg(e + (t - 1) * rowB + (long long)b * H + i) : 0.f;
-    }
-    float* xb = xs + buf * XW;
-#pragma unroll
-    for (int m = 0; m < NR; ++m) {
-      const int i = lane + 32 * m;
-      if (i < HT) {
-#pragma unroll
-        for (int vv = 0; vv < NV; ++vv) xb[vv * HT + i] = cur[m].c[vv] * v[m];
-      }
-    }
-    __syncwarp();
-    float acc[NR];
-    matvec<CELL, HT, NR, 4>(w, xb, acc);
-#pragma unroll
-    for (int m = 0; m < NR; ++m) {
-      if (CELL == BPPSA_JAC_GRU) acc[m] = fmaf(cur[m].c[3], v[m], acc[m]);
-      v[m] = acc[m] + ev[m];
-    }
-    buf ^= 1;
-    if (total) {
+      __syncwarp();
+      float acc[NR];
+      matvec<CELL, HT, NR, 4>(w, xb, acc);
 #pragma unroll
       for (int m = 0; m < NR; ++m) {
-        const int i = lane + 32 * m;
-        if (i < H) grad_init[(long long)b * H + i] = v[m];
+        if (CELL == BPPSA_JAC_GRU) acc[m] = fmaf(cur[m].c[3], v[m], acc[m]);
+        v[m] = acc[m] + ev[m];
+      }
+      buf ^= 1;
+      if (total) {
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+          const int i = lane + 32 * m;
+          if (i < H) grad_init[(long long)b * H + i] = v[m];
+        }
       }
     }
   }
+  cpa_wait<0>();                                  // no copy left in flight at exit
   if (vonly) {
 #pragma unroll
     for (int m = 0; m < NR; ++m) {
@@ -438,7 +499,8 @@ cudaError_t down_impl(const LeafArgs& a, int C, const float* carry, long long nb
                       float* grad_init, cudaStream_t st, const DownX& x) {
   const long long tasks = (long long)a.seg.B * nblk;
   const long long grid = (tasks + kWarpsPerCta - 1) / kWarpsPerCta;
-  const size_t smem = (size_t)kWarpsPerCta * 2 * NX<CELL>::v * HT * sizeof(float);
+  const int NRr = (HT + 31) / 32;
+  const size_t smem = (size_t)kWarpsPerCta * (2 * NX<CELL>::v * HT + 8 * NArr<CELL>::v * 32 * NRr) * sizeof(float);
   leaf_down_kernel<CELL, HT><<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(
       a, C, carry, nblk, grad_h, grad_init, x.e, x.vec_out, x.head_out, x.head_bstride);
   return cudaGetLastError();
