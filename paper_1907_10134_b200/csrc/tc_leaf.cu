@@ -610,7 +610,8 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_down16_kernel(LeafArgs 
 // ---------------------------------------------------------------------------
 constexpr int F_B_BYTES = 2 * TH * TH * 2;                 // [W1 | W2]: 128 rows x 64 fp16 = 16 KB
 constexpr int F_OFF_H = F_B_BYTES;
-constexpr int F_OFF_RED = F_OFF_H + NSLOT * H_BYTES;       // [slot][parity][128 rows][4 column groups] u32
+constexpr int F_OFF_RED = F_OFF_H + 2 * NSLOT * H_BYTES;   // h: [slot][2 chunk buffers] (f16g uses the first two)
+                                                           // red: [slot][parity][128 rows][4 column groups] u32
 constexpr int F_OFF_DMX = F_OFF_RED + NSLOT * 2 * TM * 16; // [slot][2 samples][HCH] dmax
 constexpr int F_OFF_BAR = F_OFF_DMX + NSLOT * 2 * HCH * 4;
 constexpr int F_SMEM_BYTES = F_OFF_BAR + 64 + 1024;
@@ -758,8 +759,10 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
   const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
   const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64;
   const uint32_t t_a1 = lane_base + 128 + NP * cgp, t_a2 = lane_base + 160 + NP * cgp;
-  float* hs = reinterpret_cast<float*>(smem + F_OFF_H + g * H_BYTES);
-  const uint32_t hs_s = su32(hs);
+  // two chunk buffers per slot: the next chunk's h (this tile's, or the next
+  // tile's first) is copied while the current chunk's steps run
+  char* const hsb0 = smem + F_OFF_H + (2 * g) * H_BYTES;
+  auto hsb = [&](int c) { return reinterpret_cast<float*>(hsb0 + c * H_BYTES); };
   float* dmx = reinterpret_cast<float*>(smem + F_OFF_DMX) + g * 2 * HCH;       // [2 samples][HCH]
   const uint32_t red0 = su32(smem + F_OFF_RED) + (uint32_t)(((g * 2) * TM + row) * 16);   // parity 0 row word
   const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
@@ -772,6 +775,32 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
   int tstep = 0;
 #endif
   const long long rowB = (long long)B * TH;
+  // one chunk of tile tx from slot scx: HCH steps of the h rows of its two
+  // samples, asynchronous (one commit group)
+  auto issue_chunk = [&](long long tx, long long scx, float* hb) {
+    const long long qx = q0 + tx / nbp;
+    const int bpx = (int)(tx % nbp);
+    const int nx = (int)min((long long)HCH, min(qx * C + (long long)C, S) - scx);
+    for (int e = et; e < 2 * nx * 16; e += EPI) {
+      const int bb2 = e / (nx * 16), rem = e % (nx * 16), st = rem / 16, ch = rem % 16;
+      float* dst = hb + (bb2 * HCH + st) * TH + ch * 4;
+      const int bs = bpx * 2 + bb2;
+      if (bs < B)
+        cp_async16(dst, a.h + (long long)a.seg.time_of(scx + st) * rowB + (long long)bs * TH + ch * 4);
+      else
+        sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto tile_s0 = [&](long long tx) {
+    const long long qx = q0 + tx / nbp;
+    return (a.seg.head && qx == 0) ? 1LL : qx * C;
+  };
+  int cb = 0;                                      // buffer of the current chunk
+  {
+    const long long t0 = 2 * (long long)blockIdx.x + g;
+    if (t0 < ntiles) issue_chunk(t0, tile_s0(t0), hsb(0));
+  }
   for (long long tau = 2 * (long long)blockIdx.x + g; tau < ntiles; tau += 2 * (long long)gridDim.x) {
     const long long q = q0 + tau / nbp;
     const int bp = (int)(tau % nbp);
@@ -790,17 +819,10 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
       c2[i] = make_float2((CPT * cgp + 2 * i == j && ok) ? 1.f : 0.f, (CPT * cgp + 2 * i + 1 == j && ok) ? 1.f : 0.f);
     for (long long sc = s0; sc < s1; sc += HCH) {
       const int n = (int)min((long long)HCH, s1 - sc);
-      named_bar(1 + g, EPI);             // previous chunk fully consumed (d is read into registers)
-      for (int e = et; e < 2 * n * 16; e += EPI) {
-        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
-        float* dst = hs + (bb2 * HCH + st) * TH + ch * 4;
-        const int bs = bp * 2 + bb2;
-        if (bs < B)
-          cp_async16(dst, a.h + (long long)a.seg.time_of(sc + st) * rowB + (long long)bs * TH + ch * 4);
-        else
-          sts128(su32(dst), 0.f, 0.f, 0.f, 0.f);
-      }
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      float* hs = hsb(cb);
+      const uint32_t hs_s = su32(hs);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");   // this chunk's copies (issued one chunk ago)
+      named_bar(1 + g, EPI);             // every thread's copies landed; the previous chunk is consumed
       // d = 1 - h^2 in place and dmax per (sample, step): 16 consecutive lanes
       // hold one 64-wide row (2n*16 is a multiple of 32: whole warps iterate)
       for (int e = et; e < 2 * n * 16; e += EPI) {
@@ -815,6 +837,12 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
         if (ch == 0) dmx[bb2 * HCH + st] = m;
       }
       named_bar(1 + g, EPI);
+      {                                  // prefetch the next chunk into the other buffer
+        const long long tn = tau + 2 * (long long)gridDim.x;
+        if (sc + HCH < s1) issue_chunk(tau, sc + HCH, hsb(cb ^ 1));
+        else if (tn < ntiles) issue_chunk(tn, tile_s0(tn), hsb(cb ^ 1));
+      }
+      cb ^= 1;
       uint32_t dp = hs_s + 4u * ((row >> 6) * HCH * TH + CPT * cgp);  // this thread's d slice of step st
       uint32_t dmp = su32(dmx + (row >> 6) * HCH);                      // dmax of step st
       for (int st = 0; st < n; ++st, dp += 4u * TH, dmp += 4u) {
