@@ -41,8 +41,11 @@ constexpr int TM = 128;                   // chains per tile (UMMA M)
 constexpr int NSLOT = 2;                  // tiles in flight per CTA
 constexpr int B_ROWS = 2 * TH;            // B = [W_hi | W_lo] stacked along N
 constexpr int B_BYTES = B_ROWS * TH * 4;  // 32 KB
-constexpr int HCH = 64;                   // steps staged per chunk
-constexpr int H_BYTES = 2 * HCH * TH * 4; // one tile's h slices (2 blocks), 32 KB
+#ifndef BPPSA_HCH
+#define BPPSA_HCH 96
+#endif
+constexpr int HCH = BPPSA_HCH;            // steps staged per chunk
+constexpr int H_BYTES = 2 * HCH * TH * 4; // one tile's h slices (2 blocks), 48 KB
 constexpr int OFF_B = 0;
 constexpr int OFF_H = OFF_B + B_BYTES;
 // TMEM columns of slot g (base 256 g): D = A [W_hi | W_lo] accumulated over
