@@ -658,6 +658,113 @@ __device__ __forceinline__ void mma8_f16_commit(uint32_t d, const uint64_t (&bd)
       : "memory");
 }
 
+// The fold's variant: A1 x [W1 | W2] first (N = 128; the first MMA
+// initialises all 128 columns), then A2 x W1 only (N = 64): the x2 W2 product
+// the N = 128 form also made is not needed, and the narrower MMAs touch half
+// the accumulator columns
+constexpr uint32_t IDESC_F16_N64 = idesc_f16(64);
+// A2 x W1 first (N = 64, initialising the left half), then A1's first K step
+// as two N = 64 MMAs (W1 accumulating into the left half, W2 initialising the
+// right half), then A1's other K steps at N = 128: the small x2 W1 sum is
+// formed before the large terms arrive (the accumulation order of the N = 128
+// form) while the accumulator traffic stays that of the narrow form
+__device__ __forceinline__ void mma9_f16_commit_mix(uint32_t d, const uint64_t (&bd)[4], const uint64_t bd2k0,
+                                                    uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 a, dr;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 dr, %0, 64;\n"
+      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %7, f;\n"
+      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %7, t;\n"
+      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %7, t;\n"
+      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %7, t;\n"
+      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %7, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [dr], [a], %8, %7, f;\n"
+      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
+      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
+      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
+      "}\n" ::"r"(d),
+      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar), "r"(IDESC_F16_N64), "l"(bd2k0)
+      : "memory");
+}
+
+// ... and with x2 W1 in its own accumulator (columns 192..255 of the slot):
+// each sum stays in its own fp32 accumulator (the tensor core's accumulation
+// of small terms into a large one loses their low bits), the epilogue adds
+// D1 + (D1' + D2) with round-to-nearest
+__device__ __forceinline__ void mma8_f16_commit_split(uint32_t d, const uint64_t (&bd)[4], uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 a, d2;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 d2, %0, 192;\n"
+      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %1, %7, f;\n"
+      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %2, %7, t;\n"
+      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %3, %7, t;\n"
+      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %4, %7, t;\n"
+      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %5, f;\n"
+      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
+      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
+      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
+      "}\n" ::"r"(d),
+      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar), "r"(IDESC_F16_N64)
+      : "memory");
+}
+
+// c' <- D1 + (D1' + D2) for this thread's CPT columns (mma8_f16_commit_split)
+template <int CPT, int NP>
+__device__ __forceinline__ void load_d_sum3(uint32_t t_d1, uint32_t t_d2, uint32_t t_d3, float2 (&c2)[NP]) {
+#pragma unroll
+  for (int h = 0; h < CPT / 16; ++h) {
+    float t1[16], t2[16], t3[16];
+    tmem_ld16(t_d1 + 16 * h, t1);
+    tmem_ld16(t_d2 + 16 * h, t2);
+    tmem_ld16(t_d3 + 16 * h, t3);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      c2[8 * h + i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]),
+                                 __fadd2_rn(make_float2(t2[2 * i], t2[2 * i + 1]), make_float2(t3[2 * i], t3[2 * i + 1])));
+  }
+}
+
+#ifndef FOLD_ISSUE
+#define FOLD_ISSUE(d, bd, bd2, bar) mma9_f16_commit_mix(d, bd, bd2, bar)
+#endif
+#ifndef LOAD_D_FOLD
+#define LOAD_D_FOLD(a, b, c, o) load_d_sum<CPT>(a, b, o)
+#endif
+__device__ __forceinline__ void mma8_f16_commit_a1first(uint32_t d, const uint64_t (&bd)[4], uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 a;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %5, f;\n"
+      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
+      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
+      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
+      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %7, t;\n"
+      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %7, t;\n"
+      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %7, t;\n"
+      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %7, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
+      "}\n" ::"r"(d),
+      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar), "r"(IDESC_F16_N64)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 // W exponent shift sw (max |W| 2^sw in [2^14, 2^15), clamped: W = 0 gives a
@@ -760,7 +867,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
   const bool issuer = wl == 0;
   const uint32_t slot_base = tmem + 256 * g;
   const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
-  const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64, t_d3 = t_d1 + 192;
   const uint32_t t_a1 = lane_base + 128 + NP * cgp, t_a2 = lane_base + 160 + NP * cgp;
   // two chunk buffers per slot: the next chunk's h (this tile's, or the next
   // tile's first) is copied while the current chunk's steps run
@@ -773,6 +880,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
   uint64_t bdesc[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  const uint64_t bd2k0 = sdesc(bb + 8192u);       // the W2 rows (64..127) at K step 0
   uint32_t ph = 0, par = 0;                        // D phase; parity of the max exchange buffer
 #ifdef BPPSA_STEP_TRACE
   int tstep = 0;
@@ -876,7 +984,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
           ph ^= 1;
           tc_fence_after();
           STEP_TRACE(4);
-          load_d_sum<CPT>(t_d1, t_d2, c2);
+          LOAD_D_FOLD(t_d1, t_d2, t_d3, c2);
           STEP_TRACE(5);
         }
         first = false;
@@ -909,7 +1017,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
         STEP_TRACE(2);
         if (issuer) {
           tc_fence_after();
-          mma8_f16_commit(slot_base, bdesc, su32(&d_full[g]));
+          FOLD_ISSUE(slot_base, bdesc, bd2k0, su32(&d_full[g]));
           STEP_TRACE(3);
         }
         if constexpr (NCG == 4) {
@@ -941,7 +1049,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
     named_bar(5 + g, EPI);
     ph ^= 1;
     tc_fence_after();
-      load_d_sum<CPT>(t_d1, t_d2, c2);
+      LOAD_D_FOLD(t_d1, t_d2, t_d3, c2);
     }
     if (ok) {
       float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + CPT * cgp);
