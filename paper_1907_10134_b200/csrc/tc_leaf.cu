@@ -607,9 +607,11 @@ __global__ void __launch_bounds__(NTHREADS16, 1) tc_leaf_down16_kernel(LeafArgs 
 // of anything smaller stays below 2^-35 of the row maximum.
 // The scaled chain c' = c 2^E keeps its exponent E (an integer per row, the
 // same in the row's four threads); the aggregate is written as c' 2^-E.
-// Per step and tile: 8 MMAs M128 N128 K16 (A2 then A1 against [W1 | W2]);
-// measured 76 cycles each (scripts/tc_f16_probe.cu) against 16 x 64 for the
-// tf32 form.  A1 / A2 are packed f16x2 in TMEM (even k in the low half).
+// Per step and tile: 12 MMAs M128 N64 K16 into one 64-column accumulator,
+// small products first (x2 W1, x1 W2, x1 W1; mma12_f16_commit_n64): the
+// fold is bound by TMEM traffic, so the narrow accumulator (half the epilogue
+// loads of the former 8 N = 128 MMAs against [W1 | W2]) is the faster form.
+// A1 / A2 are packed f16x2 in TMEM (even k in the low half).
 // ---------------------------------------------------------------------------
 constexpr int F_B_BYTES = 2 * TH * TH * 2;                 // [W1 | W2]: 128 rows x 64 fp16 = 16 KB
 constexpr int F_OFF_H = F_B_BYTES;
@@ -634,9 +636,12 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
                : "memory");
 }
 
-// A2 (corrections) then A1, K = 64 in 16-wide steps, B = [W1 | W2]; one
-// elected stream of the converged issuer warp (see mma16_commit)
-__device__ __forceinline__ void mma8_f16_commit(uint32_t d, const uint64_t (&bd)[4], uint32_t bar) {
+constexpr uint32_t IDESC_F16_N64 = idesc_f16(64);
+
+// All three products into one 64-column accumulator (N = 64 MMAs), small
+// first: x2 W1 (init), x1 W2, then x1 W1; the epilogue loads 64 columns
+__device__ __forceinline__ void mma12_f16_commit_n64(uint32_t d, const uint64_t (&bd)[4], const uint64_t (&bw2)[4],
+                                                     uint32_t bar) {
   asm volatile(
       "{\n"
       " .reg .pred e, f, t;\n"
@@ -648,101 +653,34 @@ __device__ __forceinline__ void mma8_f16_commit(uint32_t d, const uint64_t (&bd)
       " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
       " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
       " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
+      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %7, %5, t;\n"
+      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %8, %5, t;\n"
+      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %9, %5, t;\n"
+      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %10, %5, t;\n"
       " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %5, t;\n"
       " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
       " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
       " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
       " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
       "}\n" ::"r"(d),
-      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar)
+      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16_N64), "r"(bar), "l"(bw2[0]), "l"(bw2[1]),
+      "l"(bw2[2]), "l"(bw2[3])
       : "memory");
 }
 
-// The fold's variant: A1 x [W1 | W2] first (N = 128; the first MMA
-// initialises all 128 columns), then A2 x W1 only (N = 64): the x2 W2 product
-// the N = 128 form also made is not needed, and the narrower MMAs touch half
-// the accumulator columns
-constexpr uint32_t IDESC_F16_N64 = idesc_f16(64);
-// A2 x W1 first (N = 64, initialising the left half), then A1's first K step
-// as two N = 64 MMAs (W1 accumulating into the left half, W2 initialising the
-// right half), then A1's other K steps at N = 128: the small x2 W1 sum is
-// formed before the large terms arrive (the accumulation order of the N = 128
-// form) while the accumulator traffic stays that of the narrow form
-__device__ __forceinline__ void mma9_f16_commit_mix(uint32_t d, const uint64_t (&bd)[4], const uint64_t bd2k0,
-                                                    uint32_t bar) {
-  asm volatile(
-      "{\n"
-      " .reg .pred e, f, t;\n"
-      " .reg .b32 a, dr;\n"
-      " setp.ne.b32 f, 0, 0;\n"
-      " setp.eq.b32 t, 0, 0;\n"
-      " elect.sync _|e, 0xffffffff;\n"
-      " add.u32 dr, %0, 64;\n"
-      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %7, f;\n"
-      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %7, t;\n"
-      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %7, t;\n"
-      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %7, t;\n"
-      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %7, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [dr], [a], %8, %7, f;\n"
-      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
-      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
-      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
-      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
-      "}\n" ::"r"(d),
-      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar), "r"(IDESC_F16_N64), "l"(bd2k0)
-      : "memory");
-}
-
-// ... and with x2 W1 in its own accumulator (columns 192..255 of the slot):
-// each sum stays in its own fp32 accumulator (the tensor core's accumulation
-// of small terms into a large one loses their low bits), the epilogue adds
-// D1 + (D1' + D2) with round-to-nearest
-__device__ __forceinline__ void mma8_f16_commit_split(uint32_t d, const uint64_t (&bd)[4], uint32_t bar) {
-  asm volatile(
-      "{\n"
-      " .reg .pred e, f, t;\n"
-      " .reg .b32 a, d2;\n"
-      " setp.ne.b32 f, 0, 0;\n"
-      " setp.eq.b32 t, 0, 0;\n"
-      " elect.sync _|e, 0xffffffff;\n"
-      " add.u32 d2, %0, 192;\n"
-      " add.u32 a, %0, 160;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %1, %7, f;\n"
-      " add.u32 a, %0, 168;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %2, %7, t;\n"
-      " add.u32 a, %0, 176;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %3, %7, t;\n"
-      " add.u32 a, %0, 184;\n @e tcgen05.mma.cta_group::1.kind::f16 [d2], [a], %4, %7, t;\n"
-      " add.u32 a, %0, 128;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %1, %5, f;\n"
-      " add.u32 a, %0, 136;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %2, %5, t;\n"
-      " add.u32 a, %0, 144;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %3, %5, t;\n"
-      " add.u32 a, %0, 152;\n @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], %4, %5, t;\n"
-      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
-      "}\n" ::"r"(d),
-      "l"(bd[0]), "l"(bd[1]), "l"(bd[2]), "l"(bd[3]), "r"(IDESC_F16), "r"(bar), "r"(IDESC_F16_N64)
-      : "memory");
-}
-
-// c' <- D1 + (D1' + D2) for this thread's CPT columns (mma8_f16_commit_split)
+// c' <- D (one 64-column accumulator) for this thread's CPT columns
 template <int CPT, int NP>
-__device__ __forceinline__ void load_d_sum3(uint32_t t_d1, uint32_t t_d2, uint32_t t_d3, float2 (&c2)[NP]) {
+__device__ __forceinline__ void load_d_one(uint32_t t_d1, float2 (&c2)[NP]) {
 #pragma unroll
   for (int h = 0; h < CPT / 16; ++h) {
-    float t1[16], t2[16], t3[16];
+    float t1[16];
     tmem_ld16(t_d1 + 16 * h, t1);
-    tmem_ld16(t_d2 + 16 * h, t2);
-    tmem_ld16(t_d3 + 16 * h, t3);
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      c2[8 * h + i] = __fadd2_rn(make_float2(t1[2 * i], t1[2 * i + 1]),
-                                 __fadd2_rn(make_float2(t2[2 * i], t2[2 * i + 1]), make_float2(t3[2 * i], t3[2 * i + 1])));
+    for (int i = 0; i < 8; ++i) c2[8 * h + i] = make_float2(t1[2 * i], t1[2 * i + 1]);
   }
 }
 
-#ifndef FOLD_ISSUE
-#define FOLD_ISSUE(d, bd, bd2, bar) mma9_f16_commit_mix(d, bd, bd2, bar)
-#endif
-#ifndef LOAD_D_FOLD
-#define LOAD_D_FOLD(a, b, c, o) load_d_sum<CPT>(a, b, o)
-#endif
 __device__ __forceinline__ void mma8_f16_commit_a1first(uint32_t d, const uint64_t (&bd)[4], uint32_t bar) {
   asm volatile(
       "{\n"
@@ -867,7 +805,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
   const bool issuer = wl == 0;
   const uint32_t slot_base = tmem + 256 * g;
   const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
-  const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64, t_d3 = t_d1 + 192;
+  const uint32_t t_d1 = lane_base + CPT * cgp;     // the 64-column accumulator
   const uint32_t t_a1 = lane_base + 128 + NP * cgp, t_a2 = lane_base + 160 + NP * cgp;
   // two chunk buffers per slot: the next chunk's h (this tile's, or the next
   // tile's first) is copied while the current chunk's steps run
@@ -880,7 +818,9 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
   uint64_t bdesc[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
-  const uint64_t bd2k0 = sdesc(bb + 8192u);       // the W2 rows (64..127) at K step 0
+  uint64_t bw2[4];                                 // the W2 rows at every K step
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bw2[kk] = sdesc(bb + 8192u + (uint32_t)(kk * 32));
   uint32_t ph = 0, par = 0;                        // D phase; parity of the max exchange buffer
 #ifdef BPPSA_STEP_TRACE
   int tstep = 0;
@@ -984,7 +924,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
           ph ^= 1;
           tc_fence_after();
           STEP_TRACE(4);
-          LOAD_D_FOLD(t_d1, t_d2, t_d3, c2);
+          load_d_one<CPT>(t_d1, c2);
           STEP_TRACE(5);
         }
         first = false;
@@ -1017,7 +957,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
         STEP_TRACE(2);
         if (issuer) {
           tc_fence_after();
-          FOLD_ISSUE(slot_base, bdesc, bd2k0, su32(&d_full[g]));
+          mma12_f16_commit_n64(slot_base, bdesc, bw2, su32(&d_full[g]));
           STEP_TRACE(3);
         }
         if constexpr (NCG == 4) {
@@ -1049,7 +989,7 @@ __global__ void __launch_bounds__(64 * WPS, 1) tc_leaf_up_f16_kernel(LeafArgs a,
     named_bar(5 + g, EPI);
     ph ^= 1;
     tc_fence_after();
-      LOAD_D_FOLD(t_d1, t_d2, t_d3, c2);
+      load_d_one<CPT>(t_d1, c2);
     }
     if (ok) {
       float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + CPT * cgp);
@@ -1154,7 +1094,7 @@ __global__ void __launch_bounds__(512, 1) tc_leaf_up_f16g_kernel(LeafArgs a, int
   const bool issuer = wl == 0;
   const uint32_t slot_base = tmem + 256 * g;
   const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
-  const uint32_t t_d1 = lane_base + CPT * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_d1 = lane_base + CPT * cgp;     // the 64-column accumulator
   const uint32_t t_a1 = lane_base + 128 + NP * cgp, t_a2 = lane_base + 160 + NP * cgp;
   float* hs = reinterpret_cast<float*>(smem + F_OFF_H + g * H_BYTES);    // [GRP][HG][64] d
   const uint32_t hs_s = su32(hs);
@@ -1164,6 +1104,9 @@ __global__ void __launch_bounds__(512, 1) tc_leaf_up_f16g_kernel(LeafArgs a, int
   uint64_t bdesc[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  uint64_t bw2[4];                                 // the W2 rows (64..127) at every K step
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bw2[kk] = sdesc(bb + 8192u + (uint32_t)(kk * 32));
   uint32_t ph = 0, par = 0;
   const long long rowB = (long long)B * H;
   const int grp = row / H, j = row % H;
@@ -1262,7 +1205,7 @@ __global__ void __launch_bounds__(512, 1) tc_leaf_up_f16g_kernel(LeafArgs a, int
           named_bar(5 + g, EPI);
           ph ^= 1;
           tc_fence_after();
-          load_d_sum<CPT>(t_d1, t_d2, c2);
+          load_d_one<CPT>(t_d1, c2);
           if (ok && gst == len) {                   // aggregate after the group's last real step
 #pragma unroll
             for (int i = 0; i < NP; ++i) {
@@ -1298,7 +1241,7 @@ __global__ void __launch_bounds__(512, 1) tc_leaf_up_f16g_kernel(LeafArgs a, int
         named_bar(3 + g, EPI);
         if (issuer) {
           tc_fence_after();
-          mma8_f16_commit(slot_base, bdesc, su32(&d_full[g]));
+          mma12_f16_commit_n64(slot_base, bdesc, bw2, su32(&d_full[g]));
         }
         uint32_t m2[2];
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
@@ -1314,7 +1257,7 @@ __global__ void __launch_bounds__(512, 1) tc_leaf_up_f16g_kernel(LeafArgs a, int
       named_bar(5 + g, EPI);
       ph ^= 1;
       tc_fence_after();
-      load_d_sum<CPT>(t_d1, t_d2, c2);
+      load_d_one<CPT>(t_d1, c2);
       if (ok && len == nsteps && len > 0) {
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
@@ -1449,7 +1392,7 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
   const bool issuer = wl == 0;
   const uint32_t slot_base = tmem + 256 * g;
   const uint32_t lane_base = slot_base + ((uint32_t)((wl & 3) * 32) << 16);
-  const uint32_t t_d1 = lane_base + 32 * cgp, t_d2 = t_d1 + 64;
+  const uint32_t t_d1 = lane_base + 32 * cgp;      // the 64-column accumulator
   const uint32_t t_a1 = lane_base + 128 + 16 * cgp, t_a2 = lane_base + 160 + 16 * cgp;
   const uint32_t ring = su32(smem + W_OFF_RING) + (uint32_t)(g * W_NST * W_STAGE);
   const uint32_t hrow_off = (uint32_t)(row * 256 + cgp * 128);          // this thread's row half in a stage
@@ -1461,6 +1404,9 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
   uint64_t bdesc[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) bdesc[kk] = sdesc(bb + (uint32_t)(kk * 32));
+  uint64_t bw2[4];                                 // the W2 rows (64..127) at every K step
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) bw2[kk] = sdesc(bb + 8192u + (uint32_t)(kk * 32));
   const uint32_t dbar = su32(&d_full[g]), hbar0 = su32(&h_full[g * W_NST]);
   uint32_t dph = 0, par = 0, gs = 0;                       // D phase; exchange parity; slot step counter
   // tile row = j B + b holds group r = G-1-j (block q = qb + r), sample b: the
@@ -1630,7 +1576,7 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
         dph ^= 1;
         tc_fence_after();
         float2 t[16];
-        load_d_sum<32>(t_d1, t_d2, t);
+        load_d_one<32>(t_d1, t);
         const float f = __int_as_float((127 - s_prev - sw) << 23);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __fmul2_rn(t[i], make_float2(f, f));
@@ -1712,7 +1658,7 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
       WTRACE(5);
       if (issuer) {
         tc_fence_after();
-        mma8_f16_commit(slot_base, bdesc, dbar);
+        mma12_f16_commit_n64(slot_base, bdesc, bw2, dbar);
         if (!vonly) issue_stores(st, gs);
         else asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         if (st + 2 < C) {
@@ -1743,7 +1689,7 @@ __global__ void __launch_bounds__(W_NT, 1) tc_leaf_down_f16_kernel(LeafArgs a, c
     tc_fence_after();
     {
       float2 t[16];
-      load_d_sum<32>(t_d1, t_d2, t);
+      load_d_one<32>(t_d1, t);
       if ((total || vonly) && valid && len == C) {
         const float f = __int_as_float((127 - s_prev - sw) << 23);
         float2 ef[16];
