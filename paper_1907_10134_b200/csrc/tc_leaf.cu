@@ -637,6 +637,9 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
 }
 
 constexpr uint32_t IDESC_F16_N64 = idesc_f16(64);
+#ifndef FOLD_WPS
+#define FOLD_WPS 8                      // epilogue warps per slot of the fold
+#endif
 
 // All three products into one 64-column accumulator (N = 64 MMAs), small
 // first: x2 W1 (init), x1 W2, then x1 W1; the epilogue loads 64 columns
@@ -1748,9 +1751,9 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
     return cudaGetLastError();
   }
   if (prec == 0) {                                 // 3xFP16, 8 epilogue warps per slot
-    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_up_f16_kernel<8>), F_SMEM_BYTES);
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_up_f16_kernel<FOLD_WPS>), F_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    tc_leaf_up_f16_kernel<8><<<grid, 64 * 8, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
+    tc_leaf_up_f16_kernel<FOLD_WPS><<<grid, 64 * FOLD_WPS, F_SMEM_BYTES, st>>>(a, C, agg_out, n_out, q0);
     return cudaGetLastError();
   }
   cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_leaf_up16_kernel), SMEM_BYTES16);
