@@ -84,23 +84,24 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
   }
   int pc = 0;
   constexpr int ac = 0;
-  if (HP == 64 && H == 64 && Tl::NT == 256) {
+  if (HP == 64 && H == 64 && 1024 % Tl::NT == 0) {
     // H = 64: the next A_s (16 KB, column-major = A[k][i] rows of 64) is
     // prefetched as four coalesced float4 per thread (scalar loads made this
     // kernel LSU-throttled: r01h ncu, lg_throttle 20 %, LSU 47 %)
-    float4 pre4[4];
+    constexpr int U4 = 1024 / Tl::NT;               // float4 per thread per 64 x 64 matrix
+    float4 pre4[U4];
     if (s < s1) {
       const float4* m = reinterpret_cast<const float4*>(A.mat(b, s));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) pre4[u] = __ldg(m + tid + u * 256);
+      for (int u = 0; u < U4; ++u) pre4[u] = __ldg(m + tid + u * Tl::NT);
     }
     for (; s < s1; ++s) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) reinterpret_cast<float4*>(Ab[ac])[tid + u * 256] = pre4[u];
+      for (int u = 0; u < U4; ++u) reinterpret_cast<float4*>(Ab[ac])[tid + u * Tl::NT] = pre4[u];
       if (s + 1 < s1) {
         const float4* m = reinterpret_cast<const float4*>(A.mat(b, s + 1));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) pre4[u] = __ldg(m + tid + u * 256);
+        for (int u = 0; u < U4; ++u) pre4[u] = __ldg(m + tid + u * Tl::NT);
       }
       __syncthreads();
       gemm_step<HP, TM, TN>(Ab[ac], Pb[pc], Pb[pc ^ 1], tid);
@@ -593,6 +594,10 @@ cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, in
                            long long n_out, cudaStream_t st) {
   if (H == 20) return fold_impl<20, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st);
   if (H <= 32) return fold_impl<32, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st);
+  // many blocks (level 1 at C4: 1040 CTAs): 8 x 8 register tiles, 64 threads
+  // per GEMM, half the shared-memory reads per FMA (the 4 x 4 form was
+  // LSU / MIO-throttled); few blocks: 4 x 4, 256 threads, shorter chains
+  if ((long long)n_out * B >= 4LL * 148) return fold_impl<64, 8, 8>(A, H, B, n, C, head, agg_out, n_out, st);
   return fold_impl<64, 4, 4>(A, H, B, n, C, head, agg_out, n_out, st);
 }
 
