@@ -167,23 +167,31 @@ struct Bars {
 // h_init) are zero.  IX = number of input columns (hi threads only).
 template <bool LO, int IX, bool FULL, bool SPLIT>
 __device__ __forceinline__ void convert_rows(uint32_t base, uint32_t xbase, int n, int nlow, float (&av)[16],
-                                             float (&bv)[16], float& dbias, float (&dih)[MAXI], uint32_t hp_lo,
-                                             uint32_t hp_hi, int nsplit) {
+                                             float (&bh)[8], float (&bl)[8], float& dbias, float (&dih)[MAXI],
+                                             uint32_t hp_lo, uint32_t hp_hi, int nsplit) {
+  // A: delta hi (or lo) of all 16 rows (TMEM lanes are per warp quadrant, so
+  // the hi and lo rows of a column belong to different threads and each forms
+  // delta); B: h_prev hi AND lo of 8 of the 16 rows (B is in shared memory,
+  // any thread may write both rows) — the hi thread rows 0..7, the lo thread
+  // rows 8..15, so h_prev is loaded and split once
+  constexpr int R0 = LO ? 8 : 0;
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
-    // h_prev row rr: rows < nsplit from hp_lo, the rest from hp_hi (see
-    // converters); !SPLIT: every row from hp_lo
-    const float hv = lds(base + rr * ROW_BYTES), gv = lds(base + (KC + rr) * ROW_BYTES),
-                pv = lds(!SPLIT ? hp_lo + rr * ROW_BYTES
-                                : (rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES));
-    float d = (1.f - hv * hv) * gv, hp = pv;
-    if (!FULL) {
-      d = rr < n ? d : 0.f;
-      hp = (rr < n && rr >= nlow) ? hp : 0.f;
-    }
-    const float dhi = tf32_hi(d), phi = tf32_hi(hp);
+    const float hv = lds(base + rr * ROW_BYTES), gv = lds(base + (KC + rr) * ROW_BYTES);
+    float d = (1.f - hv * hv) * gv;
+    if (!FULL) d = rr < n ? d : 0.f;
+    const float dhi = tf32_hi(d);
     av[rr] = LO ? d - dhi : dhi;
-    bv[rr] = LO ? hp - phi : phi;
+    if (rr >= R0 && rr < R0 + 8) {
+      // h_prev row rr: rows < nsplit from hp_lo, the rest from hp_hi (see
+      // converters); !SPLIT: every row from hp_lo
+      float hp = lds(!SPLIT ? hp_lo + rr * ROW_BYTES
+                            : (rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES));
+      if (!FULL) hp = (rr < n && rr >= nlow) ? hp : 0.f;
+      const float phi = tf32_hi(hp);
+      bh[rr - R0] = phi;
+      bl[rr - R0] = hp - phi;
+    }
     if (!LO) {
       dbias += d;
 #pragma unroll
@@ -248,14 +256,14 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
         hp_hi = hp_lo;
         nsplit = 0;
       }
-      float av[16], bv[16];
+      float av[16], bh[8], bl[8];
       if (nsplit == 0 || nsplit >= 16) {               // my 16 h_prev rows are contiguous
         const uint32_t hp = nsplit == 0 ? hp_hi : hp_lo;
-        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, false>(base, xbase, n, nlow, av, bv, dbias, dih, hp, hp, 16);
-        else convert_rows<LO, IX, false, false>(base, xbase, n, nlow, av, bv, dbias, dih, hp, hp, 16);
+        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, false>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp, hp, 16);
+        else convert_rows<LO, IX, false, false>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp, hp, 16);
       } else {
-        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, true>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
-        else convert_rows<LO, IX, false, true>(base, xbase, n, nlow, av, bv, dbias, dih, hp_lo, hp_hi, nsplit);
+        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, true>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp_lo, hp_hi, nsplit);
+        else convert_rows<LO, IX, false, true>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp_lo, hp_hi, nsplit);
       }
       if (!reuse) {
         mbar_arrive(br.empty(s));
@@ -273,9 +281,12 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
       }
       tmem_st16(tl + 128 + 32 * b + 16 * grp, av);
       const uint32_t bt = s0 + OFF_BT + b * B_BYTES;
+      const int kb = 16 * grp + (LO ? 8 : 0);    // this thread's 8 K columns, rows i (hi) and 64 + i (lo)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        sts4(bt + sw_off(m, 16 * grp + 4 * q), bv[4 * q], bv[4 * q + 1], bv[4 * q + 2], bv[4 * q + 3]);
+      for (int q = 0; q < 2; ++q) {
+        sts4(bt + sw_off(i, kb + 4 * q), bh[4 * q], bh[4 * q + 1], bh[4 * q + 2], bh[4 * q + 3]);
+        sts4(bt + sw_off(64 + i, kb + 4 * q), bl[4 * q], bl[4 * q + 1], bl[4 * q + 2], bl[4 * q + 3]);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       tc_before();
