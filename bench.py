@@ -335,8 +335,9 @@ def e2e_ours(api, w, args):
     d2h = sum(t.numel() * 4 for t in outs_h)
     res = {"value": round(e0.elapsed_time(e1) / n, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": n,
-           "path": f"StreamedRnnBackward ({chunks} time chunks: pinned H2D overlapped with bppsa_scan_shard_up/"
-                   f"_down per chunk, then bppsa_weight_grads_rnn)"}
+           "path": f"StreamedRnnBackward ({sb.G} time chunks: pinned H2D overlapped with "
+                   f"bppsa_scan_shard_up/_down and the weight-gradient rows of each chunk, then the "
+                   f"fixed-order reduction)"}
     # the H2D alone, for reference: the floor of this e2e number
     hd = torch.empty_like(hp, device="cuda")
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -263,6 +263,29 @@ bppsa_status bppsa_weight_grads_rnn(int T, int B, int H, int I, const float* x,
                                     float* dW_hh, float* db, void* ws,
                                     size_t ws_bytes, void* stream);
 
+/* The RNN weight gradients in row ranges (for inputs that arrive in pieces,
+ * e.g. host-streamed time chunks): rows = T*B in time-major order.
+ * part_rows: the granularity of the tensor-core path (0 when it does not
+ * apply: then use bppsa_weight_grads_rnn).  rows: computes the partial
+ * slabs of rows [row0, row1) into `ws` (row0, row1 multiples of part_rows,
+ * or row1 = T*B); x, h, grad_h, h_init are the WHOLE arrays (only the range
+ * and, for h_prev, the row B before it are read).  reduce: sums every slab
+ * into dW_ih, dW_hh, db after all ranges ran on `stream` (or were otherwise
+ * ordered before it).  Covering [0, T*B) in any order gives bit-identical
+ * results to bppsa_weight_grads_rnn (same parts, same fixed reduction).    */
+bppsa_status bppsa_weight_grads_rnn_part_rows(int T, int B, int H, int I,
+                                              long long* part_rows);
+bppsa_status bppsa_weight_grads_rnn_rows(int T, int B, int H, int I,
+                                         const float* x, const float* h,
+                                         const float* h_init,
+                                         const float* grad_h, long long row0,
+                                         long long row1, void* ws,
+                                         size_t ws_bytes, void* stream);
+bppsa_status bppsa_weight_grads_rnn_reduce(int T, int B, int H, int I,
+                                           float* dW_ih, float* dW_hh,
+                                           float* db, void* ws,
+                                           size_t ws_bytes, void* stream);
+
 /* GRU (gates r,z,n order as torch): dN = g(1-z)(1-n^2), dZ = g(h_prev-n)z(1-z),
  * dR = dN M r(1-r), dM = dN r;  dW_ih3 = [dR;dZ;dN] x^T [3H][I],
  * dW_hh3 = [dR;dZ;dM] h_prev^T [3H][H], db_ih3 = sum [dR;dZ;dN],

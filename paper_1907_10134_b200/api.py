@@ -43,6 +43,10 @@ EXPORTS = {
     "bppsa_jacobians_gru": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_Jac), _vp]),
     "bppsa_scan_workspace_size": (_i, [C.POINTER(_Jac), C.POINTER(_Opts), C.POINTER(_sz)]),
     "bppsa_scan": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_weight_grads_rnn_part_rows": (_i, [_i, _i, _i, _i, C.POINTER(C.c_longlong)]),
+    "bppsa_weight_grads_rnn_rows": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, C.c_longlong, C.c_longlong, _vp, _sz,
+                                         _vp]),
+    "bppsa_weight_grads_rnn_reduce": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "bppsa_exchange_publish": (_i, [_vp, C.c_longlong, _i, _i, _vp, _vp, _vp, C.c_uint, _vp]),
     "bppsa_exchange_wait": (_i, [_vp, _i, _i, C.c_uint, _vp]),
     "bppsa_gru_gates": (_i, [_i, _i, _i, _i] + [_vp] * 12 + [_vp]),
@@ -322,6 +326,34 @@ def weight_grads_rnn(x, h, grad_h, h_init=None, ws=None, out=None, stream=None):
                                        _ptr(db, "db"), ws.data_ptr(), ws.numel(), _stream(stream)),
            "bppsa_weight_grads_rnn")
     return dW_ih, dW_hh, db
+
+
+def weight_grads_rnn_part_rows(T, B, H, I) -> int:
+    """Row granularity of bppsa_weight_grads_rnn_rows (0: not available)."""
+    n = C.c_longlong()
+    _check(_lib.bppsa_weight_grads_rnn_part_rows(T, B, H, I, C.byref(n)), "bppsa_weight_grads_rnn_part_rows")
+    return n.value
+
+
+def weight_grads_rnn_rows(x, h, grad_h, row0: int, row1: int, ws: torch.Tensor, h_init=None, stream=None):
+    """bppsa_weight_grads_rnn_rows: partial slabs of rows [row0, row1) into ws."""
+    T, B, H = h.shape
+    I = x.shape[2]
+    _check(_lib.bppsa_weight_grads_rnn_rows(T, B, H, I, _ptr(x, "x") if I else None, _ptr(h, "h"),
+                                            _ptr(h_init, "h_init"), _ptr(grad_h, "grad_h"), row0, row1,
+                                            ws.data_ptr(), ws.numel(), _stream(stream)),
+           "bppsa_weight_grads_rnn_rows")
+
+
+def weight_grads_rnn_reduce(T, B, H, I, ws: torch.Tensor, out=None, device=None, stream=None):
+    """bppsa_weight_grads_rnn_reduce -> (dW_ih [H,I], dW_hh [H,H], db [H])."""
+    dev = device or ws.device
+    if out is None:
+        out = (torch.empty((H, I), device=dev), torch.empty((H, H), device=dev), torch.empty((H,), device=dev))
+    _check(_lib.bppsa_weight_grads_rnn_reduce(T, B, H, I, _ptr(out[0], "dW_ih") if I else None,
+                                              _ptr(out[1], "dW_hh"), _ptr(out[2], "db"), ws.data_ptr(), ws.numel(),
+                                              _stream(stream)), "bppsa_weight_grads_rnn_reduce")
+    return out
 
 
 def weight_grads_gru(x, tape: dict, grad_h, ws=None, out=None, stream=None):

@@ -775,6 +775,54 @@ bppsa_status bppsa_weight_grads_rnn(int T, int B, int H, int I, const float* x, 
   return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "weight grads rnn");
 }
 
+bppsa_status bppsa_weight_grads_rnn_part_rows(int T, int B, int H, int I, long long* part_rows) {
+  if (!part_rows || T < 1 || B < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad arguments");
+  *part_rows = tc_wgrad_applies(H, I, (long long)T * B) ? tc_wgrad_part_rows() : 0;
+  return BPPSA_OK;
+}
+
+bppsa_status bppsa_weight_grads_rnn_rows(int T, int B, int H, int I, const float* x, const float* h,
+                                         const float* h_init, const float* grad_h, long long row0, long long row1,
+                                         void* ws, size_t ws_bytes, void* stream) {
+  size_t need;
+  bppsa_status s = bppsa_weight_grads_workspace_size(T, B, H, I, &need);
+  if (s != BPPSA_OK) return s;
+  const long long rows = (long long)T * B;
+  long long pr = 0;
+  bppsa_weight_grads_rnn_part_rows(T, B, H, I, &pr);
+  if (pr == 0) return fail(BPPSA_ERR_NOT_SUPPORTED, "row ranges need the tensor-core weight gradients (H = 64)");
+  if (row0 < 0 || row1 > rows || row0 >= row1 || row0 % pr != 0 || (row1 % pr != 0 && row1 != rows))
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "row range must be [row0, row1) with both multiples of the part size "
+                                             "(bppsa_weight_grads_rnn_part_rows) or row1 = T*B");
+  if (I > 0) REQUIRE_DEV(x, "x");
+  REQUIRE_DEV(h, "h");
+  REQUIRE_DEV(grad_h, "grad_h");
+  if (h_init) REQUIRE_DEV(h_init, "h_init");
+  if (ws_bytes < need || !is_device_ptr(ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace too small or not device memory");
+  auto a16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  if (!(a16(h) && a16(grad_h) && a16(h_init) && (I == 0 || a16(x))))
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "h, grad_h, h_init and x must be 16-byte aligned");
+  cudaError_t e = launch_tc_wgrad_partials(B, I, x, h, h_init, grad_h, rows, static_cast<float*>(ws), num_sms(),
+                                           (cudaStream_t)stream, row0, row1);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "weight grads rows");
+}
+
+bppsa_status bppsa_weight_grads_rnn_reduce(int T, int B, int H, int I, float* dW_ih, float* dW_hh, float* db,
+                                           void* ws, size_t ws_bytes, void* stream) {
+  size_t need;
+  bppsa_status s = bppsa_weight_grads_workspace_size(T, B, H, I, &need);
+  if (s != BPPSA_OK) return s;
+  if (I > 0) REQUIRE_DEV(dW_ih, "dW_ih");
+  REQUIRE_DEV(dW_hh, "dW_hh");
+  REQUIRE_DEV(db, "db");
+  if (ws_bytes < need || !is_device_ptr(ws)) return fail(BPPSA_ERR_WORKSPACE, "workspace too small or not device memory");
+  const long long rows = (long long)T * B;
+  if (!tc_wgrad_applies(H, I, rows)) return fail(BPPSA_ERR_NOT_SUPPORTED, "row ranges need the tensor-core path");
+  cudaError_t e = launch_wgrad_reduce_rnn(static_cast<float*>(ws), tc_wgrad_parts(rows), H, I, dW_ih, dW_hh, db,
+                                          (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "weight grads reduce");
+}
+
 bppsa_status bppsa_weight_grads_gru(int T, int B, int H, int I, const float* x, const float* h_prev,
                                     const float* r, const float* z, const float* n, const float* M,
                                     const float* grad_h, float* dW_ih3, float* dW_hh3, float* db_ih3,

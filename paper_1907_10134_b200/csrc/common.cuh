@@ -168,7 +168,9 @@ bool wgrad_supported(int H, int I);
 long long tc_wgrad_parts(long long rows);
 bool tc_wgrad_applies(int H, int I, long long rows);
 cudaError_t launch_tc_wgrad_partials(int B, int I, const float* x, const float* h, const float* h_init,
-                                     const float* grad_h, long long rows, float* ws, int num_sms, cudaStream_t st);
+                                     const float* grad_h, long long rows, float* ws, int num_sms, cudaStream_t st,
+                                     long long row0 = 0, long long row1 = -1);
+long long tc_wgrad_part_rows();
 cudaError_t launch_wgrad_reduce_rnn(const float* ws, long long nparts, int H, int I, float* dW_ih, float* dW_hh,
                                     float* db, cudaStream_t st);
 cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const float* h,

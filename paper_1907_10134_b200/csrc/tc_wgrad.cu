@@ -127,7 +127,8 @@ struct TWArgs {
   const float *x, *h, *h_init, *g;
   long long rows;
   float* ws;            // partials [P][4][H][H + I + 1]
-  long long nparts;
+  long long nparts;     // parts [part0, nparts) are computed (slabs at their absolute part index)
+  long long part0;
 };
 
 struct ChunkIter {      // walks this CTA's chunks: parts blockIdx.x + j*gridDim.x
@@ -213,7 +214,7 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
   const int NB = H + IX + 1;
   const bool reuse = w.B <= KC;
   uint32_t cg = 0;
-  for (long long part = blockIdx.x; part < w.nparts; part += gridDim.x) {
+  for (long long part = w.part0 + blockIdx.x; part < w.nparts; part += gridDim.x) {
     float acc[64];
 #pragma unroll
     for (int k = 0; k < 64; ++k) acc[k] = 0.f;
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
     if (lane == 0) {
       // ===== loader: NS chunks ahead of the converters =====
       ChunkIter ld;
-      ld.start(blockIdx.x, w.rows);
+      ld.start(w.part0 + blockIdx.x, w.rows);
       const long long B = w.B;
       while (ld.part < w.nparts) {
         const int s = (int)(ld.cg % NS);
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
     if (lane == 0) {
       // ===== MMA issuer =====
       ChunkIter mm;
-      mm.start(blockIdx.x, w.rows);
+      mm.start(w.part0 + blockIdx.x, w.rows);
       while (mm.part < w.nparts) {
         const int b = (int)(mm.cg % NBUF);
         mbar_wait(br.a_full(b), (uint32_t)((mm.cg / NBUF) & 1));
@@ -427,6 +428,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
 }  // namespace
 
 long long tc_wgrad_parts(long long rows) { return 4 * ((rows + PART_ROWS - 1) / PART_ROWS); }   // slabs
+long long tc_wgrad_part_rows() { return PART_ROWS; }
 bool tc_wgrad_applies(int H_, int I, long long rows) {
   static const int force = [] { const char* e = getenv("BPPSA_FORCE_TC_WGRAD"); return e ? atoi(e) : 0; }();
   if (H_ != H || I > MAXI) return false;
@@ -434,11 +436,15 @@ bool tc_wgrad_applies(int H_, int I, long long rows) {
 }
 
 cudaError_t launch_tc_wgrad_partials(int B, int I, const float* x, const float* h, const float* h_init,
-                                     const float* grad_h, long long rows, float* ws, int num_sms, cudaStream_t st) {
+                                     const float* grad_h, long long rows, float* ws, int num_sms, cudaStream_t st,
+                                     long long row0, long long row1) {
   cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_wgrad_kernel), SMEM);
   if (e != cudaSuccess) return e;
-  TWArgs a{B, I, x, h, h_init, grad_h, rows, ws, (rows + PART_ROWS - 1) / PART_ROWS};
-  const int grid = (int)std::min<long long>(a.nparts, num_sms);
+  if (row1 < 0) row1 = rows;
+  const long long p0 = row0 / PART_ROWS, p1 = (row1 + PART_ROWS - 1) / PART_ROWS;   // parts of [row0, row1)
+  if (p1 <= p0) return cudaSuccess;
+  TWArgs a{B, I, x, h, h_init, grad_h, rows, ws, p1, p0};
+  const int grid = (int)std::min<long long>(p1 - p0, num_sms);
   tc_wgrad_kernel<<<grid, NTH, SMEM, st>>>(a);
   return cudaGetLastError();
 }

@@ -505,3 +505,67 @@ def test_rnn_tensor_walk_group_shapes(lib, B):
     ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
     grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=64, block=8, leaf_impl="tensor")
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
+
+
+def test_weight_grads_row_ranges_bit_identical(lib):
+    """bppsa_weight_grads_rnn_rows over part-aligned ranges in any order +
+    _reduce == one bppsa_weight_grads_rnn call, bit for bit; misaligned ranges
+    are rejected."""
+    T, B, H = 1 << 14, 16, 64                     # 262144 rows = 16 parts of 16384
+    w = W.rnn_workload(T, B, H, seed=31)
+    x, h = cu(w.x), cu(w.h)
+    g = torch.randn((T, B, H), device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
+    pr = lib.weight_grads_rnn_part_rows(T, B, H, 1)
+    assert pr == 16384
+    ws = lib.workspace(lib.weight_grads_workspace_size(T, B, H, 1))
+    one = [t.clone() for t in lib.weight_grads_rnn(x, h, g, ws=ws)]
+    ws2 = lib.workspace(lib.weight_grads_workspace_size(T, B, H, 1))
+    cuts = [0, 3 * pr, 4 * pr, 11 * pr, T * B]
+    for a, b in reversed(list(zip(cuts[:-1], cuts[1:]))):
+        lib.weight_grads_rnn_rows(x, h, g, a, b, ws2)
+    got = lib.weight_grads_rnn_reduce(T, B, H, 1, ws2)
+    torch.cuda.synchronize()
+    for u, v in zip(got, one):
+        assert torch.equal(u, v)
+    with pytest.raises(lib.BppsaError, match="INVALID_ARGUMENT"):
+        lib.weight_grads_rnn_rows(x, h, g, 100, pr, ws2)
+
+
+def test_streamed_backward_chunked_weight_grads(lib):
+    """stream.py with chunk-by-chunk weight gradients (chunks = whole parts):
+    identical to the one-shot weight gradients on the streamed grad_h, and the
+    oracle's within 1e-4."""
+    from paper_1907_10134_b200.stream import StreamedRnnBackward
+    T, B, H, I = 1 << 15, 16, 64, 1
+    w = W.rnn_workload(T, B, H, seed=78)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    sb = StreamedRnnBackward(T, B, H, I, chunks=8, block0=512, block=32)
+    assert sb.wg_rows
+    dWih, dWhh, db, grad, gi = sb.run(pin(w.h), pin(w.x), pin(w.W_hh), pin(w.g))
+    torch.cuda.synchronize()
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    assert rel_pair(grad, ref, gi, ref_init) <= TOL
+    one = lib.weight_grads_rnn(cu(w.x), cu(w.h), grad)
+    torch.cuda.synchronize()
+    for u, v in zip((dWih, dWhh, db), one):
+        assert torch.equal(u, v)
+    rW = bp.weight_grads_rnn(w.x, w.h, ref)
+    for got, want in zip((dWih, dWhh, db), rW):
+        assert rel(got, want) <= TOL
+
+
+def test_streamed_backward_tail_pieces(lib):
+    """stream.py with the t = 0 chunk cut into shrinking pieces (tail = 3): the
+    shard protocol over unequal shards, == the oracle."""
+    from paper_1907_10134_b200.stream import StreamedRnnBackward
+    T, B, H, I = 1 << 15, 16, 64, 1
+    w = W.rnn_workload(T, B, H, seed=79)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    sb = StreamedRnnBackward(T, B, H, I, chunks=4, block0=512, block=32, tail=3)
+    assert sb.G == 7 and sb.bounds[0] == (0, 1024) and sb.wg_rows
+    dWih, dWhh, db, grad, gi = sb.run(pin(w.h), pin(w.x), pin(w.W_hh), pin(w.g))
+    torch.cuda.synchronize()
+    ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
+    assert rel_pair(grad, ref, gi, ref_init) <= TOL
+    for got, want in zip((dWih, dWhh, db), bp.weight_grads_rnn(w.x, w.h, ref)):
+        assert rel(got, want) <= TOL
