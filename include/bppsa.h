@@ -146,14 +146,22 @@ typedef struct bppsa_scan_opts {
   int mode;    /* bppsa_scan_mode                                              */
   int block0;  /* BLOCKED: leaf block length in slots (0 = default)            */
   int block;   /* BLOCKED: block length of the upper levels (0 = default)      */
-  int leaf_impl; /* level-0 fold engine: 0 = auto (tensor cores for the tanh
-                  * RNN with H = 64, CUDA cores otherwise), 1 = FFMA (CUDA
-                  * cores), 2 = tensor cores (up-sweep fold as 3xFP16 with
-                  * per-chain power-of-two scaling; tanh RNN with 16 <= H <= 64,
-                  * H % 4 == 0; the level-0 walk uses the tensor cores at H = 64
-                  * only), 3 = tensor cores with the 3xTF32 up-sweep fold (H =
-                  * 64).  2 and 3 fail with BPPSA_ERR_NOT_SUPPORTED outside
-                  * their range.                                              */
+  int leaf_impl; /* level-0 engine (fold and walk of the fused RNN leaves):
+                  * 0 = auto: the tanh RNN with H = 64 on the integer tensor
+                  * cores (4), everything else on the CUDA cores (1);
+                  * 1 = FFMA (CUDA cores, fp32 round-to-nearest);
+                  * 2 = 3xFP16 tensor-core fold with per-chain power-of-two
+                  * scaling (tanh RNN, 16 <= H <= 64, H % 4 == 0; the walk on
+                  * the tensor cores at H = 64) — opt-in: its fp32 accumulation
+                  * truncates (a one-signed ~1.4 ulp bias per step);
+                  * 3 = the same with a 3xTF32 fold (H = 64);
+                  * 4 = exact-integer tensor cores (tanh RNN, H = 64): operands
+                  * as 8-bit digits of fixed-point rows (23-bit X per chain row,
+                  * 31-bit W), products accumulated EXACTLY in s32 by
+                  * tcgen05.mma kind::i8, combined once in fp32
+                  * round-to-nearest; no biased rounding anywhere.
+                  * 2, 3 and 4 fail with BPPSA_ERR_NOT_SUPPORTED outside their
+                  * range.                                                    */
   /* Optional instrumentation (all may be NULL/0): if `events` is non-NULL the
    * library records events[2k] / events[2k+1] (cudaEvent_t, created by the
    * caller) on `stream` immediately before / after its k-th kernel launch,

@@ -169,7 +169,7 @@ def jacobians_dense(JT: torch.Tensor) -> Jacobians:
 
 
 # ----------------------------------------------------------------- scan
-LEAF_IMPL = {"auto": 0, "ffma": 1, "tensor": 2, "tensor_tf32": 3}
+LEAF_IMPL = {"auto": 0, "ffma": 1, "tensor": 2, "tensor_tf32": 3, "int8": 4}
 
 
 def _opts(mode="blocked", block0=0, block=0, trace=None, leaf_impl="auto", levels=(0, 0)) -> _Opts:

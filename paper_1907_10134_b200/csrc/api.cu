@@ -117,23 +117,31 @@ int num_sms() {
   return n;
 }
 
-// tcgen05 level-0 fold: tanh RNN with H = 64 (a dense 64-wide contraction per
-// step); everything else runs on the CUDA cores.
-// fold: the 3xFP16 kernels take 16 <= H <= 64 with H % 4 == 0 (the 3xTF32
-// fold, leaf_impl 3, H = 64 only); the tensor-core walk is H = 64 only
+// Level-0 engine of the fused RNN leaves (bppsa_scan_opts.leaf_impl):
+// kCuda (FFMA), kF16 (3xFP16 fold, 16 <= H <= 64, H % 4 == 0), kTf32 (3xTF32
+// fold, H = 64), kInt8 (exact-integer fold and walk, H = 64).  Auto takes
+// kInt8 for the tanh RNN at H = 64: below, the fold is latency-bound (C2,
+// H = 20: 0.45 ms on either engine) and the CUDA-core kernel keeps ~100x more
+// chains in flight.
+enum LeafEngine { kCuda = 0, kF16 = 1, kTf32 = 2, kInt8 = 3 };
 bool tensor_fold_ok(const bppsa_jac& j, int leaf_impl) {
   if (j.kind != BPPSA_JAC_RNN_TANH) return false;
-  return leaf_impl == 3 ? j.H == 64 : (j.H >= 16 && j.H <= 64 && j.H % 4 == 0);
+  if (leaf_impl == 3 || leaf_impl == 4) return j.H == 64;
+  return j.H >= 16 && j.H <= 64 && j.H % 4 == 0;
 }
-// auto (leaf_impl 0) takes the tensor cores at H = 64 only: below, the fold is
-// latency-bound (C2, H = 20: 0.45 ms on either engine; C1: 0.042 tensor vs
-// 0.033 ms FFMA) and the CUDA-core kernel keeps ~100x more chains in flight
-bool use_tensor_leaf(const bppsa_jac& j, int leaf_impl) {
-  const bool ok = tensor_fold_ok(j, leaf_impl);
-  return leaf_impl >= 2 ? ok : (leaf_impl == 0 && ok && j.H == 64);
+LeafEngine leaf_engine(const bppsa_jac& j, int leaf_impl) {
+  switch (leaf_impl) {
+    case 0: return (j.kind == BPPSA_JAC_RNN_TANH && j.H == 64) ? kInt8 : kCuda;
+    case 2: return tensor_fold_ok(j, 2) ? kF16 : kCuda;
+    case 3: return tensor_fold_ok(j, 3) ? kTf32 : kCuda;
+    case 4: return tensor_fold_ok(j, 4) ? kInt8 : kCuda;
+    default: return kCuda;
+  }
 }
+// the 3xFP16 TMA walk (H = 64) serves kF16 and kTf32
 bool use_tensor_walk(const bppsa_jac& j, int leaf_impl) {
-  return use_tensor_leaf(j, leaf_impl) && j.H == 64;
+  const LeafEngine e = leaf_engine(j, leaf_impl);
+  return (e == kF16 || e == kTf32) && j.H == 64;
 }
 
 struct Plan {
@@ -206,10 +214,10 @@ bppsa_status make_plan(const bppsa_jac& j, int head, const bppsa_scan_opts* opts
   const size_t HH = (size_t)j.H * j.H, B = (size_t)j.B;
   size_t off = 0;
   p->leaf_impl = opts ? opts->leaf_impl : 0;
-  if (p->leaf_impl < 0 || p->leaf_impl > 3) return fail(BPPSA_ERR_INVALID_ARGUMENT, "leaf_impl must be 0, 1, 2 or 3");
+  if (p->leaf_impl < 0 || p->leaf_impl > 4) return fail(BPPSA_ERR_INVALID_ARGUMENT, "leaf_impl must be in 0..4");
   if (p->leaf_impl >= 2 && !tensor_fold_ok(j, p->leaf_impl))
     return fail(BPPSA_ERR_NOT_SUPPORTED,
-                "tensor-core leaf fold: tanh RNN with 16 <= H <= 64, H % 4 == 0 (3xTF32: H = 64)");
+                "tensor-core leaf fold: tanh RNN with 16 <= H <= 64, H % 4 == 0 (3xTF32 and int8: H = 64)");
   const bool tree = (mode == BPPSA_SCAN_ALG1 || mode == BPPSA_SCAN_HYBRID);
   p->has_dense = (j.kind == BPPSA_JAC_DENSE) && !tree;
   if (p->has_dense) {
@@ -329,22 +337,21 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
     tr.begin(st);
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
       const LeafArgs la = leaf_args(j, head, seed);
-      if (use_tensor_leaf(j, p.leaf_impl)) {
-        const int prec = p.leaf_impl == 3 ? 1 : 0;
-        if (prec != 1) {
-          // 3xFP16 fold: the head block is folded as the matrix of its leaves
-          // with all other blocks, then applied to the seed
-          e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], 0, num_sms(), st, prec);
-          if (e == cudaSuccess && head) {                  // its own traced launch
-            tr.end(st);
-            tr.begin(st);
-            e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, H, st);
-          }
-        } else {
-          // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
-          e = head ? launch_leaf_up(la, p.C[0], dst, p.n[1], 0, 1, st) : cudaSuccess;
-          if (e == cudaSuccess) e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], head, num_sms(), st, prec);
+      const LeafEngine eng = leaf_engine(j, p.leaf_impl);
+      if (eng == kF16 || eng == kInt8) {
+        // tensor-core fold of every block; the head block is folded as the
+        // matrix of its leaves with all other blocks, then applied to the seed
+        e = eng == kInt8 ? launch_tc_fold_i8(la, p.C[0], dst, p.n[1], 0, num_sms(), st)
+                         : launch_tc_leaf_up(la, p.C[0], dst, p.n[1], 0, num_sms(), st, 0);
+        if (e == cudaSuccess && head) {                  // its own traced launch
+          tr.end(st);
+          tr.begin(st);
+          e = launch_head_apply(dst, p.n[1] * (long long)H * H, seed, B, H, st);
         }
+      } else if (eng == kTf32) {
+        // head block (a GEMV chain from the seed) on the CUDA cores, matrix blocks on tcgen05
+        e = head ? launch_leaf_up(la, p.C[0], dst, p.n[1], 0, 1, st) : cudaSuccess;
+        if (e == cudaSuccess) e = launch_tc_leaf_up(la, p.C[0], dst, p.n[1], head, num_sms(), st, 1);
       } else {
         e = launch_leaf_up(la, p.C[0], dst, p.n[1], 0, p.n[1], st);
       }

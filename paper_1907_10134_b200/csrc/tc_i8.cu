@@ -1,0 +1,422 @@
+// tc_i8.cu — the level-0 up-sweep fold of the tanh-RNN leaves (H = 64) on the
+// tcgen05 INTEGER tensor cores, with exact accumulation.
+//
+// The fold computes every level-0 block aggregate a[s1-1] ... a[s0] (Alg. 1's
+// up-sweep products over one block) column by column: column j is a
+// BP chain c <- J_t^T c = W^T (d_t o c) from e_j, d_t = 1 - h_t^2 (eqn:rnn,
+// P:315; DESIGN reading 1).  All chains step with the same W, so one step of a
+// tile of 128 chains is one dense contraction C'[128 x 64] = X[128 x 64] W.
+//
+// Why integers.  fp32-accurate products on the fp16/tf32 tensor cores need
+// split operands AND fp32 accumulation, and the tcgen05 accumulator truncates:
+// a one-signed bias of ~1.35 ulp per step that grows linearly along a chain
+// (profiles/tc_precision.md).  kind::i8 accumulates in s32,
+// EXACTLY.  So every operand is a fixed-point integer split into 8-bit digits:
+//   x = y 2^-sigma,  X = rint(y 2^sigma) in [-2^23, 2^23)  (one rounding, RN:
+//       per row, sigma puts max|X| in [2^22, 2^23): 23 bits + sign),
+//       X = x0 2^16 + x1 2^8 + x2   (two's complement bytes: x0 s8, x1 x2 u8)
+//   W = Wint 2^-tau,  |Wint| < 2^31 - 2^24 (one scale for the matrix, RN),
+//       Wint = W0 2^24 + W1 2^16 + W2 2^8 + W3   (balanced s8 digits)
+// and X Wint = 2^40 sum_{i,j} x_i W_j 2^-8(i+j).  The products with i + j <= 3
+// are accumulated EXACTLY in four s32 regions R_r = sum_{i+j=r} x_i W_j (the
+// dropped i + j >= 4 terms are < 2^-30 of the result), then combined once in
+// fp32 round-to-nearest:  S = 256 R0 + R1, T = 256 R2 + R3 (exact s32),
+//   c' = fma(float(T), 2^-16, float(S)) = 2^-32 X Wint (1 + O(2^-24)).
+// Every rounding is round-to-nearest (unbiased); nothing truncates.  W keeps
+// 31 bits (the systematic part of the error), X 23 bits + sign per row.
+//
+// MMA shape.  Region r lives at TMEM columns [64 r, 64 r + 64) of the slot's
+// 256-column accumulator; B = [W0 | W1 | W2 | W3] (256 rows, K-major) and the
+// digit products land in their regions by shifting the D address:
+//   x0 [W0 W1 W2 W3] -> D + 0   (N = 256, initialises all four regions)
+//   x1 [W0 W1 W2]    -> D + 64  (N = 192)
+//   x2 [W0 W1]       -> D + 128 (N = 128)
+// each over K = 64 in two K = 32 instructions: 6 MMAs per step and tile.  The
+// two slots' accumulators fill TMEM (2 x 256 columns), so the x digits are
+// staged in shared memory (the SS form; SWIZZLE_64B K-major tiles).
+// Measured (scripts/tc_i8_probe.cu): an i8 MMA costs ~146 cycles (TS) / 167
+// (SS, N <= 192) / 182 (SS, N = 256) whatever N, so a step is ~1030 cycles of
+// tensor pipe.
+//
+// Scale bookkeeping: a chain row is c 2^E (fp32 c, integer E).  With y = c o d
+// and X = rint(y 2^sigma), the new row is c' 2^(E + 32 - sigma - tau).
+// Tile, slots and staging follow tc_leaf.cu's 3xFP16 fold: a tile = the 64
+// column chains of block q for samples b, b+1; two tiles in flight per CTA,
+// 8 epilogue warps per slot (thread = chain row x 32 columns); the row max of
+// y is exchanged between the row's two threads through shared memory.
+#include <algorithm>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace bppsa {
+namespace {
+using namespace ptx;
+
+constexpr int TH = 64;                              // hidden size
+constexpr int TM = 128;                             // chains per tile (UMMA M)
+constexpr int NSLOT = 2;                            // tiles in flight per CTA
+constexpr int I8_HCH = 64;                          // steps of h staged per chunk
+constexpr int I8_WPS = 8, I8_EPI = 32 * I8_WPS, I8_NT = NSLOT * I8_EPI;
+constexpr int I8_B_BYTES = 4 * TH * TH;             // [W0|W1|W2|W3]: 256 rows x 64 B
+constexpr int I8_A_TILE = TM * TH;                  // one x-digit tile: 128 rows x 64 B
+constexpr int I8_OFF_A = I8_B_BYTES;                // [slot][digit]
+constexpr int I8_OFF_H = I8_OFF_A + NSLOT * 3 * I8_A_TILE;
+constexpr int I8_H_BYTES = 2 * I8_HCH * TH * 4;     // a chunk: [2 samples][HCH][64] fp32
+constexpr int I8_OFF_RED = I8_OFF_H + NSLOT * 2 * I8_H_BYTES;   // [slot][parity][128 rows][2] u32
+constexpr int I8_OFF_BAR = I8_OFF_RED + NSLOT * 2 * TM * 8;
+constexpr int I8_SMEM = I8_OFF_BAR + 64 + 1024;
+constexpr uint32_t TMEM_COLS = 512;
+
+// K-major SWIZZLE_64B tile with 64-byte rows: the 16-byte chunk index is XORed
+// with address bits [7, 9) = (row / 2) % 4 (8-row atoms of 512 B)
+__device__ __forceinline__ uint32_t sw64(int row, int k) {
+  return (uint32_t)(row * 64 + ((((k >> 4) ^ ((row >> 1) & 3))) << 4) + (k & 15));
+}
+__device__ __forceinline__ uint64_t sdesc64(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused: K fits one swizzle atom)
+  d |= (uint64_t)(512 >> 4) << 32;   // SBO: 8-row groups
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;            // SWIZZLE_64B
+  return d;
+}
+// D s32, B s8, A s8 (asg = 1) or u8 (0), both K-major, M = 128
+constexpr uint32_t idesc_i8(int N, int asg) {
+  return (2u << 4) | ((uint32_t)asg << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+
+// exponent of a positive finite float (denormals included)
+__device__ __forceinline__ int ilogb_pos(float m) {
+  const uint32_t b = __float_as_uint(m);
+  return (b >> 23) ? (int)(b >> 23) - 127 : -118 - (int)__clz(b);
+}
+// sigma with max|y| 2^sigma in [2^22, 2^23 - 1]: rint never reaches 2^23
+__device__ __forceinline__ int row_sigma(float M) {
+  int s = 22 - ilogb_pos(M);
+  if ((__float_as_uint(M) & 0x7FFFFFu) == 0x7FFFFFu) s -= 1;
+  return min(s, 126);
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }   // e in [-126, 127]
+__device__ __forceinline__ int rni(float v) {
+  int r;
+  asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+
+// W digits into the B tile (all threads).  tau: max|W| 2^tau in [2^30, 2^31 -
+// 2^24), so the balanced top digit stays in [-127, 127]; red[0] a zeroed word.
+__device__ void w_digits(const float* __restrict__ W, char* smem, uint32_t* red, int* tau_out) {
+  uint32_t m = 0;
+  for (int e = threadIdx.x; e < TH * TH; e += blockDim.x) m = max(m, __float_as_uint(fabsf(__ldg(W + e))));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(red, m);
+  __syncthreads();
+  const float mx = __uint_as_float(red[0]);
+  int tau = 0;
+  if (mx > 0.f) {
+    tau = 30 - ilogb_pos(mx);
+    if ((double)mx * ldexp(1.0, tau) >= 2147483648.0 - 16777216.0) tau -= 1;
+  }
+  const double sc = ldexp(1.0, tau);
+  for (int e = threadIdx.x; e < TH * TH; e += blockDim.x) {
+    const int n = e / TH, k = e % TH;               // B[n][k] = digit of W[k][n]
+    long long wi = llrint((double)__ldg(W + (long long)k * TH + n) * sc);
+    int dg[4];
+#pragma unroll
+    for (int r = 3; r >= 1; --r) {
+      dg[r] = (int)(((wi + 128) & 255) - 128);
+      wi = (wi - dg[r]) >> 8;
+    }
+    dg[0] = (int)wi;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) smem[sw64(r * TH + n, k)] = (char)dg[r];
+  }
+  *tau_out = tau;
+}
+
+// The step's 6 MMAs (x0, x1, x2 digits against the shifted B windows, K = 64
+// in two halves) and their commit, as one elected instruction stream.
+__device__ __forceinline__ void mma6_i8_commit(uint32_t d, const uint64_t (&ad)[6], const uint64_t (&bd)[2],
+                                               uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 a;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %7, %9, f;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %2, %8, %9, t;\n"
+      " add.u32 a, %0, 64;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [a], %3, %7, %10, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [a], %4, %8, %10, t;\n"
+      " add.u32 a, %0, 128;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [a], %5, %7, %11, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [a], %6, %8, %11, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n"
+      "}\n" ::"r"(d),
+      "l"(ad[0]), "l"(ad[1]), "l"(ad[2]), "l"(ad[3]), "l"(ad[4]), "l"(ad[5]), "l"(bd[0]), "l"(bd[1]),
+      "r"(idesc_i8(256, 1)), "r"(idesc_i8(192, 0)), "r"(idesc_i8(128, 0)), "r"(bar)
+      : "memory");
+}
+
+// c' for 8 columns of this thread from the four s32 regions (TMEM columns
+// t0 + 64 r), combined once in fp32 RN
+__device__ __forceinline__ void regions_to_c(uint32_t t0, float (&c)[8]) {
+  uint32_t r0[8], r1[8], r2[8], r3[8];
+  tmem_ld8(t0, r0);
+  tmem_ld8(t0 + 64, r1);
+  tmem_ld8(t0 + 128, r2);
+  tmem_ld8(t0 + 192, r3);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int S = (int)r0[i] * 256 + (int)r1[i];
+    const int T = (int)r2[i] * 256 + (int)r3[i];
+    c[i] = fmaf(__int2float_rn(T), 0x1p-16f, __int2float_rn(S));
+  }
+}
+
+__global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                            long long n_out, long long q0) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + I8_OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + NSLOT);
+  uint32_t* wred = tmem_slot + 1;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nq = n_out - q0;
+  const int nbp = (B + 1) / 2;
+  const long long ntiles = (long long)nbp * nq;
+
+  if (threadIdx.x == 0) wred[0] = 0;
+  __syncthreads();
+  int tau;
+  w_digits(a.W, smem, wred, &tau);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < NSLOT; ++s) mbar_init(su32(&d_full[s]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int g = warp / I8_WPS, wl = warp % I8_WPS;
+  const int quad = wl & 3, row = quad * 32 + lane;
+  const int cgp = wl >> 2;                          // column half: columns [32 cgp, 32 cgp + 32)
+  const int et = wl * 32 + lane;
+  const bool issuer = wl == 0;
+  const uint32_t slot_base = tmem + 256 * g;
+  const uint32_t t_mine = slot_base + ((uint32_t)(quad * 32) << 16) + 32 * cgp;
+  const uint32_t a_tiles = su32(smem + I8_OFF_A + g * 3 * I8_A_TILE);
+  // this row's two 16-byte chunks (k in [32 cgp, 32 cgp + 32)) of a digit tile
+  const uint32_t a_c0 = a_tiles + (uint32_t)(row * 64 + (((2 * cgp) ^ ((row >> 1) & 3)) << 4));
+  const uint32_t a_c1 = a_tiles + (uint32_t)(row * 64 + (((2 * cgp + 1) ^ ((row >> 1) & 3)) << 4));
+  char* const hsb0 = smem + I8_OFF_H + (2 * g) * I8_H_BYTES;
+  auto hsb = [&](int c) { return reinterpret_cast<float*>(hsb0 + c * I8_H_BYTES); };
+  const uint32_t red0 = su32(smem + I8_OFF_RED) + (uint32_t)(((g * 2) * TM + row) * 8);
+  const uint32_t dbar = su32(&d_full[g]);
+  const int pair_bar = 7 + 4 * g + quad;            // the row's two threads (warps wl, wl ^ 4)
+  uint64_t ad[6], bd[2];
+  {
+    const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+    const uint32_t ab = __shfl_sync(0xffffffffu, a_tiles, 0);
+#pragma unroll
+    for (int dgt = 0; dgt < 3; ++dgt)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) ad[2 * dgt + ks] = sdesc64(ab + (uint32_t)(dgt * I8_A_TILE + 32 * ks));
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) bd[ks] = sdesc64(bb + (uint32_t)(32 * ks));
+  }
+  uint32_t ph = 0, par = 0;
+  const long long rowB = (long long)B * TH;
+  // one chunk of tile tx from slot scx: I8_HCH steps of the h rows of its two
+  // samples, asynchronous (one commit group)
+  auto issue_chunk = [&](long long tx, long long scx, float* hb) {
+    const long long qx = q0 + tx / nbp;
+    const int bpx = (int)(tx % nbp);
+    const int nx = (int)min((long long)I8_HCH, min(qx * C + (long long)C, S) - scx);
+    for (int e = et; e < 2 * nx * 16; e += I8_EPI) {
+      const int bb2 = e / (nx * 16), rem = e % (nx * 16), st = rem / 16, ch = rem % 16;
+      const uint32_t dst = su32(hb + (bb2 * I8_HCH + st) * TH + ch * 4);
+      const int bs = bpx * 2 + bb2;
+      if (bs < B)
+        cp_async16(dst, a.h + (long long)a.seg.time_of(scx + st) * rowB + (long long)bs * TH + ch * 4);
+      else
+        sts128(dst, 0.f, 0.f, 0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto tile_s0 = [&](long long tx) {
+    const long long qx = q0 + tx / nbp;
+    return (a.seg.head && qx == 0) ? 1LL : qx * C;
+  };
+  int cb = 0;
+  {
+    const long long t0 = 2 * (long long)blockIdx.x + g;
+    if (t0 < ntiles) issue_chunk(t0, tile_s0(t0), hsb(0));
+  }
+  for (long long tau_t = 2 * (long long)blockIdx.x + g; tau_t < ntiles; tau_t += 2 * (long long)gridDim.x) {
+    const long long q = q0 + tau_t / nbp;
+    const int bp = (int)(tau_t % nbp);
+    const int b = bp * 2 + (row >> 6);
+    const int j = row & 63;
+    const bool ok = b < B;
+    // the head block (slot 0 = the seed) is folded as the matrix of its leaves,
+    // slots 1..C-1; head_apply_kernel then applies it to the seed
+    const long long s0 = (a.seg.head && q == 0) ? 1 : q * C, s1 = min(q * C + (long long)C, S);
+    int E = 0;                                      // chain row = c 2^E
+    bool first = true;
+    for (long long sc = s0; sc < s1; sc += I8_HCH) {
+      const int n = (int)min((long long)I8_HCH, s1 - sc);
+      float* hs = hsb(cb);
+      const uint32_t hs_s = su32(hs);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      named_bar(1 + g, I8_EPI);                     // copies landed; the previous chunk is consumed
+      for (int e = et; e < 2 * n * 16; e += I8_EPI) {   // d = 1 - h^2 in place
+        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+        const uint32_t p = hs_s + 4u * ((bb2 * I8_HCH + st) * TH + ch * 4);
+        const float4 h4 = lds128(p);
+        sts128(p, fmaf(-h4.x, h4.x, 1.f), fmaf(-h4.y, h4.y, 1.f), fmaf(-h4.z, h4.z, 1.f), fmaf(-h4.w, h4.w, 1.f));
+      }
+      named_bar(1 + g, I8_EPI);
+      {                                             // prefetch the next chunk into the other buffer
+        const long long tn = tau_t + 2 * (long long)gridDim.x;
+        if (sc + I8_HCH < s1) issue_chunk(tau_t, sc + I8_HCH, hsb(cb ^ 1));
+        else if (tn < ntiles) issue_chunk(tn, tile_s0(tn), hsb(cb ^ 1));
+      }
+      cb ^= 1;
+      uint32_t dp = hs_s + 4u * ((row >> 6) * I8_HCH * TH + 32 * cgp);   // this thread's d slice of step st
+      for (int st = 0; st < n; ++st, dp += 4u * TH) {
+        float y[32];                                // y = c o d_t (this thread's 32 columns)
+        if (first) {
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 d4 = lds128(dp + 16u * q4);
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) y[4 * q4 + e] = (32 * cgp + 4 * q4 + e == j && ok) ? dv[e] : 0.f;
+          }
+        } else {
+          if (issuer) {
+            if (lane == 0) mbar_wait(dbar, ph);
+            __syncwarp();
+          }
+          named_bar(5 + g, I8_EPI);
+          ph ^= 1;
+          tc_fence_after();
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            float c[8];
+            regions_to_c(t_mine + 8 * qq, c);
+            const float4 da = lds128(dp + 32u * qq), db = lds128(dp + 32u * qq + 16u);
+            const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) y[8 * qq + i] = c[i] * dv[i];
+          }
+        }
+        first = false;
+        float pm = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pm = fmaxf(pm, fabsf(y[i]));
+        const uint32_t redp = red0 + par * (TM * 8);
+        asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+        named_bar(pair_bar, 64);
+        uint32_t m2[2];
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
+        par ^= 1;
+        const float M = __uint_as_float(max(m2[0], m2[1]));
+        const int sig = M > 0.f ? row_sigma(M) : 0;
+        const float scl = pow2f(sig);
+        if (M > 0.f) E += 32 - sig - tau;
+        // X = rint(y 2^sigma) in [-2^23, 2^23): bytes 2, 1, 0 = digits x0 (s8), x1, x2 (u8);
+        // words of 4 consecutive k per digit (7 byte permutes per 4 elements)
+        uint32_t w0[8], w1[8], w2[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t X0 = (uint32_t)rni(y[4 * u] * scl), X1 = (uint32_t)rni(y[4 * u + 1] * scl);
+          const uint32_t X2 = (uint32_t)rni(y[4 * u + 2] * scl), X3 = (uint32_t)rni(y[4 * u + 3] * scl);
+          const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
+          const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
+          w2[u] = prmt(p01, p23, 0x5410u);
+          w1[u] = prmt(p01, p23, 0x7632u);
+          w0[u] = prmt(q01, q23, 0x5410u);
+        }
+        sts128u(a_c0, w0[0], w0[1], w0[2], w0[3]);
+        sts128u(a_c1, w0[4], w0[5], w0[6], w0[7]);
+        sts128u(a_c0 + I8_A_TILE, w1[0], w1[1], w1[2], w1[3]);
+        sts128u(a_c1 + I8_A_TILE, w1[4], w1[5], w1[6], w1[7]);
+        sts128u(a_c0 + 2 * I8_A_TILE, w2[0], w2[1], w2[2], w2[3]);
+        sts128u(a_c1 + 2 * I8_A_TILE, w2[4], w2[5], w2[6], w2[7]);
+        fence_async_smem();                         // the digits -> visible to the tensor core
+        tc_fence_before();
+        named_bar(3 + g, I8_EPI);                   // the slot's three digit tiles are complete
+        if (issuer) {
+          tc_fence_after();
+          mma6_i8_commit(slot_base, ad, bd, dbar);
+        }
+      }
+    }
+    float cfin[32];
+    if (!first) {                                   // D of the tile's last step
+      if (issuer) {
+        if (lane == 0) mbar_wait(dbar, ph);
+        __syncwarp();
+      }
+      named_bar(5 + g, I8_EPI);
+      ph ^= 1;
+      tc_fence_after();
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        float c[8];
+        regions_to_c(t_mine + 8 * qq, c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cfin[8 * qq + i] = c[i];
+      }
+    } else {                                        // an empty head block: the identity
+#pragma unroll
+      for (int k = 0; k < 32; ++k) cfin[k] = (32 * cgp + k == j) ? 1.f : 0.f;
+    }
+    if (ok) {
+      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 32 * cgp);
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4)
+        dst[k4] = make_float4(ldexpf(cfin[4 * k4], E), ldexpf(cfin[4 * k4 + 1], E), ldexpf(cfin[4 * k4 + 2], E),
+                              ldexpf(cfin[4 * k4 + 3], E));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace
+
+// Matrix blocks q in [q0, n_out) of an RNN H = 64 segment, exact-integer fold.
+cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, int num_sms,
+                              cudaStream_t st) {
+  if (a.seg.H != TH) return cudaErrorInvalidValue;
+  const long long ntiles = (long long)((a.seg.B + 1) / 2) * (n_out - q0);
+  const int grid = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_fold_i8_kernel), I8_SMEM);
+  if (e != cudaSuccess) return e;
+  tc_fold_i8_kernel<<<grid, I8_NT, I8_SMEM, st>>>(a, C, agg_out, n_out, q0);
+  return cudaGetLastError();
+}
+
+}  // namespace bppsa
