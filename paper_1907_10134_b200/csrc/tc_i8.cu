@@ -36,7 +36,15 @@
 // staged in shared memory (the SS form; SWIZZLE_64B K-major tiles).
 // Measured (scripts/tc_i8_probe.cu): an i8 MMA costs ~146 cycles (TS) / 167
 // (SS, N <= 192) / 182 (SS, N = 256) whatever N, so a step is ~1030 cycles of
-// tensor pipe.
+// tensor pipe.  The epilogue (4 s32 regions -> fp32 -> y -> row max -> 3
+// digit bytes) is ~11 instructions per element and sets the pace: ~1500
+// cycles per tile-step at C4, both the FMA and the ALU pipe ~60 % busy
+// (ncu, profiles/r02_tc_fold_i8_ncu.md).  Rounding to the 24-bit X is done on
+// the FMA pipe (rint24x2): cvt.rni is an XU instruction at a quarter of the
+// rate and cost 34 % XU.  Tried and slower: 16 epilogue warps
+// alternating between the two slots of a 4-sample super-tile with a
+// dedicated issuer warp (62 ms vs 46 ms at C4): one slot's epilogue then
+// cannot overlap the other's.
 //
 // Scale bookkeeping: a chain row is c 2^E (fp32 c, integer E).  With y = c o d
 // and X = rint(y 2^sigma), the new row is c' 2^(E + 32 - sigma - tau).
@@ -98,10 +106,30 @@ __device__ __forceinline__ int row_sigma(float M) {
   return min(s, 126);
 }
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }   // e in [-126, 127]
-__device__ __forceinline__ int rni(float v) {
-  int r;
-  asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return r;
+// X = rint(y 2^sigma) as a 24-bit two's complement integer, on the FMA pipe
+// (cvt.rni is an XU instruction at a quarter of the rate; measured 34 % XU):
+//   F_hi = fma.rm(y, 2^(sigma-8), M) = M + floor(v / 256)          (M = 1.5 2^23, v = y 2^sigma)
+//   r    = fma(y, 2^sigma, 256 M - 256 F_hi) = v - 256 floor(v / 256)  in [0, 256), exact
+//   F_lo = r + 2^23 (RN)             = 2^23 + rint(r)               (rint(r) in [0, 256])
+//   (bits(F_hi) << 8) + bits(F_lo) = 0x8B000000 + X  (mod 2^32)
+// since 256 bits(M) = 0 mod 2^24 and bits(2^23) = 0x4B000000: its low three
+// bytes are X's (the carry of rint(r) = 256 included).
+__device__ __forceinline__ float2 ffma2_rm(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+// two elements at a time on the paired fp32 pipe (FFMA2 / FADD2)
+__device__ __forceinline__ void rint24x2(float2 y, float2 scl, float2 scl8, uint32_t& X0, uint32_t& X1) {
+  const float2 fh = ffma2_rm(y, scl8, make_float2(12582912.f, 12582912.f));
+  const float2 a = __ffma2_rn(fh, make_float2(-256.f, -256.f), make_float2(3221225472.f, 3221225472.f));
+  const float2 r = __ffma2_rn(y, scl, a);
+  const float2 fl = __fadd2_rn(r, make_float2(8388608.f, 8388608.f));
+  X0 = (__float_as_uint(fh.x) << 8) + __float_as_uint(fl.x);
+  X1 = (__float_as_uint(fh.y) << 8) + __float_as_uint(fl.y);
 }
 
 // W digits into the B tile (all threads).  tau: max|W| 2^tau in [2^30, 2^31 -
@@ -163,7 +191,7 @@ __device__ __forceinline__ void mma6_i8_commit(uint32_t d, const uint64_t (&ad)[
 
 // c' for 8 columns of this thread from the four s32 regions (TMEM columns
 // t0 + 64 r), combined once in fp32 RN
-__device__ __forceinline__ void regions_to_c(uint32_t t0, float (&c)[8]) {
+__device__ __forceinline__ void regions_to_c(uint32_t t0, float2 (&c)[4]) {
   uint32_t r0[8], r1[8], r2[8], r3[8];
   tmem_ld8(t0, r0);
   tmem_ld8(t0 + 64, r1);
@@ -171,10 +199,11 @@ __device__ __forceinline__ void regions_to_c(uint32_t t0, float (&c)[8]) {
   tmem_ld8(t0 + 192, r3);
   tmem_wait_ld();
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int S = (int)r0[i] * 256 + (int)r1[i];
-    const int T = (int)r2[i] * 256 + (int)r3[i];
-    c[i] = fmaf(__int2float_rn(T), 0x1p-16f, __int2float_rn(S));
+  for (int i = 0; i < 4; ++i) {
+    const int S0 = (int)r0[2 * i] * 256 + (int)r1[2 * i], S1 = (int)r0[2 * i + 1] * 256 + (int)r1[2 * i + 1];
+    const int T0 = (int)r2[2 * i] * 256 + (int)r3[2 * i], T1 = (int)r2[2 * i + 1] * 256 + (int)r3[2 * i + 1];
+    c[i] = __ffma2_rn(make_float2(__int2float_rn(T0), __int2float_rn(T1)), make_float2(0x1p-16f, 0x1p-16f),
+                      make_float2(__int2float_rn(S0), __int2float_rn(S1)));
   }
 }
 
@@ -299,14 +328,14 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
       cb ^= 1;
       uint32_t dp = hs_s + 4u * ((row >> 6) * I8_HCH * TH + 32 * cgp);   // this thread's d slice of step st
       for (int st = 0; st < n; ++st, dp += 4u * TH) {
-        float y[32];                                // y = c o d_t (this thread's 32 columns)
+        float2 y[16];                               // y = c o d_t (this thread's 32 columns)
         if (first) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
             const float4 d4 = lds128(dp + 16u * q4);
-            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) y[4 * q4 + e] = (32 * cgp + 4 * q4 + e == j && ok) ? dv[e] : 0.f;
+            const int k0 = 32 * cgp + 4 * q4;
+            y[2 * q4] = make_float2(k0 == j && ok ? d4.x : 0.f, k0 + 1 == j && ok ? d4.y : 0.f);
+            y[2 * q4 + 1] = make_float2(k0 + 2 == j && ok ? d4.z : 0.f, k0 + 3 == j && ok ? d4.w : 0.f);
           }
         } else {
           if (issuer) {
@@ -318,18 +347,19 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
           tc_fence_after();
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
-            float c[8];
+            float2 c[4];
             regions_to_c(t_mine + 8 * qq, c);
             const float4 da = lds128(dp + 32u * qq), db = lds128(dp + 32u * qq + 16u);
-            const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
-#pragma unroll
-            for (int i = 0; i < 8; ++i) y[8 * qq + i] = c[i] * dv[i];
+            y[4 * qq] = __fmul2_rn(c[0], make_float2(da.x, da.y));
+            y[4 * qq + 1] = __fmul2_rn(c[1], make_float2(da.z, da.w));
+            y[4 * qq + 2] = __fmul2_rn(c[2], make_float2(db.x, db.y));
+            y[4 * qq + 3] = __fmul2_rn(c[3], make_float2(db.z, db.w));
           }
         }
         first = false;
         float pm = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pm = fmaxf(pm, fabsf(y[i]));
+        for (int i = 0; i < 16; ++i) pm = fmaxf(pm, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
         const uint32_t redp = red0 + par * (TM * 8);
         asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
         named_bar(pair_bar, 64);
@@ -338,15 +368,16 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
         par ^= 1;
         const float M = __uint_as_float(max(m2[0], m2[1]));
         const int sig = M > 0.f ? row_sigma(M) : 0;
-        const float scl = pow2f(sig);
+        const float2 scl = make_float2(pow2f(sig), pow2f(sig)), scl8 = make_float2(pow2f(sig - 8), pow2f(sig - 8));
         if (M > 0.f) E += 32 - sig - tau;
         // X = rint(y 2^sigma) in [-2^23, 2^23): bytes 2, 1, 0 = digits x0 (s8), x1, x2 (u8);
         // words of 4 consecutive k per digit (7 byte permutes per 4 elements)
         uint32_t w0[8], w1[8], w2[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const uint32_t X0 = (uint32_t)rni(y[4 * u] * scl), X1 = (uint32_t)rni(y[4 * u + 1] * scl);
-          const uint32_t X2 = (uint32_t)rni(y[4 * u + 2] * scl), X3 = (uint32_t)rni(y[4 * u + 3] * scl);
+          uint32_t X0, X1, X2, X3;
+          rint24x2(y[2 * u], scl, scl8, X0, X1);
+          rint24x2(y[2 * u + 1], scl, scl8, X2, X3);
           const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
           const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
           w2[u] = prmt(p01, p23, 0x5410u);
@@ -368,7 +399,7 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
         }
       }
     }
-    float cfin[32];
+    float2 cfin[16];
     if (!first) {                                   // D of the tile's last step
       if (issuer) {
         if (lane == 0) mbar_wait(dbar, ph);
@@ -379,21 +410,22 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
       tc_fence_after();
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
-        float c[8];
+        float2 c[4];
         regions_to_c(t_mine + 8 * qq, c);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) cfin[8 * qq + i] = c[i];
+        for (int i = 0; i < 4; ++i) cfin[4 * qq + i] = c[i];
       }
     } else {                                        // an empty head block: the identity
 #pragma unroll
-      for (int k = 0; k < 32; ++k) cfin[k] = (32 * cgp + k == j) ? 1.f : 0.f;
+      for (int k = 0; k < 16; ++k)
+        cfin[k] = make_float2(32 * cgp + 2 * k == j ? 1.f : 0.f, 32 * cgp + 2 * k + 1 == j ? 1.f : 0.f);
     }
     if (ok) {
       float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 32 * cgp);
 #pragma unroll
       for (int k4 = 0; k4 < 8; ++k4)
-        dst[k4] = make_float4(ldexpf(cfin[4 * k4], E), ldexpf(cfin[4 * k4 + 1], E), ldexpf(cfin[4 * k4 + 2], E),
-                              ldexpf(cfin[4 * k4 + 3], E));
+        dst[k4] = make_float4(ldexpf(cfin[2 * k4].x, E), ldexpf(cfin[2 * k4].y, E), ldexpf(cfin[2 * k4 + 1].x, E),
+                              ldexpf(cfin[2 * k4 + 1].y, E));
     }
   }
   tc_fence_before();
