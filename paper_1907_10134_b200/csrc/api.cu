@@ -404,7 +404,9 @@ bppsa_status run_down(const bppsa_jac& j, int head, const float* seed, const Pla
     if (l == 0 && j.kind != BPPSA_JAC_DENSE) {
       // tcgen05 walk: many short chains (the linear scan's single long chain per
       // sample stays on the CUDA cores; so do single-block segments)
-      if (use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8 && (!e_aff || j.B <= 128))
+      if (!e_aff && leaf_engine(j, p.leaf_impl) == kInt8 && nblk >= 2)
+        e = launch_tc_walk_i8(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st);
+      else if (use_tensor_walk(j, p.leaf_impl) && nblk >= 2 && Cl >= 8 && (!e_aff || j.B <= 128))
         e = launch_tc_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, num_sms(), st, e_aff);
       else
         e = launch_leaf_down(leaf_args(j, head, seed), Cl, carry, nblk, grad_h, grad_init, st, e_aff);

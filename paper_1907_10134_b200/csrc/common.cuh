@@ -101,6 +101,9 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
 // exact-integer tensor-core fold (tc_i8.cu): RNN, H == 64, blocks q in [q0, n_out)
 cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, int num_sms,
                               cudaStream_t st);
+// exact-integer tensor-core walk (tc_i8.cu): RNN, H == 64; carries [B][nblk][H] (head: the seed)
+cudaError_t launch_tc_walk_i8(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
+                              float* grad_init, int num_sms, cudaStream_t st);
 // level-1 head slot: column-major H = 64 matrix at lvl + b*bstride -> M . seed_b (in place)
 cudaError_t launch_head_apply(float* lvl, long long bstride, const float* seed, int B, int H, cudaStream_t st);
 // e / vec_out / head_out: the affine terms as for launch_leaf_down (B <= 128)

@@ -207,6 +207,15 @@ __device__ __forceinline__ void regions_to_c(uint32_t t0, float2 (&c)[4]) {
   }
 }
 
+#ifdef BPPSA_I8_TRACE
+// dev aid: clock64 per step on CTA 0 (warp 0, lane 0): [event][step]
+__device__ long long g_i8_trace[12][2048];
+#define I8T(ev, i) \
+  if (blockIdx.x == 0 && lane == 0 && (i) < 2048) g_i8_trace[ev][i] = clock64();
+#else
+#define I8T(ev, i)
+#endif
+
 __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
                                                             long long n_out, long long q0) {
   extern __shared__ uint8_t smem_raw[];
@@ -436,7 +445,312 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Level-0 DOWN-walk on the integer tensor cores (the down-sweep's GEMV chains,
+// every down-sweep op is a vector times the transposed Jacobians).
+// Chain (b, q) starts from the carry of block q (the seed for the head
+// block), writes the exclusive output grad_h[t(s)] = v at every slot s of the
+// block and steps v <- W^T (d_t o v) with the same digit arithmetic as the
+// fold (v kept in true fp32 scale: v = c' 2^(32 - sigma - tau)).  The walk
+// is bound by HBM (h read + grad_h written once) and by the latency of its
+// dependent steps, not by the tensor pipe, so it runs ONE 128-chain tile per
+// SM with the digits in TMEM (the TS form: 146 instead of ~170 cycles per
+// MMA, no shared-memory round trip): D at TMEM columns [0, 256), the three
+// digit tiles at [256, 304).  16 warps, thread = chain row x 16 columns.
+// Chains are ordered id = q B + b, so at one step a tile's h rows (and
+// grad_h rows) are a few contiguous runs of B rows; all threads copy them in
+// and out COALESCED (each warp instruction moves 512 contiguous bytes)
+// through shared memory with padded 272-byte rows, so the per-chain column
+// slices are read and written without bank conflicts (per-thread 128-byte
+// global accesses at a 256-byte stride measured 3300 cycles per step).  The
+// copies (h two steps ahead into a 4-stage ring, the previous step's grad_h
+// out of a double-buffered staging area) run while the step's MMAs do.
+// ---------------------------------------------------------------------------
+constexpr int WK_NST = 4;                           // h ring stages (prefetch distance 2)
+constexpr int WK_PF = 2;
+constexpr int WK_EPI = 512;                         // 16 warps: thread = chain row x 16 columns
+constexpr int WK_ROW = 272;                         // padded row: 256 B + 16
+constexpr int WK_STAGE = TM * WK_ROW;
+constexpr int WK_OFF_RING = I8_B_BYTES;             // [stage][128 rows][WK_ROW]
+constexpr int WK_OFF_OUT = WK_OFF_RING + WK_NST * WK_STAGE;   // grad_h staging [2][128 rows][WK_ROW]
+constexpr int WK_OFF_RED = WK_OFF_OUT + 2 * WK_STAGE;         // [parity][128 rows][4] u32
+constexpr int WK_OFF_BAR = WK_OFF_RED + 2 * TM * 16;
+constexpr int WK_SMEM = WK_OFF_BAR + 64 + 1024;
+constexpr uint32_t WK_A_COL = 256;                  // TMEM column of the x0 digit tile (x1 +16, x2 +32)
+constexpr int WK_CP = TM / (WK_EPI / 16);           // copy passes per tile (16 lanes per row)
+
+__device__ __forceinline__ void mma6_i8_ts_commit(uint32_t d, uint32_t a, const uint64_t (&bd)[2], uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 dd, aa;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, f;\n"
+      " add.u32 aa, %1, 8;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [aa], %3, %4, t;\n"
+      " add.u32 dd, %0, 64;\n"
+      " add.u32 aa, %1, 16;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [dd], [aa], %2, %5, t;\n"
+      " add.u32 aa, %1, 24;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [dd], [aa], %3, %5, t;\n"
+      " add.u32 dd, %0, 128;\n"
+      " add.u32 aa, %1, 32;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [dd], [aa], %2, %6, t;\n"
+      " add.u32 aa, %1, 40;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [dd], [aa], %3, %6, t;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n"
+      "}\n" ::"r"(d),
+      "r"(a), "l"(bd[0]), "l"(bd[1]), "r"(idesc_i8(256, 1)), "r"(idesc_i8(192, 0)), "r"(idesc_i8(128, 0)), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(r0), "r"(r1), "r"(r2),
+               "r"(r3)
+               : "memory");
+}
+// 2^e as a float for any integer e (0 below the denormal range, inf above)
+__device__ __forceinline__ float exp2i(int e) {
+  if (e > 127) return __int_as_float(0x7f800000);
+  if (e >= -126) return __int_as_float((e + 127) << 23);
+  if (e >= -149) return __int_as_float(1 << (e + 149));
+  return 0.f;
+}
+
+__global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8_kernel(LeafArgs a, int C, const float* __restrict__ carry,
+                                                             long long nblk, float* __restrict__ grad_h,
+                                                             float* __restrict__ grad_init) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + WK_OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_full + 1);
+  uint32_t* wred = tmem_slot + 1;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nch = (long long)B * nblk, ntiles = (nch + TM - 1) / TM;
+
+  if (threadIdx.x == 0) wred[0] = 0;
+  __syncthreads();
+  int tau;
+  w_digits(a.W, smem, wred, &tau);
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(su32(&d_full[0]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int quad = warp & 3, row = quad * 32 + lane, cq = warp >> 2;   // columns [16 cq, 16 cq + 16)
+  const bool issuer = warp == 0;
+  const uint32_t t_mine = tmem + ((uint32_t)(quad * 32) << 16) + 16 * cq;   // + 64 r (regions)
+  const uint32_t a_mine = tmem + ((uint32_t)(quad * 32) << 16) + WK_A_COL + 4 * cq;   // + 16 digit
+  const uint32_t ring0 = su32(smem + WK_OFF_RING);
+  const uint32_t out0 = su32(smem + WK_OFF_OUT);
+  const uint32_t mine = (uint32_t)(row * WK_ROW + cq * 64);               // this thread's slice in a stage
+  const uint32_t red0 = su32(smem + WK_OFF_RED) + (uint32_t)(row * 16);
+  const uint32_t dbar = su32(&d_full[0]);
+  uint64_t bd[2];
+  {
+    const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+    bd[0] = sdesc64(bb);
+    bd[1] = sdesc64(bb + 32);
+  }
+  const uint32_t a_tile = __shfl_sync(0xffffffffu, tmem + WK_A_COL, 0);
+  uint32_t ph = 0, par = 0;
+  const long long rowB = (long long)B * TH;
+  auto blk = [&](long long q, long long& st0, long long& st1) {   // slots [st0, st1) of block q
+    st0 = (a.seg.head && q == 0) ? 1 : q * C;
+    st1 = min(q * C + (long long)C, S);
+  };
+  // coalesced copy roles: 16 lanes per 256-byte row (16 bytes each), 32 rows per pass
+  const int crow = threadIdx.x >> 4, cchunk = threadIdx.x & 15;
+  for (long long tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+    const long long id = tt * TM + row;
+    const bool valid = id < nch;
+    const long long q = valid ? id / B : 0;
+    const int b = valid ? (int)(id % B) : 0;
+    long long s_start, s1;
+    blk(q, s_start, s1);
+    const int len = valid ? (int)(s1 - s_start) : 0;
+    const bool total = valid && grad_init != nullptr && s1 == S;
+    const int nJ = total ? len : max(len - 1, 0);          // J applications of this chain
+    int steps = 0;                                         // the longest chain of the tile
+    {
+      const long long q_lo = (tt * TM) / B, q_hi = min(nblk - 1, (tt * TM + TM - 1) / B);
+      for (long long qq = q_lo; qq <= q_hi; ++qq) {
+        long long a0, a1;
+        blk(qq, a0, a1);
+        steps = max(steps, (int)(a1 - a0));
+      }
+    }
+    // this thread's copy rows r = 32 pass + crow: slot start, length, sample
+    int cr_s0[WK_CP], cr_len[WK_CP], cr_b[WK_CP];
+#pragma unroll
+    for (int pass = 0; pass < WK_CP; ++pass) {
+      const long long cid = tt * TM + pass * 32 + crow;
+      cr_len[pass] = 0, cr_s0[pass] = 0, cr_b[pass] = 0;
+      if (cid < nch) {
+        long long c0, c1;
+        blk(cid / B, c0, c1);
+        cr_s0[pass] = (int)c0;
+        cr_len[pass] = (int)(c1 - c0);
+        cr_b[pass] = (int)(cid % B);
+      }
+    }
+    auto row_off = [&](int pass, int st) -> long long {    // h / grad_h offset of copy row `pass`, or -1
+      if (st >= cr_len[pass]) return -1;
+      return (long long)a.seg.time_of(cr_s0[pass] + st) * rowB + (long long)cr_b[pass] * TH;
+    };
+    auto stage = [&](int st) {                             // h rows of step st -> ring stage st % 4
+      const uint32_t dst0 = ring0 + (uint32_t)((st % WK_NST) * WK_STAGE);
+#pragma unroll
+      for (int pass = 0; pass < WK_CP; ++pass) {
+        const long long off = row_off(pass, st);
+        if (off >= 0) cp_async16(dst0 + (uint32_t)((pass * 32 + crow) * WK_ROW + cchunk * 16), a.h + off + cchunk * 4);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");   // one group per step, empty or not
+    };
+    auto copy_out = [&](int st) {                          // staged grad_h rows of step st -> HBM
+      const uint32_t src0 = out0 + (uint32_t)((st & 1) * WK_STAGE);
+#pragma unroll
+      for (int pass = 0; pass < WK_CP; ++pass) {
+        const long long off = row_off(pass, st);
+        if (off >= 0)
+          reinterpret_cast<float4*>(grad_h + off)[cchunk] = lds128(src0 + (uint32_t)((pass * 32 + crow) * WK_ROW + cchunk * 16));
+      }
+    };
+    float2 v[8];                                    // this thread's 16 columns of the chain (true scale)
+    {
+      const float* src = (a.seg.head && q == 0) ? a.seed + (long long)b * TH : carry + ((long long)b * nblk + q) * TH;
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const float4 f = valid ? __ldg(reinterpret_cast<const float4*>(src + 16 * cq) + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[2 * k4] = make_float2(f.x, f.y);
+        v[2 * k4 + 1] = make_float2(f.z, f.w);
+      }
+    }
+    for (int st = 0; st < WK_PF; ++st) stage(st);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(WK_PF - 1) : "memory");   // step 0's rows (this thread's)
+    __syncthreads();                                       // ... and everyone's
+    for (int st = 0; st < steps; ++st) {
+      const int tz = (int)(tt / gridDim.x) * 600 + st;
+      if (warp == 0) I8T(0, tz);
+      const uint32_t hs = ring0 + (uint32_t)((st % WK_NST) * WK_STAGE) + mine;
+      const bool apply = st < nJ;
+      float2 y[8];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 h4 = lds128(hs + 16u * c);
+        const float2 d0 = make_float2(fmaf(-h4.x, h4.x, 1.f), fmaf(-h4.y, h4.y, 1.f));
+        const float2 d1 = make_float2(fmaf(-h4.z, h4.z, 1.f), fmaf(-h4.w, h4.w, 1.f));
+        y[2 * c] = apply ? __fmul2_rn(d0, v[2 * c]) : make_float2(0.f, 0.f);
+        y[2 * c + 1] = apply ? __fmul2_rn(d1, v[2 * c + 1]) : make_float2(0.f, 0.f);
+      }
+      float pm = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pm = fmaxf(pm, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
+      const uint32_t redp = red0 + par * (TM * 16);
+      asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cq), "r"(__float_as_uint(pm)) : "memory");
+      if (warp == 0) I8T(3, tz);
+      named_bar(3 + quad, 128);                     // the row's four threads (warps quad + 4 cq)
+      if (warp == 0) I8T(4, tz);
+      uint32_t m4[4];
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(m4[0]), "=r"(m4[1]), "=r"(m4[2]), "=r"(m4[3])
+                   : "r"(redp)
+                   : "memory");
+      par ^= 1;
+      const float M = __uint_as_float(max(max(m4[0], m4[1]), max(m4[2], m4[3])));
+      const int sig = M > 0.f ? row_sigma(M) : 0;
+      const float2 scl = make_float2(pow2f(sig), pow2f(sig)), scl8 = make_float2(pow2f(sig - 8), pow2f(sig - 8));
+      const float f = M > 0.f ? exp2i(32 - sig - tau) : 0.f;
+      uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t X0, X1, X2, X3;
+        rint24x2(y[2 * u], scl, scl8, X0, X1);
+        rint24x2(y[2 * u + 1], scl, scl8, X2, X3);
+        const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
+        const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
+        w2[u] = prmt(p01, p23, 0x5410u);
+        w1[u] = prmt(p01, p23, 0x7632u);
+        w0[u] = prmt(q01, q23, 0x5410u);
+      }
+      if (warp == 0) I8T(5, tz);
+      tmem_st4(a_mine, w0[0], w0[1], w0[2], w0[3]);
+      tmem_st4(a_mine + 16, w1[0], w1[1], w1[2], w1[3]);
+      tmem_st4(a_mine + 32, w2[0], w2[1], w2[2], w2[3]);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tc_fence_before();
+      named_bar(1, WK_EPI);                         // digits complete
+      if (warp == 0) I8T(7, tz);
+      if (issuer) {
+        tc_fence_after();
+        mma6_i8_ts_commit(tmem, a_tile, bd, dbar);
+      }
+      // while the MMAs run: grad_h of this slot (= v, the exclusive output) into
+      // staging, the previous step's rows out, the rows of step st+2 in
+      {
+        const uint32_t o = out0 + (uint32_t)((st & 1) * WK_STAGE) + mine;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sts128(o + 16u * c, v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
+      }
+      if (st > 0) copy_out(st - 1);
+      stage(st + WK_PF);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(WK_PF - 1) : "memory");   // step st+1's rows (this thread's)
+      if (issuer) {
+        if (lane == 0) mbar_wait(dbar, ph);
+        __syncwarp();
+      }
+      named_bar(2, WK_EPI);                         // D ready; step st+1's rows landed; staging written
+      if (warp == 0) I8T(8, tz);
+      ph ^= 1;
+      tc_fence_after();
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        float2 c[4];
+        regions_to_c(t_mine + 8 * qq, c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[4 * qq + i] = __fmul2_rn(c[i], make_float2(f, f));
+      }
+      if (warp == 0) I8T(9, tz);
+      if (total && st == len - 1) {                 // dl/dh_init = J_0^T grad_h[0]
+        float4* dst = reinterpret_cast<float4*>(grad_init + (long long)b * TH + 16 * cq);
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) dst[k4] = make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+      }
+    }
+    if (steps > 0) copy_out(steps - 1);             // (staged before the last D barrier)
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 }  // namespace
+
+#ifdef BPPSA_I8_TRACE
+extern "C" int bppsa_debug_i8_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_i8_trace, sizeof(g_i8_trace));
+}
+#endif
 
 // Matrix blocks q in [q0, n_out) of an RNN H = 64 segment, exact-integer fold.
 cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, int num_sms,
@@ -448,6 +762,19 @@ cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long lon
   cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_fold_i8_kernel), I8_SMEM);
   if (e != cudaSuccess) return e;
   tc_fold_i8_kernel<<<grid, I8_NT, I8_SMEM, st>>>(a, C, agg_out, n_out, q0);
+  return cudaGetLastError();
+}
+
+// Level-0 walk of an RNN H = 64 segment on the integer tensor cores.
+cudaError_t launch_tc_walk_i8(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
+                              float* grad_init, int num_sms, cudaStream_t st) {
+  if (a.seg.H != TH) return cudaErrorInvalidValue;
+  const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
+  const int grid = (int)std::min<long long>(ntiles, num_sms);
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_walk_i8_kernel), WK_SMEM);
+  if (e != cudaSuccess) return e;
+  tc_walk_i8_kernel<<<grid, WK_EPI, WK_SMEM, st>>>(a, C, carry, nblk, grad_h, grad_init);
   return cudaGetLastError();
 }
 
