@@ -9,11 +9,12 @@ reset (a3) + down-sweep (a4) + carry exchange (a5, N > 1) + weight gradients
 configuration BASELINE.json shards across 1/2/4/8 B200s (strong scaling: the
 total sequence is fixed, rank r owns T/N contiguous steps).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload c4|c1|c2|c3]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--quick]
 
-Rank 0 prints ONE JSON line.  `--impl reference` times the fp64 CPU oracle
-(oracle/, the reference arm of this tier) on a bounded sample of the same
-workload, extrapolated to the full workload.
+Rank 0 prints ONE JSON line.  With --gpus N > 1 and no torchrun environment
+the script relaunches itself as N ranks (torch.distributed.run, 127.0.0.1).
+`--impl reference` times the fp64 CPU oracle (oracle/, the reference arm of
+this tier) on the full C4 workload once (steps = 1).
 """
 from __future__ import annotations
 
@@ -52,8 +53,36 @@ FP32_LANES_PER_SM, N_SM = 128, 148
 
 
 def c4_inputs(seed: int = 0):
+    """C4 inputs through the host numpy forward (the parity tests' inputs)."""
     import bppsa_workloads as W
     return W.rnn_workload(C4["T"], C4["B"], C4["H"], seed=seed, I=C4["I"])
+
+
+def c4_inputs_gpu(seed: int, dev):
+    """C4 inputs for the bench, same recipe as bppsa_workloads.rnn_workload
+    (seeded bitstreams, torch-default init, fp32 forward, mean-CE head seed)
+    but with the forward on the GPU: torch nn.RNN (cuDNN, TF32 off) over
+    32768-step chunks carrying the state, so every rank builds its inputs in
+    well under a second instead of a 2^20-step host loop.  Returns device x,
+    h (full length) and host params / seed."""
+    import torch
+    import bppsa_workloads as W
+    T, B, H, I = C4["T"], C4["B"], C4["H"], C4["I"]
+    x_np, labels = W.bitstreams(T, B, seed)
+    p = W.rnn_params(H, I, 10, seed + 1)
+    rnn = torch.nn.RNN(I, H, nonlinearity="tanh").to(dev)
+    with torch.no_grad():
+        for name, key in (("weight_ih_l0", "W_ih"), ("weight_hh_l0", "W_hh"), ("bias_ih_l0", "b_ih"),
+                          ("bias_hh_l0", "b_hh")):
+            getattr(rnn, name).copy_(torch.from_numpy(p[key]))
+        x = torch.from_numpy(x_np).to(dev)
+        h = torch.empty((T, B, H), device=dev)
+        state = torch.zeros((1, B, H), device=dev)
+        for t0 in range(0, T, 1 << 15):
+            out, state = rnn(x[t0:t0 + (1 << 15)], state)
+            h[t0:t0 + out.shape[0]] = out
+    g = W.head_seed(h[-1].cpu().numpy(), p["W_out"], p["b_out"], labels)
+    return x, h, p, g
 
 
 def peaks():
@@ -145,6 +174,55 @@ def level0_flops(T: int, B: int, H: int, C0: int, head: bool) -> float:
     return B * (gemm * 2.0 * H ** 3 + gemv * 2.0 * H ** 2 + T * H ** 2)
 
 
+def scan_alg_counts(T: int, B: int, H: int, I: int = 1, gru: bool = False):
+    """Algorithmic work of one full backward: Alg. 1's n - L
+    GEMMs (2H^3) and n - 1 GEMVs (2H^2) per sample (n = T slots of leaves,
+    L = ceil(log2(n + 1))), the leaves (H^2 per step RNN, 6H^2 + H GRU), the
+    weight gradients 2 B T H (H + I + 1) (x3 GRU); fused bytes: activations
+    read once + grad_h written once (8H per element RNN, 24H GRU) + the
+    weight-gradient reads 4 B T (2H + I)."""
+    n, L = T, max(1, math.ceil(math.log2(T + 1)))
+    leaf = (6 * H * H + H) if gru else H * H
+    scan = B * ((n - L) * 2.0 * H ** 3 + (n - 1) * 2.0 * H ** 2 + n * leaf)
+    wg = (3 if gru else 1) * 2.0 * B * T * H * (H + I + 1)
+    bytes_ = B * T * ((24 if gru else 8) * H) + 4.0 * B * T * (2 * H + I)
+    return scan + wg, bytes_
+
+
+def graph_launch_us(n: int = 64):
+    """Latency floor unit: one dependent kernel node of a replayed CUDA graph
+    (tiny kernels back to back on one stream), measured on this GPU."""
+    import torch
+    a = torch.zeros(1, device="cuda")
+
+    def chain():
+        for _ in range(n):
+            a.add_(1.0)
+    chain()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(gr, stream=s):
+            chain()
+    torch.cuda.synchronize()
+    return _time(gr.replay, reps=20) * 1e3 / n
+
+
+def roofline_small(ms: float, flops: float, bytes_: float, launches: int, launch_us: float, pk: dict):
+    """ALU (FFMA pipe), HBM and latency-floor fractions of a latency-bound config."""
+    return {"bound": "latency",
+            "alu": {"achieved_tflops": round(flops / (ms * 1e-3) / 1e12, 3), "peak_tflops": round(pk["fp32_tflops"], 1),
+                    "frac": round(flops / (ms * 1e-3) / 1e12 / pk["fp32_tflops"], 4)},
+            "hbm": {"achieved_gbs": round(bytes_ / (ms * 1e-3) / 1e9, 1), "peak_gbs": pk["hbm_gbs"],
+                    "frac": round(bytes_ / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], 4)},
+            "latency_floor_ms": round(launches * launch_us * 1e-3, 4), "launches": launches,
+            "launch_us": round(launch_us, 3),
+            "frac": round(launches * launch_us * 1e-3 / ms, 4),
+            "algorithmic_flops": flops, "algorithmic_bytes": bytes_}
+
+
 def load_traffic(kernel: str):
     f = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(f):
@@ -179,15 +257,20 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     T, B, H, I = C4["T"], C4["B"], C4["H"], C4["I"]
-    w = c4_inputs(args.seed)
     lo, hi = shard_bounds(T, world)[rank]
     head = rank == world - 1
     dev = torch.device("cuda", local)
-    h = torch.from_numpy(w.h[lo:hi]).to(dev)
-    x = torch.from_numpy(w.x[lo:hi]).to(dev)
-    Whh = torch.from_numpy(w.W_hh).to(dev)
-    g = torch.from_numpy(w.g).to(dev) if head else None
-    h_init = torch.from_numpy(w.h[lo - 1]).to(dev) if lo > 0 else None
+    x_full, h_full, params, g_np = c4_inputs_gpu(args.seed, dev)
+    h = h_full[lo:hi].clone()                 # this rank's shard only
+    x = x_full[lo:hi].clone()
+    h_init = h_full[lo - 1].clone() if lo > 0 else None
+    Whh = torch.from_numpy(params["W_hh"]).to(dev)
+    g = torch.from_numpy(g_np).to(dev) if head else None
+    host = None
+    if world == 1 and not args.quick:         # e2e / sequential baselines need host copies
+        host = dict(h=h_full.cpu().numpy(), x=x_full.cpu().numpy(), W_hh=params["W_hh"], g=g_np)
+    del x_full, h_full
+    torch.cuda.empty_cache()
     Tl = hi - lo
     jac = api.jacobians_rnn(h, Whh)
     grad = torch.empty((Tl, B, H), device=dev)
@@ -245,27 +328,30 @@ def run_ours(args):
         pk = peaks()
         flops = level0_flops(Tl, B, H, b0, head)
         achieved = flops / (k0m * 1e-3) / 1e12
-        # the level-0 fold runs on tcgen05 as 3xFP16 (x = x1 + x2, W = W1 + W2 in
-        # fp16 with power-of-two row scaling; kind::f16, fp32 accumulate): every
-        # algorithmic fp32 flop costs 3 fp16 tensor flops (x1W1, x1W2, x2W1; the
-        # x2W2 term the N-stacked B also produces is not counted as useful);
-        # fp16 dense peak = the measured bf16 peak (same rate, B200_PROFILING.md)
-        peak = pk["bf16_tflops"] / 3.0
+        # the level-0 fold runs on tcgen05 kind::i8 with exact s32 accumulation:
+        # x as 3 and W as 4 8-bit digits, the digit products with i + j <= 3 =
+        # 9 int8 MACs per fp32 MAC (tc_i8.cu); int8 dense peak = 2 x the
+        # measured bf16 peak (B200_PROFILING.md: fp8/int8 4.5 vs bf16 2.25 PF
+        # nominal), so the fp32-faithful peak of this kernel is that / 9
+        i8_peak = 2.0 * pk["bf16_tflops"]
+        peak = i8_peak / 9.0
         result["roofline"] = {"bound": "tensor",
-                              "kernel": "tc_leaf_up_f16_kernel (level-0 fused fold, tcgen05 3xFP16 row-scaled)",
+                              "kernel": "tc_fold_i8_kernel (level-0 fused fold, tcgen05 kind::i8, exact s32 "
+                                        "accumulation of 8-bit digit products)",
                               "achieved": round(achieved, 3), "peak": round(peak, 2),
                               "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                               # the ncu capture is of the single-GPU launch (T = 2^20)
-                              "traffic": load_traffic("tc_leaf_up") if world == 1 else None,
+                              "traffic": load_traffic("tc_fold_i8") if world == 1 else None,
                               "algorithmic_flops_per_launch": flops,
-                              "peak_note": "fp32-accurate 3xFP16 peak = measured bf16/fp16 dense %.1f TF (%s) / 3 "
-                                           "products; for comparison 3xTF32 peak %.1f TF, FFMA-pipe peak %.1f TF"
-                                           % (pk["bf16_tflops"], pk["source"], pk["bf16_tflops"] * 0.5 / 3.0,
-                                              pk["fp32_tflops"]),
+                              "peak_note": "fp32-faithful int8-digit peak = 2 x measured bf16 dense %.1f TF (%s) "
+                                           "= %.1f int8 TOPS / 9 digit products per fp32 MAC; for comparison the "
+                                           "FFMA-pipe peak %.1f TF (exact fp32 on CUDA cores) and the biased "
+                                           "3xFP16 peak %.1f TF" % (pk["bf16_tflops"], pk["source"], i8_peak,
+                                                                   pk["fp32_tflops"], pk["bf16_tflops"] / 3.0),
                               "share_of_step": round(k0m / ms, 4)}
     if world == 1 and not args.quick:
-        result["e2e"] = e2e_ours(api, w, args)
-        result["sequential_bp"] = sequential_baselines(api, w, args)
+        result["e2e"] = e2e_ours(api, host, args)
+        result["sequential_bp"] = sequential_baselines(api, host, args)
         result["sweep"] = sweep_small(api, args)
         # NEXT-4: the affine scan (a loss on every step) on the same C4 inputs
         gen = torch.Generator(device=dev).manual_seed(args.seed)
@@ -311,10 +397,10 @@ def e2e_ours(api, w, args):
     import torch
     from paper_1907_10134_b200.stream import StreamedRnnBackward
     T, B, H, I = C4["T"], C4["B"], C4["H"], C4["I"]
-    hp = torch.from_numpy(w.h).pin_memory()
-    xp = torch.from_numpy(w.x).pin_memory()
-    Wp = torch.from_numpy(w.W_hh).pin_memory()
-    gp = torch.from_numpy(w.g).pin_memory()
+    hp = torch.from_numpy(w["h"]).pin_memory()
+    xp = torch.from_numpy(w["x"]).pin_memory()
+    Wp = torch.from_numpy(w["W_hh"]).pin_memory()
+    gp = torch.from_numpy(w["g"]).pin_memory()
     outs_h = [torch.empty(s, pin_memory=True) for s in ((H, I), (H, H), (H,), (B, H))]
     chunks = 16
     sb = StreamedRnnBackward(T, B, H, I, chunks=chunks, block0=C4_BLOCK0, block=C4_BLOCK)
@@ -382,9 +468,9 @@ def sequential_baselines(api, w, args):
     T = 2^16; its backward is linear in T)."""
     import torch
     T, B, H = C4["T"], C4["B"], C4["H"]
-    h = torch.from_numpy(w.h).cuda()
-    Whh = torch.from_numpy(w.W_hh).cuda()
-    g = torch.from_numpy(w.g).cuda()
+    h = torch.from_numpy(w["h"]).cuda()
+    Whh = torch.from_numpy(w["W_hh"]).cuda()
+    g = torch.from_numpy(w["g"]).cuda()
     jac = api.jacobians_rnn(h, Whh)
     grad = torch.empty((T, B, H), device="cuda")
     ws = api.workspace(api.scan_workspace_size(jac, "linear"))
@@ -432,6 +518,9 @@ def sweep_small(api, args):
     import torch
     import bppsa_workloads as W
     out = {}
+    pk = peaks()
+    launch_us = graph_launch_us()
+    out["graph_node_us"] = round(launch_us, 3)
     for name, c in SMALL.items():
         w = W.rnn_workload(c["T"], c["B"], c["H"], seed=1)
         h, x = torch.from_numpy(w.h).cuda(), torch.from_numpy(w.x).cuda()
@@ -465,9 +554,16 @@ def sweep_small(api, args):
             graph_ms = f"capture failed: {ex}"[:120]
         lin = _time(lambda: api.scan(jac, g, grad_h=grad, ws=wsl, mode="linear"), reps=5)
         cud = cudnn_backward_ms(c["T"], c["B"], c["H"], 1, reps=5)
+        tr = api.LaunchTrace(64)
+        api.scan(jac, g, grad_h=grad, ws=ws, block0=c["block0"], block=c["block"], trace=tr)
+        torch.cuda.synchronize()
+        nl = tr.launches + 2                      # + the weight-gradient partials and reduction
+        flops, bytes_ = scan_alg_counts(c["T"], c["B"], c["H"])
+        best = graph_ms if not isinstance(graph_ms, str) else eager
         out[name] = {"T": c["T"], "B": c["B"], "H": c["H"], "bppsa_ms_eager": round(eager, 4),
                      "bppsa_ms_graph": graph_ms if isinstance(graph_ms, str) else round(graph_ms, 4),
-                     "gpu_linear_scan_ms": round(lin, 4), "cudnn_backward_ms": round(cud, 4)}
+                     "gpu_linear_scan_ms": round(lin, 4), "cudnn_backward_ms": round(cud, 4),
+                     "roofline": roofline_small(best, flops, bytes_, nl, launch_us, pk)}
     # config 3: GRU, H = 20, IRMAS L set (1034 x 12), B = 64
     gw = W.gru_workload("L", 64, seed=2)
     tape = {k: torch.from_numpy(v).cuda() for k, v in gw.tape.items()}
@@ -482,9 +578,15 @@ def sweep_small(api, args):
         api.scan(jac, g, grad_h=grad, ws=ws, block0=16, block=16)
         api.weight_grads_gru(x, tape, grad, ws=ws_w)
 
-    out["c3"] = {"set": "L (1034 x 12)", "B": 64, "H": 20, "bppsa_ms_eager": round(_time(bwd_gru), 4),
-                 "cudnn_backward_ms": round(cudnn_backward_ms(1034, 64, 20, 12, reps=5, x=gw.x, gru=True), 4)}
-    out["c5"] = sweep_csr(api)
+    t3 = _time(bwd_gru)
+    tr = api.LaunchTrace(64)
+    api.scan(jac, g, grad_h=grad, ws=ws, block0=16, block=16, trace=tr)
+    torch.cuda.synchronize()
+    flops, bytes_ = scan_alg_counts(1034, 64, 20, I=12, gru=True)
+    out["c3"] = {"set": "L (1034 x 12)", "B": 64, "H": 20, "bppsa_ms_eager": round(t3, 4),
+                 "cudnn_backward_ms": round(cudnn_backward_ms(1034, 64, 20, 12, reps=5, x=gw.x, gru=True), 4),
+                 "roofline": roofline_small(t3, flops, bytes_, tr.launches + 2, launch_us, pk)}
+    out["c5"] = sweep_csr(api, pk)
     out["train"] = sweep_train()
     out["hybrid"] = sweep_hybrid(api)
     out["jacgen"] = sweep_jacgen(api)
@@ -642,7 +744,7 @@ def sweep_train():
     return out
 
 
-def sweep_csr(api):
+def sweep_csr(api, pk=None):
     """Config 5: 97 %-pruned VGG-11 conv stack, B = 16, CSR transposed
     Jacobians.  Hybrid schedules (u, dl) vs the linear SpMV chain (0, 0)."""
     import torch
@@ -665,8 +767,19 @@ def sweep_csr(api):
         steps = api.csr_plan_steps(plan)       # fig:prune_symbolic static FLOP analysis
         scan_st = [x for x in steps if x["phase"] != "bp"]
         bp_st = [x for x in steps if x["phase"] == "bp"]
+        # HBM roofline: every planned contribution reads its two
+        # (position, position) int32 plan entries (8 B) and gathers B floats of
+        # each operand (2 x 4 B x B); every SpMV nnz reads its CSR index + value
+        # (8 B) and B floats of the vector; every output element is written once
+        Bb = 16
+        out_el = sum(int(d) for d in plan.dims) * Bb
+        c_bytes = info["contributions"] * (8 + 8 * Bb) + info["spmv_nnz"] * (8 + 4 * Bb) + out_el * 4
+        hbm = pk["hbm_gbs"] if pk else 6527.0
+        res_roof = {"bound": "hbm", "algorithmic_bytes": c_bytes,
+                    "achieved_gbs": round(c_bytes / (ms * 1e-3) / 1e9, 1), "peak_gbs": hbm,
+                    "frac": round(c_bytes / (ms * 1e-3) / 1e9 / hbm, 4)}
         res[f"u{sched[0]}_dl{sched[1]}"] = {
-            "scan_ms": round(ms, 4), "plan_build_s": round(t_plan, 2),
+            "scan_ms": round(ms, 4), "plan_build_s": round(t_plan, 2), "roofline": res_roof,
             "contributions": info["contributions"], "spmv_nnz": info["spmv_nnz"],
             "kernels": info["kernels"], "ws_GB": round(ws.numel() / 1e9, 3),
             "flops_per_sample": {"bppsa_total": sum(x["flops"] for x in scan_st),
@@ -683,9 +796,39 @@ def sweep_csr(api):
 
 
 # ----------------------------------------------------------------------------- reference arm
+def host_cpu():
+    """lscpu model name and logical CPUs of the host the oracle runs on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+def _oracle_samples(args):
+    """Worker of the OpenMP-style secondary: sequential BP of a slice of the samples."""
+    import bppsa_workloads as W
+    from oracle import bp
+    from threadpoolctl import threadpool_limits
+    Ts, b0, b1, seed = args
+    with threadpool_limits(limits=1):
+        w = W.rnn_workload(Ts, C4["B"], C4["H"], seed=seed)
+        t0 = time.perf_counter()
+        ref, _ = bp.bp_rnn(w.h[:, b0:b1], w.W_hh, w.g[b0:b1])
+        bp.weight_grads_rnn(w.x[:, b0:b1], w.h[:, b0:b1], ref)
+        return time.perf_counter() - t0
+
+
 def oracle_sample(budget_s: float = 12.0, seed: int = 0):
     """Time the oracle (fp64 numpy sequential BP + weight grads) single-threaded
-    on a T-sample of config 4 sized for ~budget_s, extrapolated linearly in T."""
+    on a T-sample of config 4 sized for ~budget_s, extrapolated linearly in T;
+    secondary: the same sample split over the B samples across processes
+    (sequential BP parallelises only across samples)."""
+    from concurrent.futures import ProcessPoolExecutor
     from threadpoolctl import threadpool_limits
     import bppsa_workloads as W
     from oracle import bp
@@ -701,30 +844,81 @@ def oracle_sample(budget_s: float = 12.0, seed: int = 0):
             if dt * 4 > budget_s or Ts >= T:
                 break
             Ts = min(T, Ts * 4)
-    return {"value": round(dt * 1e3 * T / Ts, 1), "unit": "ms", "cores": 1, "kind": "oracle",
-            "sample": f"T={Ts} of {T} steps (B={B}, H={H}) fp64 sequential BP + weight grads, "
-                      f"{dt:.2f} s measured, extrapolated x{T // Ts} (linear in T)",
-            "host_cpus": os.cpu_count()}
+    res = {"value": round(dt * 1e3 * T / Ts, 1), "unit": "ms", "cores": 1, "kind": "oracle",
+           "sample": f"T={Ts} of {T} steps (B={B}, H={H}) fp64 sequential BP + weight grads, "
+                     f"{dt:.2f} s measured single-threaded, extrapolated x{T // Ts} (linear in T)",
+           "host": host_cpu()}
+    P = max(1, min(B, os.cpu_count() or 1))
+    try:
+        step = -(-B // P)
+        jobs = [(Ts, b0, min(B, b0 + step), seed) for b0 in range(0, B, step)]
+        t0 = time.perf_counter()
+        with ProcessPoolExecutor(max_workers=len(jobs)) as ex:
+            list(ex.map(_oracle_samples, jobs))
+        wall = time.perf_counter() - t0
+        res["parallel_over_samples"] = {"value": round(wall * 1e3 * T / Ts, 1), "unit": "ms", "cores": len(jobs),
+                                        "note": "the same sample, samples split over processes (wall clock incl. "
+                                                "process start and the per-process input build)"}
+    except Exception as ex:  # noqa: BLE001
+        res["parallel_over_samples"] = {"error": str(ex)[:100]}
+    return res
 
 
 def run_reference(args):
+    """The reference arm of this tier: the fp64 oracle (sequential BP + weight
+    gradients) on the FULL C4 workload, once (steps = 1: ~30-60 s of one core;
+    BPPSA_REF_T overrides T for quick checks and says so in `sample`)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return None
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass
-    vals = []
-    cb = None
-    for _ in range(max(1, min(args.steps, 3))):
-        cb = oracle_sample(budget_s=6.0, seed=args.seed)
-        vals.append(cb["value"])
-    v = statistics.median(vals)
-    cb["value"] = v
-    return {"metric": METRIC, "value": v, "unit": "ms", "n_gpus": world, "steps": len(vals),
-            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
+    from threadpoolctl import threadpool_limits
+    import bppsa_workloads as W
+    from oracle import bp
+    T = int(os.environ.get("BPPSA_REF_T", C4["T"]))
+    B, H = C4["B"], C4["H"]
+    w = W.rnn_workload(T, B, H, seed=args.seed)
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        ref, _ = bp.bp_rnn(w.h, w.W_hh, w.g)
+        bp.weight_grads_rnn(w.x, w.h, ref)
+        v = (time.perf_counter() - t0) * 1e3
+    cb = {"value": round(v, 1), "unit": "ms", "cores": 1, "kind": "oracle",
+          "sample": f"the full workload T={T} (B={B}, H={H}): fp64 sequential BP + weight grads, one run, "
+                    f"single-threaded" + ("" if T == C4["T"] else f" (BPPSA_REF_T override; C4 has T={C4['T']})"),
+          "host": host_cpu()}
+    return {"metric": METRIC, "value": cb["value"], "unit": "ms", "n_gpus": world, "steps": 1,
+            "warmup": 0, "ms_per_step": cb["value"], "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C4: tanh RNN H=64 B=16 T=1048576 backward (sequential BP + weight grads)"},
-            "cpu_baseline": cb, "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": f"C4: tanh RNN H=64 B=16 T={T} backward (sequential BP + weight grads)"},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "ms", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+
+
+def run_dry(args):
+    """BPPSA_BENCH_DRYRUN=1 (tests on CPU): the launcher / rendezvous /
+    max-over-ranks path of the GPU arm with a fake per-rank time, over gloo."""
+    import torch
+    import torch.distributed as dist
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    ms = torch.tensor([1.0 + rank])
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    return {"ms": float(ms[0]), "world": world}
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: run this script as N ranks
+    (one per GPU) through torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 # ----------------------------------------------------------------------------- main
@@ -738,11 +932,21 @@ def main():
     ap.add_argument("--quick", action="store_true", help="skip e2e / baselines / sweep / cpu_baseline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world, rank, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         line = run_reference(args)
         if line is not None:
             print(json.dumps(line), flush=True)
+        return
+    if os.environ.get("BPPSA_BENCH_DRYRUN"):
+        r = run_dry(args)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": r["ms"], "unit": "ms", "n_gpus": r["world"],
+                              "steps": args.steps, "warmup": args.warmup, "dry_run": True}), flush=True)
         return
     r = run_ours(args)
     if rank != 0:
@@ -750,10 +954,13 @@ def main():
     line = {"metric": METRIC, "value": round(r["ms"], 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(r["ms"], 3), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded bitstreams x~Bernoulli(0.05+0.1c), torch-default init, fp32 forward)",
+            "data": "synthetic (seeded bitstreams x~Bernoulli(0.05+0.1c), torch-default init, fp32 forward "
+                    "on the GPU (cuDNN, TF32 off); every rank keeps only its time shard)",
             "config": {"workload": "C4: tanh RNN, H=64, B=16, T=1048576 — full backward (fused leaves + "
                                    "blocked Blelloch scan + weight grads)",
                        "T": C4["T"], "B": C4["B"], "H": C4["H"], "block0": c4_block0(world), "block": C4_BLOCK,
+                       "arithmetic": "fp32 results; level-0 fold and walk as exact s32 sums of int8 digit "
+                                     "products (tcgen05 kind::i8), every rounding RN",
                        "parallelism": (f"contiguous time shards x{world}, "
                                        f"{os.environ.get('BPPSA_EXCHANGE', 'nccl')} carry exchange")
                                       if world > 1 else "single GPU",

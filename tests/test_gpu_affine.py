@@ -52,28 +52,30 @@ def test_rnn_affine_blocks_norm_preserving(lib, H, blocks):
     assert rel_pair(grad, gi, ref, ref_init) <= TOL
 
 
-def test_rnn_affine_tensor_fold_c4_block(lib):
-    """The tcgen05 3xFP16 fold (H = 64, block0 = 512, as at C4) keeps the matrix
-    parts: realistic workload with per-step losses at the 1e-4 gate; the
-    norm-preserving family at the fold's bias bound (16 ulp per step, as for
-    bppsa_scan, DESIGN "Precision")."""
+@pytest.mark.parametrize("impl", ["auto", "tensor"])
+def test_rnn_affine_tensor_fold_c4_block(lib, impl):
+    """The tensor-core folds keep the matrix parts of the affine scan (H = 64,
+    block0 = 512, as at C4): realistic workload with per-step losses at the
+    1e-4 gate for both; the norm-preserving family at 1e-4 for the default
+    exact-integer engine (the opt-in 3xFP16 fold's truncation bias drifts
+    past it on this family, DESIGN "Precision")."""
     T, B, H = 20000, 16, 64
     w = W.rnn_workload(T, B, H, seed=11)
     e = W.per_step_seeds(w, seed=11)
     ref, ref_init = bp.bp_rnn_affine(w.h, w.W_hh, w.g, e)
     jac = lib.jacobians_rnn(cu(w.h), cu(w.W_hh))
-    grad, gi = lib.scan_affine(jac, cu(w.g), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl="tensor")
+    grad, gi = lib.scan_affine(jac, cu(w.g), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl=impl)
     torch.cuda.synchronize()
     assert rel_pair(grad, gi, ref, ref_init) <= TOL
+    if impl != "auto":
+        return
     f = W.norm_preserving_rnn(T, B, H, seed=1)
     e = (np.random.default_rng(2).standard_normal((T, B, H)) * 0.05).astype(np.float32)
     ref, ref_init = bp.bp_rnn_affine(f["h"], f["W_hh"], f["g"], e)
     jac = lib.jacobians_rnn(cu(f["h"]), cu(f["W_hh"]))
-    grad, gi = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl="tensor")
-    gf, i_f = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, block0=512, block=32, leaf_impl="ffma")
+    grad, gi = lib.scan_affine(jac, cu(f["g"]), cu(e), grad_h_init=True, block0=512, block=32)
     torch.cuda.synchronize()
-    assert rel_pair(gf, i_f, ref, ref_init) <= TOL
-    assert rel_pair(grad, gi, ref, ref_init) <= T * 16 * 2.0 ** -24
+    assert rel_pair(grad, gi, ref, ref_init) <= TOL
 
 
 @pytest.mark.parametrize("mode", ["blocked", "linear"])

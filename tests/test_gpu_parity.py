@@ -58,14 +58,23 @@ def test_rnn_H_and_block_sweep(lib, H, blocks):
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
 
 
-# Tensor-core level-0 fold (tcgen05 3xTF32, RNN H = 64).  Its accumulation
-# truncates: a one-signed bias of <= ~5 ulp per step (profiles/tc_precision.md),
-# so along a norm-preserving chain of n steps the error is bounded by
-# n * 16 ulp (2^-24 * 16 per step, a 3x margin); on the realistic workload the
-# gradients vanish within ~35 steps and the 1e-4 gate applies as is.
-BIAS_PER_STEP = 16 * 2.0 ** -24
+def block_rel(got, ref, blk=256, floor=1e-30):
+    """Reading 12's second metric: the worst per-`blk`-step block max-norm
+    relative error over blocks whose reference max exceeds `floor`."""
+    got = got.detach().cpu().numpy().astype(np.float64) if torch.is_tensor(got) else got
+    worst = 0.0
+    for t0 in range(0, ref.shape[0], blk):
+        den = np.abs(ref[t0:t0 + blk]).max()
+        if den > floor:
+            worst = max(worst, float(np.abs(got[t0:t0 + blk] - ref[t0:t0 + blk]).max() / den))
+    return worst
 
 
+# Opt-in tensor-core engines with fp32 accumulation (leaf_impl "tensor" =
+# 3xFP16, "tensor_tf32" = 3xTF32): the tcgen05 accumulator truncates, a
+# one-signed bias per step (profiles/tc_precision.md), so they are held to
+# 1e-4 on the realistic workload only; the default H = 64 engine is the exact
+# integer one ("int8"/auto), held to 1e-4 on every family below.
 TENSOR_IMPLS = ["tensor", "tensor_tf32"]
 
 
@@ -89,10 +98,6 @@ def test_rnn_tensor_leaf_small_H(lib, H, T, B, blocks):
     ref, ref_init = bp.bp_rnn(w.h, w.W_hh, w.g)
     grad, gi = run_rnn(lib, w.h, w.W_hh, w.g, block0=blocks[0], block=blocks[1], leaf_impl="tensor")
     assert rel_pair(grad, ref, gi, ref_init) <= TOL
-    f = W.norm_preserving_rnn(T, B, H, seed=H)
-    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
-    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1], leaf_impl="tensor")
-    assert rel_pair(gt, ref, it, ref_init) <= max(TOL, T * BIAS_PER_STEP)
 
 
 @pytest.mark.parametrize("wscale", [1e-20, 1e-3, 1.0])
@@ -110,11 +115,13 @@ def test_rnn_tensor_leaf_scaling_range(lib, wscale):
     g[3] = 0.0                        # an all-zero chain
     ref, ref_init = bp.bp_rnn(h, Wm, g)
     for C0 in (64, 256):
-        gt, it = run_rnn(lib, h, Wm, g, leaf_impl="tensor", block0=C0)
         gf, i_f = run_rnn(lib, h, Wm, g, leaf_impl="ffma", block0=C0)
-        et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
-        assert np.isfinite(gt.cpu().numpy()).all()
-        assert et <= max(TOL, 4 * ef), (C0, et, ef)
+        ef = rel_pair(gf, ref, i_f, ref_init)
+        for impl in ("auto", "tensor"):
+            gt, it = run_rnn(lib, h, Wm, g, leaf_impl=impl, block0=C0)
+            et = rel_pair(gt, ref, it, ref_init)
+            assert np.isfinite(gt.cpu().numpy()).all()
+            assert et <= max(TOL, 4 * ef), (impl, C0, et, ef)
 
 
 @pytest.mark.parametrize("s", [0.5, 2.0])
@@ -126,23 +133,29 @@ def test_rnn_tensor_leaf_growth_and_decay(lib, s):
     Wm = (f["W_hh"] * s).astype(np.float32)
     ref, ref_init = bp.bp_rnn(f["h"], Wm, f["g"])
     for C0 in (16, 64):
-        gt, it = run_rnn(lib, f["h"], Wm, f["g"], leaf_impl="tensor", block0=C0)
         gf, i_f = run_rnn(lib, f["h"], Wm, f["g"], leaf_impl="ffma", block0=C0)
-        et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
-        assert et <= max(TOL, 4 * ef), (C0, et, ef)
+        ef = rel_pair(gf, ref, i_f, ref_init)
+        for impl in ("auto", "tensor"):
+            gt, it = run_rnn(lib, f["h"], Wm, f["g"], leaf_impl=impl, block0=C0)
+            et = rel_pair(gt, ref, it, ref_init)
+            assert et <= max(TOL, 4 * ef), (impl, C0, et, ef)
 
 
-@pytest.mark.parametrize("impl", TENSOR_IMPLS)
-@pytest.mark.parametrize("B", [1, 2, 3, 16, 17])
-def test_rnn_tensor_leaf_norm_preserving_bias_bound(lib, B, impl):
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 5, 16, 17])
+@pytest.mark.parametrize("blocks", [(0, 0), (512, 32), (64, 8)])
+def test_rnn_int8_norm_preserving(lib, B, blocks):
+    """The default H = 64 engine (exact s32 accumulation of int8 digit
+    products, fp32 RN combination): 1e-4 on the norm-preserving family, and
+    no worse than the CUDA-core FFMA engine by more than a small factor
+    (the opt-in 3xFP16 engine drifts to ~1e-3 here)."""
     T = 2000
     f = W.norm_preserving_rnn(T, B, 64, seed=B)
     ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
-    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], leaf_impl=impl)
-    gf, i_f = run_rnn(lib, f["h"], f["W_hh"], f["g"], leaf_impl="ffma")
+    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1])
+    gf, i_f = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1], leaf_impl="ffma")
     et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
-    print(f"B={B}: tensor {et:.2e}  ffma {ef:.2e}")
-    assert ef <= TOL and et <= T * BIAS_PER_STEP
+    print(f"B={B} blocks={blocks}: int8 {et:.2e}  ffma {ef:.2e}")
+    assert et <= TOL and et <= max(3 * ef, 2e-5)
 
 
 def test_rnn_config1(lib):
@@ -163,16 +176,39 @@ def test_rnn_config2(lib, T):
     assert rel(grad, ref) <= TOL
 
 
+@pytest.mark.parametrize("blocks", [(0, 0), (512, 32)])
 @pytest.mark.parametrize("H,T", [(20, 65536), (64, 65536), (64, 4096)])
-def test_rnn_norm_preserving(lib, H, T):
+def test_rnn_norm_preserving(lib, H, T, blocks):
     """Reading 12 (ii): the norm-preserving family keeps every grad_h O(seed)
-    over the whole sequence, so the global max-norm constrains every step."""
+    over the whole sequence, so the global max-norm constrains every step.
+    The DEFAULT engine (H = 64: exact-integer tensor cores; H = 20: FFMA),
+    the default and the bench's block shapes; reading 12's per-256-step-block
+    error is held to the same 1e-4."""
     f = W.norm_preserving_rnn(T, 4, H, seed=7)
-    ref, _ = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
-    grad, _ = run_rnn(lib, f["h"], f["W_hh"], f["g"], leaf_impl="ffma")
-    e = rel(grad, ref)
-    print(f"norm-preserving H={H} T={T}: rel={e:.3e}")
-    assert e <= TOL
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    grad, gi = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1])
+    e, eb = rel_pair(grad, ref, gi, ref_init), block_rel(grad, ref)
+    print(f"norm-preserving H={H} T={T} blocks={blocks}: rel={e:.3e} worst 256-block={eb:.3e}")
+    assert e <= TOL and eb <= TOL
+
+
+@pytest.mark.slow
+def test_rnn_norm_preserving_2p20_gate_iii(lib):
+    """Reading 12 (iii): at T = 2^20 (C4's length) report the default path's
+    error next to the fp32 sequential chain's (our LINEAR mode on the CUDA
+    cores, i.e. plain fp32 BP).  Both drift like sqrt(T) on this family; the
+    exact-integer tree must stay within a small factor of plain fp32 BP."""
+    T, B, H = 1 << 20, 2, 64
+    f = W.norm_preserving_rnn(T, B, H, seed=20)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=512, block=32)
+    e_tree, eb_tree = rel_pair(gt, ref, it, ref_init), block_rel(gt, ref)
+    del gt, it
+    gl, il = run_rnn(lib, f["h"], f["W_hh"], f["g"], mode="linear")
+    e_lin = rel_pair(gl, ref, il, ref_init)
+    print(f"gate (iii) T=2^20 norm-preserving: BLOCKED int8 {e_tree:.3e} (worst 256-block {eb_tree:.3e})"
+          f"  LINEAR fp32 chain {e_lin:.3e}")
+    assert e_tree <= max(4 * e_lin, TOL)
 
 
 @pytest.mark.parametrize("mode,blocks", [("blocked", (0, 0)), ("blocked", (2, 3)), ("blocked", (5, 2)),
@@ -426,7 +462,7 @@ def test_shard_loopback(lib, kind, G):
     aggs = []
     for r, (j, ws) in enumerate(zip(jacs, wss)):
         agg = torch.empty((B, H * H), device="cuda")
-        lib.scan_shard_up(j, cu(g) if r == G - 1 else None, agg, ws, leaf_impl="ffma")
+        lib.scan_shard_up(j, cu(g) if r == G - 1 else None, agg, ws)
         aggs.append(agg)
     gathered = torch.stack(aggs)
     outs, init = [], None
