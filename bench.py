@@ -852,13 +852,12 @@ def oracle_sample(budget_s: float = 12.0, seed: int = 0):
     try:
         step = -(-B // P)
         jobs = [(Ts, b0, min(B, b0 + step), seed) for b0 in range(0, B, step)]
-        t0 = time.perf_counter()
         with ProcessPoolExecutor(max_workers=len(jobs)) as ex:
-            list(ex.map(_oracle_samples, jobs))
-        wall = time.perf_counter() - t0
-        res["parallel_over_samples"] = {"value": round(wall * 1e3 * T / Ts, 1), "unit": "ms", "cores": len(jobs),
-                                        "note": "the same sample, samples split over processes (wall clock incl. "
-                                                "process start and the per-process input build)"}
+            times = list(ex.map(_oracle_samples, jobs))
+        res["parallel_over_samples"] = {"value": round(max(times) * 1e3 * T / Ts, 1), "unit": "ms",
+                                        "cores": len(jobs),
+                                        "note": "the same sample, the B samples split over processes (one core "
+                                                "each): the slowest process's oracle time, extrapolated likewise"}
     except Exception as ex:  # noqa: BLE001
         res["parallel_over_samples"] = {"error": str(ex)[:100]}
     return res

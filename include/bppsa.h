@@ -232,25 +232,33 @@ bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed,
 /* Peer-memory carry exchange (row a5 without NCCL; SURVEY 8(e) "fused
  * variant"): replaces the all-gather between bppsa_scan_shard_up and
  * bppsa_scan_shard_down.  Every rank owns a mailbox of 2 x world x n floats
- * (n = B*H*H, the aggregate size; an epoch-parity double buffer) and flags
- * [world] u32, zero-initialised, mapped into every other rank's address
- * space (CUDA IPC over NVLink / NVSwitch, or the same device).
- * publish: stores `aggregate` [n] into mailbox[p][epoch & 1][rank] of every
- * rank p (peer_mailboxes: device array [world] of device pointers) and, once
- * every block's stores are performed (system-scope fence, last-block count in
- * this rank's `counter`, zero-initialised), release-stores `epoch` into
- * flags[p][rank].  wait: an acquire spin until flags[r] >= epoch for every
- * r > rank (the ranks whose aggregates this rank's carry needs); kernels
- * after it on `stream` may read mailbox[epoch & 1] as shard_down's
- * `gathered`.  Epochs start at 1 and increase by 1 per exchange; a rank must
- * not publish epoch e+2 before every reader finished epoch e (any collective
- * per step, e.g. the weight-gradient all-reduce, guarantees it).            */
+ * (n = B*H*H, the aggregate size; an epoch-parity double buffer), flags
+ * [world] u32 and acks [world] u32, zero-initialised, mapped into every
+ * other rank's address space (CUDA IPC over NVLink / NVSwitch, or the same
+ * device).
+ * publish: first waits (acquire) until acks[r] >= epoch - 2 for every
+ * r < rank (the readers of this rank's slot have finished the epoch whose
+ * slot is about to be overwritten), then stores `aggregate` [n] into
+ * mailbox[p][epoch & 1][rank] of every rank p (peer_mailboxes: device array
+ * [world] of device pointers) and, once every block's stores are performed
+ * (system-scope fence, last-block count in this rank's `counter`,
+ * zero-initialised), release-stores `epoch` into flags[p][rank].
+ * wait: an acquire spin until flags[r] >= epoch for every r > rank (the
+ * ranks whose aggregates this rank's carry needs); kernels after it on
+ * `stream` may read mailbox[epoch & 1] as shard_down's `gathered`.
+ * ack: after those reads (stream order: call it after bppsa_scan_shard_down),
+ * release-stores `epoch` into acks[p][rank] of every later rank p
+ * (peer_acks: device array [world] of device pointers).  Epochs start at 1
+ * and increase by 1 per exchange.  A rank that skips ack blocks its writers
+ * two epochs later (no silent overwrite).                                   */
 bppsa_status bppsa_exchange_publish(const float* aggregate, long long n,
                                     int rank, int world,
                                     float* const* peer_mailboxes,
                                     unsigned* const* peer_flags,
-                                    unsigned* counter, unsigned epoch,
-                                    void* stream);
+                                    unsigned* counter, const unsigned* acks,
+                                    unsigned epoch, void* stream);
+bppsa_status bppsa_exchange_ack(int rank, int world, unsigned* const* peer_acks,
+                                unsigned epoch, void* stream);
 bppsa_status bppsa_exchange_wait(const unsigned* flags, int rank, int world,
                                  unsigned epoch, void* stream);
 

@@ -47,7 +47,8 @@ EXPORTS = {
     "bppsa_weight_grads_rnn_rows": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, C.c_longlong, C.c_longlong, _vp, _sz,
                                          _vp]),
     "bppsa_weight_grads_rnn_reduce": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "bppsa_exchange_publish": (_i, [_vp, C.c_longlong, _i, _i, _vp, _vp, _vp, C.c_uint, _vp]),
+    "bppsa_exchange_publish": (_i, [_vp, C.c_longlong, _i, _i, _vp, _vp, _vp, _vp, C.c_uint, _vp]),
+    "bppsa_exchange_ack": (_i, [_i, _i, _vp, C.c_uint, _vp]),
     "bppsa_exchange_wait": (_i, [_vp, _i, _i, C.c_uint, _vp]),
     "bppsa_gru_gates": (_i, [_i, _i, _i, _i] + [_vp] * 12 + [_vp]),
     "bppsa_scan_affine": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
@@ -116,6 +117,25 @@ def _ptr(t: torch.Tensor | None, name: str = "tensor"):
     return t.data_ptr()
 
 
+def _req(t: torch.Tensor | None, shape: tuple, name: str, dev: torch.device | None = None) -> None:
+    """Shape / device check of a caller tensor before its raw pointer crosses
+    the C ABI (the library cannot see extents: a wrong-shaped buffer would be
+    read or written out of bounds)."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch.Tensor")
+    if tuple(t.shape) != tuple(int(v) for v in shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if dev is not None and t.device != dev:
+        raise ValueError(f"{name} is on {t.device}, expected {dev}")
+
+
+def _ws(ws: torch.Tensor, dev: torch.device) -> None:
+    if ws.dtype != torch.uint8 or not ws.is_cuda or not ws.is_contiguous() or ws.device != dev:
+        raise ValueError(f"workspace must be a contiguous uint8 CUDA tensor on {dev}")
+
+
 def _stream(stream=None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -142,7 +162,11 @@ class Jacobians:
 def jacobians_rnn(h: torch.Tensor, W_hh: torch.Tensor, JT_out: torch.Tensor | None = None, stream=None):
     """bppsa_jacobians_rnn: J_t^T = W_hh^T diag(1-h_t^2) (fused descriptor, or
     materialised into JT_out [T,B,H,H])."""
+    if h.dim() != 3:
+        raise ValueError("h must be [T, B, H]")
     T, B, H = h.shape
+    _req(W_hh, (H, H), "W_hh", h.device)
+    _req(JT_out, (T, B, H, H), "JT_out", h.device)
     d = _Jac()
     _check(_lib.bppsa_jacobians_rnn(T, B, H, _ptr(h, "h"), _ptr(W_hh, "W_hh"), _ptr(JT_out, "JT_out"),
                                     C.byref(d), _stream(stream)), "bppsa_jacobians_rnn")
@@ -151,7 +175,13 @@ def jacobians_rnn(h: torch.Tensor, W_hh: torch.Tensor, JT_out: torch.Tensor | No
 
 def jacobians_gru(h_prev, r, z, n, M, W_hh3, JT_out: torch.Tensor | None = None, stream=None):
     """bppsa_jacobians_gru: eqn:gru_jcb leaves from the saved GRU tape."""
+    if r.dim() != 3:
+        raise ValueError("r must be [T, B, H]")
     T, B, H = r.shape
+    for t_, nm in ((h_prev, "h_prev"), (z, "z"), (n, "n"), (M, "M")):
+        _req(t_, (T, B, H), nm, r.device)
+    _req(W_hh3, (3 * H, H), "W_hh3", r.device)
+    _req(JT_out, (T, B, H, H), "JT_out", r.device)
     d = _Jac()
     _check(_lib.bppsa_jacobians_gru(T, B, H, _ptr(h_prev, "h_prev"), _ptr(r, "r"), _ptr(z, "z"), _ptr(n, "n"),
                                     _ptr(M, "M"), _ptr(W_hh3, "W_hh3"), _ptr(JT_out, "JT_out"), C.byref(d),
@@ -161,8 +191,9 @@ def jacobians_gru(h_prev, r, z, n, M, W_hh3, JT_out: torch.Tensor | None = None,
 
 def jacobians_dense(JT: torch.Tensor) -> Jacobians:
     """A DENSE descriptor over caller-provided J_t^T [T,B,H,H] (row-major)."""
+    if JT.dim() != 4 or JT.shape[2] != JT.shape[3]:
+        raise ValueError("JT must be [T, B, H, H]")
     T, B, H, H2 = JT.shape
-    assert H == H2
     d = _Jac()
     d.kind, d.T, d.B, d.H, d.JT = JAC_DENSE, T, B, H, _ptr(JT, "JT")
     return Jacobians(d, (JT,))
@@ -220,15 +251,19 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
     `levels` = (up_levels, down_levels) for mode="hybrid" (P:472)."""
     T, B, H = jac.T, jac.B, jac.H
     dev = seed.device
+    _req(seed, (B, H), "seed")
     if grad_h is None:
         grad_h = torch.empty((T, B, H), dtype=torch.float32, device=dev)
     if grad_h_init is True:
         grad_h_init = torch.empty((B, H), dtype=torch.float32, device=dev)
     elif grad_h_init is False:
         grad_h_init = None
+    _req(grad_h, (T, B, H), "grad_h", dev)
+    _req(grad_h_init, (B, H), "grad_h_init", dev)
     o = _opts(mode, block0, block, trace, leaf_impl, levels)
     if ws is None:
         ws = workspace(scan_workspace_size(jac, mode, block0, block, levels), dev)
+    _ws(ws, dev)
     _check(_lib.bppsa_scan(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(grad_h, "grad_h"),
                            _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
                            _stream(stream)), "bppsa_scan")
@@ -236,12 +271,18 @@ def scan(jac: Jacobians, seed: torch.Tensor, grad_h: torch.Tensor | None = None,
 
 
 def exchange_publish(aggregate: torch.Tensor, rank: int, world: int, peer_mailboxes: torch.Tensor,
-                     peer_flags: torch.Tensor, counter: torch.Tensor, epoch: int, stream=None):
-    """bppsa_exchange_publish: aggregate -> every rank's mailbox, then the flags
-    (peer_mailboxes / peer_flags: int64 device arrays of device pointers)."""
+                     peer_flags: torch.Tensor, counter: torch.Tensor, acks: torch.Tensor, epoch: int, stream=None):
+    """bppsa_exchange_publish: (after the readers' acks of epoch - 2) aggregate
+    -> every rank's mailbox, then the flags (peer_mailboxes / peer_flags:
+    int64 device arrays of device pointers; acks: this rank's ack words)."""
     _check(_lib.bppsa_exchange_publish(_ptr(aggregate, "aggregate"), aggregate.numel(), rank, world,
                                        peer_mailboxes.data_ptr(), peer_flags.data_ptr(), counter.data_ptr(),
-                                       epoch, _stream(stream)), "bppsa_exchange_publish")
+                                       acks.data_ptr(), epoch, _stream(stream)), "bppsa_exchange_publish")
+
+
+def exchange_ack(rank: int, world: int, peer_acks: torch.Tensor, epoch: int, stream=None):
+    """bppsa_exchange_ack: this rank finished reading epoch `epoch`."""
+    _check(_lib.bppsa_exchange_ack(rank, world, peer_acks.data_ptr(), epoch, _stream(stream)), "bppsa_exchange_ack")
 
 
 def exchange_wait(flags: torch.Tensor, rank: int, world: int, epoch: int, stream=None):
@@ -253,8 +294,16 @@ def gru_gates(x: torch.Tensor, h: torch.Tensor, W_ih3: torch.Tensor, W_hh3: torc
     """bppsa_gru_gates (FO): the GRU tape {h_prev, r, z, n, M} recomputed from x and h."""
     T, B, I = x.shape
     H = h.shape[2]
+    _req(h, (T, B, H), "h", x.device)
+    _req(W_ih3, (3 * H, I), "W_ih3", x.device)
+    _req(W_hh3, (3 * H, H), "W_hh3", x.device)
+    _req(b_ih3, (3 * H,), "b_ih3", x.device)
+    _req(b_hh3, (3 * H,), "b_hh3", x.device)
+    _req(h_init, (B, H), "h_init", x.device)
     if out is None:
         out = {k: torch.empty((T, B, H), dtype=torch.float32, device=h.device) for k in ("h_prev", "r", "z", "n", "M")}
+    for k in ("h_prev", "r", "z", "n", "M"):
+        _req(out[k], (T, B, H), k, x.device)
     _check(_lib.bppsa_gru_gates(T, B, H, I, _ptr(x, "x"), _ptr(h, "h"), _ptr(h_init, "h_init"), _ptr(W_ih3, "W_ih3"),
                                 _ptr(W_hh3, "W_hh3"), _ptr(b_ih3, "b_ih3"), _ptr(b_hh3, "b_hh3"),
                                 *[_ptr(out[k], k) for k in ("h_prev", "r", "z", "n", "M")], _stream(stream)),
@@ -269,15 +318,20 @@ def scan_affine(jac: Jacobians, seed: torch.Tensor, e: torch.Tensor, grad_h: tor
     """bppsa_scan_affine: per-step losses, e [T,B,H] = dl_t/dh_t (partial)."""
     T, B, H = jac.T, jac.B, jac.H
     dev = seed.device
+    _req(seed, (B, H), "seed")
+    _req(e, (T, B, H), "e", dev)
     if grad_h is None:
         grad_h = torch.empty((T, B, H), dtype=torch.float32, device=dev)
     if grad_h_init is True:
         grad_h_init = torch.empty((B, H), dtype=torch.float32, device=dev)
     elif grad_h_init is False:
         grad_h_init = None
+    _req(grad_h, (T, B, H), "grad_h", dev)
+    _req(grad_h_init, (B, H), "grad_h_init", dev)
     o = _opts(mode, block0, block, trace, leaf_impl)
     if ws is None:
         ws = workspace(scan_workspace_size(jac, mode, block0, block), dev)
+    _ws(ws, dev)
     _check(_lib.bppsa_scan_affine(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(e, "e"), _ptr(grad_h, "grad_h"),
                                   _ptr(grad_h_init, "grad_h_init"), ws.data_ptr(), ws.numel(), C.byref(o),
                                   _stream(stream)), "bppsa_scan_affine")
@@ -287,6 +341,11 @@ def scan_affine(jac: Jacobians, seed: torch.Tensor, e: torch.Tensor, grad_h: tor
 def scan_shard_up(jac: Jacobians, seed: torch.Tensor | None, aggregate: torch.Tensor, ws: torch.Tensor,
                   block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None,
                   leaf_impl="auto"):
+    dev = aggregate.device
+    _req(seed, (jac.B, jac.H), "seed", dev)
+    if aggregate.numel() != jac.B * jac.H * jac.H:
+        raise ValueError(f"aggregate must hold B*H*H = {jac.B * jac.H * jac.H} floats")
+    _ws(ws, dev)
     o = _opts("blocked", block0, block, trace, leaf_impl)
     _check(_lib.bppsa_scan_shard_up(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(aggregate, "aggregate"),
                                     ws.data_ptr(), ws.numel(), C.byref(o), _stream(stream)), "bppsa_scan_shard_up")
@@ -296,6 +355,14 @@ def scan_shard_up(jac: Jacobians, seed: torch.Tensor | None, aggregate: torch.Te
 def scan_shard_down(jac: Jacobians, seed: torch.Tensor | None, gathered: torch.Tensor | None, rank: int,
                     world: int, grad_h: torch.Tensor, grad_h_init: torch.Tensor | None, ws: torch.Tensor,
                     block0: int = 0, block: int = 0, stream=None, trace: LaunchTrace | None = None):
+    dev = grad_h.device
+    T, B, H = jac.T, jac.B, jac.H
+    _req(seed, (B, H), "seed", dev)
+    if gathered is not None and gathered.numel() != world * B * H * H:
+        raise ValueError(f"gathered must hold world*B*H*H = {world * B * H * H} floats")
+    _req(grad_h, (T, B, H), "grad_h", dev)
+    _req(grad_h_init, (B, H), "grad_h_init", dev)
+    _ws(ws, dev)
     o = _opts("blocked", block0, block, trace)
     _check(_lib.bppsa_scan_shard_down(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(gathered, "gathered"), rank,
                                       world, _ptr(grad_h, "grad_h"), _ptr(grad_h_init, "grad_h_init"),
@@ -316,11 +383,18 @@ def weight_grads_rnn(x, h, grad_h, h_init=None, ws=None, out=None, stream=None):
     T, B, H = h.shape
     I = x.shape[2]
     dev = h.device
+    _req(x, (T, B, I), "x", dev)
+    _req(grad_h, (T, B, H), "grad_h", dev)
+    _req(h_init, (B, H), "h_init", dev)
     if out is None:
         out = (torch.empty((H, I), device=dev), torch.empty((H, H), device=dev), torch.empty((H,), device=dev))
     if ws is None:
         ws = workspace(weight_grads_workspace_size(T, B, H, I), dev)
+    _ws(ws, dev)
     dW_ih, dW_hh, db = out
+    _req(dW_ih, (H, I), "dW_ih", dev)
+    _req(dW_hh, (H, H), "dW_hh", dev)
+    _req(db, (H,), "db", dev)
     _check(_lib.bppsa_weight_grads_rnn(T, B, H, I, _ptr(x, "x"), _ptr(h, "h"), _ptr(h_init, "h_init"),
                                        _ptr(grad_h, "grad_h"), _ptr(dW_ih, "dW_ih"), _ptr(dW_hh, "dW_hh"),
                                        _ptr(db, "db"), ws.data_ptr(), ws.numel(), _stream(stream)),
@@ -339,6 +413,10 @@ def weight_grads_rnn_rows(x, h, grad_h, row0: int, row1: int, ws: torch.Tensor, 
     """bppsa_weight_grads_rnn_rows: partial slabs of rows [row0, row1) into ws."""
     T, B, H = h.shape
     I = x.shape[2]
+    _req(x, (T, B, I), "x", h.device)
+    _req(grad_h, (T, B, H), "grad_h", h.device)
+    _req(h_init, (B, H), "h_init", h.device)
+    _ws(ws, h.device)
     _check(_lib.bppsa_weight_grads_rnn_rows(T, B, H, I, _ptr(x, "x") if I else None, _ptr(h, "h"),
                                             _ptr(h_init, "h_init"), _ptr(grad_h, "grad_h"), row0, row1,
                                             ws.data_ptr(), ws.numel(), _stream(stream)),
@@ -350,6 +428,10 @@ def weight_grads_rnn_reduce(T, B, H, I, ws: torch.Tensor, out=None, device=None,
     dev = device or ws.device
     if out is None:
         out = (torch.empty((H, I), device=dev), torch.empty((H, H), device=dev), torch.empty((H,), device=dev))
+    _req(out[0], (H, I), "dW_ih", ws.device)
+    _req(out[1], (H, H), "dW_hh", ws.device)
+    _req(out[2], (H,), "db", ws.device)
+    _ws(ws, ws.device)
     _check(_lib.bppsa_weight_grads_rnn_reduce(T, B, H, I, _ptr(out[0], "dW_ih") if I else None,
                                               _ptr(out[1], "dW_hh"), _ptr(out[2], "db"), ws.data_ptr(), ws.numel(),
                                               _stream(stream)), "bppsa_weight_grads_rnn_reduce")
@@ -361,12 +443,20 @@ def weight_grads_gru(x, tape: dict, grad_h, ws=None, out=None, stream=None):
     T, B, H = tape["r"].shape
     I = x.shape[2]
     dev = grad_h.device
+    _req(x, (T, B, I), "x", dev)
+    _req(grad_h, (T, B, H), "grad_h", dev)
+    for k in ("h_prev", "r", "z", "n", "M"):
+        _req(tape[k], (T, B, H), k, dev)
     if out is None:
         out = (torch.empty((3 * H, I), device=dev), torch.empty((3 * H, H), device=dev),
                torch.empty((3 * H,), device=dev), torch.empty((3 * H,), device=dev))
     if ws is None:
         ws = workspace(weight_grads_workspace_size(T, B, H, I), dev)
+    _ws(ws, dev)
     a, b_, c, d = out
+    for t_, shp, nm in ((a, (3 * H, I), "dW_ih3"), (b_, (3 * H, H), "dW_hh3"), (c, (3 * H,), "db_ih3"),
+                        (d, (3 * H,), "db_hh3")):
+        _req(t_, shp, nm, dev)
     _check(_lib.bppsa_weight_grads_gru(T, B, H, I, _ptr(x, "x"), _ptr(tape["h_prev"], "h_prev"),
                                        _ptr(tape["r"], "r"), _ptr(tape["z"], "z"), _ptr(tape["n"], "n"),
                                        _ptr(tape["M"], "M"), _ptr(grad_h, "grad_h"), _ptr(a, "dW_ih3"),

@@ -564,6 +564,16 @@ bppsa_status bppsa_scan_workspace_size(const bppsa_jac* jac, const bppsa_scan_op
   return BPPSA_OK;
 }
 
+// The tensor-core leaf kernels move h / grad_h / seed / carries in 16-byte
+// units (cp.async 16, float4): a caller buffer at an odd 4-byte offset would
+// fault, so such calls take the CUDA-core engine (4-byte accesses) instead.
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static void demote_unaligned(const bppsa_jac& j, Plan* p, const void* seed, const void* grad_h,
+                             const void* grad_h_init) {
+  if (j.kind == BPPSA_JAC_RNN_TANH && !(al16(j.h) && al16(seed) && al16(grad_h) && al16(grad_h_init)))
+    p->leaf_impl = 1;
+}
+
 static bppsa_status scan_impl(const bppsa_jac* jac, const float* seed, const float* e_aff, float* grad_h,
                               float* grad_h_init, void* ws, size_t ws_bytes, const bppsa_scan_opts* opts,
                               void* stream) {
@@ -576,6 +586,8 @@ static bppsa_status scan_impl(const bppsa_jac* jac, const float* seed, const flo
   Plan p;
   s = make_plan(j, 1, opts, false, &p);
   if (s != BPPSA_OK) return s;
+  demote_unaligned(j, &p, seed, grad_h, grad_h_init);
+  if (e_aff && !al16(e_aff)) p.leaf_impl = 1;
   s = check_ws(p, ws, ws_bytes);
   if (s != BPPSA_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
@@ -662,6 +674,7 @@ bppsa_status bppsa_scan_shard_up(const bppsa_jac* jac, const float* seed, float*
   Plan p;
   s = make_plan(*jac, head, opts, true, &p);
   if (s != BPPSA_OK) return s;
+  demote_unaligned(*jac, &p, seed, nullptr, nullptr);
   s = check_ws(p, ws, ws_bytes);
   if (s != BPPSA_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
@@ -693,6 +706,7 @@ bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed, cons
   Plan p;
   s = make_plan(*jac, head, opts, true, &p);
   if (s != BPPSA_OK) return s;
+  demote_unaligned(*jac, &p, seed, grad_h, grad_h_init);
   s = check_ws(p, ws, ws_bytes);
   if (s != BPPSA_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
@@ -713,16 +727,25 @@ bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed, cons
 
 bppsa_status bppsa_exchange_publish(const float* aggregate, long long n, int rank, int world,
                                     float* const* peer_mailboxes, unsigned* const* peer_flags, unsigned* counter,
-                                    unsigned epoch, void* stream) {
+                                    const unsigned* acks, unsigned epoch, void* stream) {
   if (n < 1 || world < 1 || rank < 0 || rank >= world || epoch == 0)
     return fail(BPPSA_ERR_INVALID_ARGUMENT, "need n >= 1, 0 <= rank < world, epoch >= 1");
   REQUIRE_DEV(aggregate, "aggregate");
   REQUIRE_DEV(peer_mailboxes, "peer_mailboxes");
   REQUIRE_DEV(peer_flags, "peer_flags");
   REQUIRE_DEV(counter, "counter");
-  cudaError_t e = launch_exchange_publish(aggregate, n, rank, world, peer_mailboxes, peer_flags, counter, epoch,
-                                          num_sms(), (cudaStream_t)stream);
+  REQUIRE_DEV(acks, "acks");
+  cudaError_t e = launch_exchange_publish(aggregate, n, rank, world, peer_mailboxes, peer_flags, counter, acks,
+                                          epoch, num_sms(), (cudaStream_t)stream);
   return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "exchange publish");
+}
+
+bppsa_status bppsa_exchange_ack(int rank, int world, unsigned* const* peer_acks, unsigned epoch, void* stream) {
+  if (world < 1 || rank < 0 || rank >= world || epoch == 0)
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "need 0 <= rank < world, epoch >= 1");
+  REQUIRE_DEV(peer_acks, "peer_acks");
+  cudaError_t e = launch_exchange_ack(rank, world, peer_acks, epoch, (cudaStream_t)stream);
+  return e == cudaSuccess ? BPPSA_OK : cuda_status(e, "exchange ack");
 }
 
 bppsa_status bppsa_exchange_wait(const unsigned* flags, int rank, int world, unsigned epoch, void* stream) {

@@ -138,8 +138,9 @@ cudaError_t launch_affine_seed(const float* seed, const float* e, int T, int B, 
 
 // peer-memory carry exchange (exchange.cu)
 cudaError_t launch_exchange_publish(const float* src, long long n, int rank, int world, float* const* peers,
-                                    unsigned* const* peer_flags, unsigned* counter, unsigned epoch, int num_sms,
-                                    cudaStream_t st);
+                                    unsigned* const* peer_flags, unsigned* counter, const unsigned* acks,
+                                    unsigned epoch, int num_sms, cudaStream_t st);
+cudaError_t launch_exchange_ack(int rank, int world, unsigned* const* peer_acks, unsigned epoch, cudaStream_t st);
 cudaError_t launch_exchange_wait(const unsigned* flags, int rank, int world, unsigned epoch, cudaStream_t st);
 
 // GRU forward overhead (FO): the tape from (x, h) (gates.cu)

@@ -65,8 +65,11 @@ class PeerExchange:
     flags [world] are mapped into every other rank with CUDA IPC (handles
     swapped once through torch.distributed), so the up-sweep aggregate is
     stored straight into every peer's memory over NVLink and the down-sweep
-    waits on the flags of the later ranks only.  One instance per (rank,
-    shape); every call of `exchange` is a new epoch."""
+    waits on the flags of the later ranks only.  Back-pressure: after its
+    down-sweep read the mailbox, a rank acks the epoch in every later rank
+    (`release`), and a writer publishing epoch e first waits for the acks of
+    e - 2 (whose slot it overwrites).  One instance per (rank, shape); every
+    call of `exchange` is a new epoch, followed by one `release`."""
 
     def __init__(self, B: int, H: int, group=None):
         from torch.multiprocessing.reductions import reduce_tensor
@@ -76,22 +79,24 @@ class PeerExchange:
         self.n = B * H * H
         self.mail = torch.zeros((2, self.world, B, H * H), dtype=torch.float32, device="cuda")
         self.flags = torch.zeros(self.world, dtype=torch.int32, device="cuda")
+        self.acks = torch.zeros(self.world, dtype=torch.int32, device="cuda")
         self.counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         torch.cuda.synchronize()
-        mine = (self.rank, reduce_tensor(self.mail), reduce_tensor(self.flags))
+        mine = (self.rank, reduce_tensor(self.mail), reduce_tensor(self.flags), reduce_tensor(self.acks))
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=group)
         self._peers = []                                   # keep the mappings alive
-        mail_ptrs, flag_ptrs = [0] * self.world, [0] * self.world
-        for r, (fm, am), (ff, af) in allh:
+        mail_ptrs, flag_ptrs, ack_ptrs = [0] * self.world, [0] * self.world, [0] * self.world
+        for r, (fm, am), (ff, af), (fa, aa) in allh:
             if r == self.rank:
-                m, f = self.mail, self.flags
+                m, f, k = self.mail, self.flags, self.acks
             else:
-                m, f = fm(*am), ff(*af)
-                self._peers.append((m, f))
-            mail_ptrs[r], flag_ptrs[r] = m.data_ptr(), f.data_ptr()
+                m, f, k = fm(*am), ff(*af), fa(*aa)
+                self._peers.append((m, f, k))
+            mail_ptrs[r], flag_ptrs[r], ack_ptrs[r] = m.data_ptr(), f.data_ptr(), k.data_ptr()
         self.mail_ptrs = torch.tensor(mail_ptrs, dtype=torch.int64, device="cuda")
         self.flag_ptrs = torch.tensor(flag_ptrs, dtype=torch.int64, device="cuda")
+        self.ack_ptrs = torch.tensor(ack_ptrs, dtype=torch.int64, device="cuda")
         self.epoch = 0
         dist.barrier(group=group)
 
@@ -100,9 +105,13 @@ class PeerExchange:
         gathered [world, B, H*H] view (valid for kernels after this call)."""
         self.epoch += 1
         self.api.exchange_publish(agg.contiguous(), self.rank, self.world, self.mail_ptrs, self.flag_ptrs,
-                                  self.counter, self.epoch)
+                                  self.counter, self.acks, self.epoch)
         self.api.exchange_wait(self.flags, self.rank, self.world, self.epoch)
         return self.mail[self.epoch & 1]
+
+    def release(self):
+        """This rank's reads of the current epoch's mailbox are enqueued: ack it."""
+        self.api.exchange_ack(self.rank, self.world, self.ack_ptrs, self.epoch)
 
 
 def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None, exchange=None):
@@ -122,4 +131,7 @@ def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None
         gathered = flat.view((world,) + tuple(agg.shape))
     else:
         gathered = agg.unsqueeze(0)
-    return backend.down(seed, None if head else gathered, rank, world, grad_h=grad_h, want_init=want_init)
+    out = backend.down(seed, None if head else gathered, rank, world, grad_h=grad_h, want_init=want_init)
+    if world > 1 and exchange is not None:
+        exchange.release()
+    return out

@@ -192,6 +192,25 @@ def test_rnn_norm_preserving(lib, H, T, blocks):
     assert e <= TOL and eb <= TOL
 
 
+def test_unaligned_buffers_take_the_cuda_core_engine(lib):
+    """contiguous tensors at an odd 4-byte offset would fault in the
+    16-byte cp.async / float4 paths of the tensor-core kernels; the library
+    routes such calls to the CUDA-core engine, with the same results."""
+    T, B, H = 700, 3, 64
+    f = W.norm_preserving_rnn(T, B, H, seed=5)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    hb = torch.empty(T * B * H + 1, device="cuda")
+    h = hb[1:].view(T, B, H)
+    h.copy_(cu(f["h"]))
+    gb = torch.empty(T * B * H + 3, device="cuda")
+    grad = gb[3:].view(T, B, H)
+    assert h.data_ptr() % 16 and grad.data_ptr() % 16
+    jac = lib.jacobians_rnn(h, cu(f["W_hh"]))
+    _, gi = lib.scan(jac, cu(f["g"]), grad_h=grad, grad_h_init=True, block0=64, block=8)
+    torch.cuda.synchronize()
+    assert rel_pair(grad, ref, gi, ref_init) <= TOL
+
+
 @pytest.mark.slow
 def test_rnn_norm_preserving_2p20_gate_iii(lib):
     """Reading 12 (iii): at T = 2^20 (C4's length) report the default path's

@@ -1,0 +1,41 @@
+"""compute-sanitizer tier: memcheck, racecheck and synccheck over
+small runs of every hand-written kernel family (tests/sanitize/small_paths.py:
+the tcgen05 / TMA / mbarrier kernels, the CUDA-core levels, the CSR scan and
+the peer-exchange release/acquire kernels).  Zero reported errors."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    pytest.skip("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "9", "--print-limit", "20",
+           sys.executable, os.path.join(ROOT, "tests", "sanitize", "small_paths.py")]
+    if tool == "memcheck":
+        cmd[1:1] = ["--leak-check", "no"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=3000, cwd=ROOT)
+    text = out.stdout + out.stderr
+    print(text[-3000:])
+    m = re.search(r"ERROR SUMMARY: (\d+) error", text) or re.search(r"SUMMARY: \d+ hazards? displayed \((\d+) error", text)
+    assert m is not None, text[-2000:]
+    assert int(m.group(1)) == 0 and out.returncode == 0, text[-3000:]
+    if tool == "racecheck":
+        assert re.search(r"\(0 errors, 0 warnings\)", text), text[-2000:]
+    assert "small paths ok" in text
