@@ -44,7 +44,12 @@
 // rate and cost 34 % XU.  Tried and slower: 16 epilogue warps
 // alternating between the two slots of a 4-sample super-tile with a
 // dedicated issuer warp (62 ms vs 46 ms at C4): one slot's epilogue then
-// cannot overlap the other's.
+// cannot overlap the other's; and each 8-warp group alternating the two
+// 2-sample halves of a super-tile through its one accumulator, issuing the
+// other half's MMAs right after converting D so that MMA latency hides
+// behind the other half's epilogue (47.7 ms): the epilogue, not MMA latency,
+// is the limit (ncu: issue 62 %, FMA and ALU pipes ~40 %, pipe-throttle and
+// dependency stalls).
 //
 // Scale bookkeeping: a chain row is c 2^E (fp32 c, integer E).  With y = c o d
 // and X = rint(y 2^sigma), the new row is c' 2^(E + 32 - sigma - tau).
