@@ -35,16 +35,19 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BPPSA backward ms vs sequential BP (1/2/4/8 GPU); % HBM/tensor roofline"
 C4 = dict(T=1 << 20, B=16, H=64, I=1)
-C4_BLOCK0, C4_BLOCK = 512, 32
+C4_BLOCK0, C4_BLOCK = 1024, 32
+E2E_BLOCK0 = 256        # the streamed e2e path: a short last-chunk walk (DESIGN "Host inputs")
 
 
 def c4_block0(world: int) -> int:
-    """Level-0 block per rank for time shards of 2^20 / world steps: the walk's
-    time is ~block0 dependent steps (its tiles fit one wave), the level-1 fold
-    scales with the number of blocks, so the block shrinks as the shard does
-    (a model of the single-GPU kernel times, DESIGN "Multi-GPU"; 512 at N = 1
-    is measured)."""
-    return {1: 512, 2: 256, 4: 256}.get(world, 128)
+    """Level-0 block per rank for time shards of 2^20 / world steps, measured
+    on one B200 (DESIGN "Multi-GPU"): the int8 walk runs one 128-chain tile per
+    SM for block0 dependent steps, so its time is ~ceil(tiles / 148) x block0
+    step times; the level-1 fold shrinks with fewer blocks.  Shard up + down:
+    N = 1: 1024 48.8 / 512 49.1 / 256 49.6 ms (full scan); N = 2 (T = 2^19):
+    256 25.2 / 512 24.8 / 1024 25.5; N = 4: 128 13.2 / 256 12.8 / 512 13.0;
+    N = 8: 64 7.26 / 128 6.89 / 256 6.78."""
+    return {1: 1024, 2: 512}.get(world, 256)
 SMALL = {   # secondary configs (N = 1 sweep): (T, B, H, block0, block)
     "c1": dict(T=1000, B=16, H=20, block0=8, block=8),
     "c2": dict(T=30000, B=16, H=20, block0=16, block=16),
@@ -284,11 +287,11 @@ def run_ours(args):
     if world > 1 and os.environ.get("BPPSA_EXCHANGE", "nccl") == "peer":
         from paper_1907_10134_b200.dist import PeerExchange
         exchange = PeerExchange(B, H)
-    ws = api.workspace(api.scan_workspace_size(jac, "blocked", C4_BLOCK0, C4_BLOCK), dev) if world == 1 else None
+    ws = api.workspace(api.scan_workspace_size(jac, "blocked", b0, C4_BLOCK), dev) if world == 1 else None
 
     def step(trace=None):
         if world == 1:
-            api.scan(jac, g, grad_h=grad, ws=ws, block0=C4_BLOCK0, block=C4_BLOCK, trace=trace)
+            api.scan(jac, g, grad_h=grad, ws=ws, block0=b0, block=C4_BLOCK, trace=trace)
         else:
             sharded_scan(_Traced(backend, trace), g, grad_h=grad, exchange=exchange)
         dWih, dWhh, db = api.weight_grads_rnn(x, h, grad, h_init=h_init, ws=ws_w, out=wout)
@@ -356,9 +359,9 @@ def run_ours(args):
         # NEXT-4: the affine scan (a loss on every step) on the same C4 inputs
         gen = torch.Generator(device=dev).manual_seed(args.seed)
         e_steps = torch.randn((T, B, H), device=dev, generator=gen) * 0.01
-        aff = _time(lambda: api.scan_affine(jac, g, e_steps, grad_h=grad, ws=ws, block0=C4_BLOCK0,
+        aff = _time(lambda: api.scan_affine(jac, g, e_steps, grad_h=grad, ws=ws, block0=b0,
                                             block=C4_BLOCK), reps=5, warm=2)
-        plain = _time(lambda: api.scan(jac, g, grad_h=grad, ws=ws, block0=C4_BLOCK0, block=C4_BLOCK), reps=5, warm=2)
+        plain = _time(lambda: api.scan(jac, g, grad_h=grad, ws=ws, block0=b0, block=C4_BLOCK), reps=5, warm=2)
         result["affine"] = {"workload": "C4 shapes, per-step losses e ~ 0.01 N(0,1) (synthetic)",
                             "scan_affine_ms": round(aff, 3), "scan_ms": round(plain, 3)}
         del e_steps
@@ -403,7 +406,7 @@ def e2e_ours(api, w, args):
     gp = torch.from_numpy(w["g"]).pin_memory()
     outs_h = [torch.empty(s, pin_memory=True) for s in ((H, I), (H, H), (H,), (B, H))]
     chunks = 16
-    sb = StreamedRnnBackward(T, B, H, I, chunks=chunks, block0=C4_BLOCK0, block=C4_BLOCK)
+    sb = StreamedRnnBackward(T, B, H, I, chunks=chunks, block0=E2E_BLOCK0, block=C4_BLOCK)
 
     def step():
         sb.run(hp, xp, Wp, gp, out_host=outs_h)
