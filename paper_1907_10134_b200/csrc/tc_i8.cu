@@ -39,9 +39,18 @@
 // tensor pipe.  The epilogue (4 s32 regions -> fp32 -> y -> row max -> 3
 // digit bytes) is ~11 instructions per element and sets the pace: ~1500
 // cycles per tile-step at C4, both the FMA and the ALU pipe ~60 % busy
-// (ncu, profiles/r02_tc_fold_i8_ncu.md).  Rounding to the 24-bit X is done on
-// the FMA pipe (rint24x2): cvt.rni is an XU instruction at a quarter of the
-// rate and cost 34 % XU.  Tried and slower: 16 epilogue warps
+// (ncu, profiles/r02_tc_fold_i8_ncu.md).  Rounding to the 24-bit X: half of
+// the 4-column groups on the FMA pipe (rint24x2), half with cvt.rni on the XU
+// pipe (I8_F2I_MASK = 0xAA; all-FMA 46.2 ms, all-XU 47.2, half 44.0 at C4:
+// the pipes balance).  A single-FFMA magic-number rounding (X < 2^22 with a
+// non-power-of-two row scale, 40.8 ms) was measured and rejected: 22-bit X
+// doubled the norm-preserving error at T = 65536 (8.5e-5 vs 4.0e-5, worst
+// block 1.05e-4 > the gate) and non-power-of-two scales break the integer
+// families' bit-exactness (scripts/prec_ab.py, scripts/ozaki_sim2.py).
+// Measured too (scripts/tc_i8_rate2.cu): an i8 MMA costs ~180 (TS) / ~250
+// (SS) cycles whatever N (64..256) and whether or not consecutive MMAs share
+// an accumulator, so the 6 MMAs per step are the tensor floor (~920 cycles
+// issue -> D ready in the fold's trace, scripts/f8_trace.py).  Tried and slower: 16 epilogue warps
 // alternating between the two slots of a 4-sample super-tile with a
 // dedicated issuer warp (62 ms vs 46 ms at C4): one slot's epilogue then
 // cannot overlap the other's; and each 8-warp group alternating the two
@@ -70,7 +79,12 @@ constexpr int TH = 64;                              // hidden size
 constexpr int TM = 128;                             // chains per tile (UMMA M)
 constexpr int NSLOT = 2;                            // tiles in flight per CTA
 constexpr int I8_HCH = 64;                          // steps of h staged per chunk
-constexpr int I8_WPS = 8, I8_EPI = 32 * I8_WPS, I8_NT = NSLOT * I8_EPI;
+#ifndef I8_WPS_DEF
+#define I8_WPS_DEF 8
+#endif
+constexpr int I8_WPS = I8_WPS_DEF, I8_EPI = 32 * I8_WPS, I8_NT = NSLOT * I8_EPI;
+constexpr int I8_CPT = 256 / I8_WPS;                // accumulator columns per epilogue thread (32 or 64)
+constexpr int I8_NCG = TH / I8_CPT;                 // threads per chain row (2: the row max is exchanged)
 constexpr int I8_B_BYTES = 4 * TH * TH;             // [W0|W1|W2|W3]: 256 rows x 64 B
 constexpr int I8_A_TILE = TM * TH;                  // one x-digit tile: 128 rows x 64 B
 constexpr int I8_OFF_A = I8_B_BYTES;                // [slot][digit]
@@ -80,6 +94,9 @@ constexpr int I8_OFF_RED = I8_OFF_H + NSLOT * 2 * I8_H_BYTES;   // [slot][parity
 constexpr int I8_OFF_BAR = I8_OFF_RED + NSLOT * 2 * TM * 8;
 constexpr int I8_SMEM = I8_OFF_BAR + 64 + 1024;
 constexpr uint32_t TMEM_COLS = 512;
+#ifndef I8_F2I_MASK
+#define I8_F2I_MASK 0xAA                            // groups of 4 columns rounded with cvt.rni (XU) instead of rint24x2
+#endif
 
 // K-major SWIZZLE_64B tile with 64-byte rows: the 16-byte chunk index is XORed
 // with address bits [7, 9) = (row / 2) % 4 (8-row atoms of 512 B)
@@ -211,7 +228,51 @@ __device__ __forceinline__ void regions_to_c(uint32_t t0, float2 (&c)[4]) {
                       make_float2(__int2float_rn(S0), __int2float_rn(S1)));
   }
 }
+// Four regions x 8 columns (t0 + 64 r + [0, 8)) into r[8 r + i], asynchronously:
+// the registers are written when tcgen05.wait::ld retires, so every wait is
+// followed by ld_retired(), an empty asm that "modifies" the registers the
+// wait completed -- no use of them can be scheduled above the wait.
+__device__ __forceinline__ void ld_regions8(uint32_t t0, uint32_t (&r)[32]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[8 * g]), "=r"(r[8 * g + 1]), "=r"(r[8 * g + 2]), "=r"(r[8 * g + 3]), "=r"(r[8 * g + 4]),
+                   "=r"(r[8 * g + 5]), "=r"(r[8 * g + 6]), "=r"(r[8 * g + 7])
+                 : "r"(t0 + 64u * g));
+}
+__device__ __forceinline__ void ld_retired(uint32_t (&r)[32]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    asm volatile(""
+                 : "+r"(r[8 * g]), "+r"(r[8 * g + 1]), "+r"(r[8 * g + 2]), "+r"(r[8 * g + 3]), "+r"(r[8 * g + 4]),
+                   "+r"(r[8 * g + 5]), "+r"(r[8 * g + 6]), "+r"(r[8 * g + 7])
+                 :
+                 : "memory");
+}
+// y = c' o d for 8 columns from the loaded regions (d: two float4 in shared memory)
+__device__ __forceinline__ void regions8_to_y(const uint32_t (&r)[32], float4 da, float4 db, float2* y) {
+  float2 c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int S0 = (int)r[2 * i] * 256 + (int)r[8 + 2 * i], S1 = (int)r[2 * i + 1] * 256 + (int)r[8 + 2 * i + 1];
+    const int T0 = (int)r[16 + 2 * i] * 256 + (int)r[24 + 2 * i], T1 = (int)r[16 + 2 * i + 1] * 256 + (int)r[24 + 2 * i + 1];
+    c[i] = __ffma2_rn(make_float2(__int2float_rn(T0), __int2float_rn(T1)), make_float2(0x1p-16f, 0x1p-16f),
+                      make_float2(__int2float_rn(S0), __int2float_rn(S1)));
+  }
+  y[0] = __fmul2_rn(c[0], make_float2(da.x, da.y));
+  y[1] = __fmul2_rn(c[1], make_float2(da.z, da.w));
+  y[2] = __fmul2_rn(c[2], make_float2(db.x, db.y));
+  y[3] = __fmul2_rn(c[3], make_float2(db.z, db.w));
+}
 
+#ifdef BPPSA_F8_TRACE
+// dev aid: clock64 per fold step on CTA 0, each slot's issuer lane: [slot * 8 + event][step]
+__device__ long long g_f8_trace[16][4096];
+#define F8T(ev, i) \
+  if (blockIdx.x == 0 && issuer && lane == 0 && (i) < 4096) g_f8_trace[g * 8 + (ev)][i] = clock64();
+#else
+#define F8T(ev, i)
+#endif
 #ifdef BPPSA_I8_TRACE
 // dev aid: clock64 per step on CTA 0 (warp 0, lane 0): [event][step]
 __device__ long long g_i8_trace[12][2048];
@@ -257,15 +318,17 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
 
   const int g = warp / I8_WPS, wl = warp % I8_WPS;
   const int quad = wl & 3, row = quad * 32 + lane;
-  const int cgp = wl >> 2;                          // column half: columns [32 cgp, 32 cgp + 32)
+  const int cgp = wl >> 2;                          // column group: columns [CPT cgp, CPT cgp + CPT)
   const int et = wl * 32 + lane;
   const bool issuer = wl == 0;
   const uint32_t slot_base = tmem + 256 * g;
-  const uint32_t t_mine = slot_base + ((uint32_t)(quad * 32) << 16) + 32 * cgp;
+  const uint32_t t_mine = slot_base + ((uint32_t)(quad * 32) << 16) + I8_CPT * cgp;
   const uint32_t a_tiles = su32(smem + I8_OFF_A + g * 3 * I8_A_TILE);
-  // this row's two 16-byte chunks (k in [32 cgp, 32 cgp + 32)) of a digit tile
-  const uint32_t a_c0 = a_tiles + (uint32_t)(row * 64 + (((2 * cgp) ^ ((row >> 1) & 3)) << 4));
-  const uint32_t a_c1 = a_tiles + (uint32_t)(row * 64 + (((2 * cgp + 1) ^ ((row >> 1) & 3)) << 4));
+  // this row's 16-byte chunks (k in [CPT cgp, CPT cgp + CPT)) of a digit tile
+  uint32_t a_c[I8_CPT / 16];
+#pragma unroll
+  for (int c = 0; c < I8_CPT / 16; ++c)
+    a_c[c] = a_tiles + (uint32_t)(row * 64 + ((((I8_CPT / 16) * cgp + c) ^ ((row >> 1) & 3)) << 4));
   char* const hsb0 = smem + I8_OFF_H + (2 * g) * I8_H_BYTES;
   auto hsb = [&](int c) { return reinterpret_cast<float*>(hsb0 + c * I8_H_BYTES); };
   const uint32_t red0 = su32(smem + I8_OFF_RED) + (uint32_t)(((g * 2) * TM + row) * 8);
@@ -283,6 +346,7 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
     for (int ks = 0; ks < 2; ++ks) bd[ks] = sdesc64(bb + (uint32_t)(32 * ks));
   }
   uint32_t ph = 0, par = 0;
+  int tstep = 0;
   const long long rowB = (long long)B * TH;
   // one chunk of tile tx from slot scx: I8_HCH steps of the h rows of its two
   // samples, asynchronous (one commit group)
@@ -340,80 +404,104 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
         else if (tn < ntiles) issue_chunk(tn, tile_s0(tn), hsb(cb ^ 1));
       }
       cb ^= 1;
-      uint32_t dp = hs_s + 4u * ((row >> 6) * I8_HCH * TH + 32 * cgp);   // this thread's d slice of step st
+      uint32_t dp = hs_s + 4u * ((row >> 6) * I8_HCH * TH + I8_CPT * cgp);   // this thread's d slice of step st
       for (int st = 0; st < n; ++st, dp += 4u * TH) {
-        float2 y[16];                               // y = c o d_t (this thread's 32 columns)
+        float2 y[I8_CPT / 2];                       // y = c o d_t (this thread's CPT columns)
         if (first) {
 #pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
+          for (int q4 = 0; q4 < I8_CPT / 4; ++q4) {
             const float4 d4 = lds128(dp + 16u * q4);
-            const int k0 = 32 * cgp + 4 * q4;
+            const int k0 = I8_CPT * cgp + 4 * q4;
             y[2 * q4] = make_float2(k0 == j && ok ? d4.x : 0.f, k0 + 1 == j && ok ? d4.y : 0.f);
             y[2 * q4 + 1] = make_float2(k0 + 2 == j && ok ? d4.z : 0.f, k0 + 3 == j && ok ? d4.w : 0.f);
           }
         } else {
+          F8T(0, tstep);
           if (issuer) {
             if (lane == 0) mbar_wait(dbar, ph);
             __syncwarp();
           }
           named_bar(5 + g, I8_EPI);
+          F8T(1, tstep);
           ph ^= 1;
           tc_fence_after();
+          {                                         // chunks of 8 columns, TMEM loads one chunk ahead
+            uint32_t ra[32], rb[32];
+            ld_regions8(t_mine, ra);
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            float2 c[4];
-            regions_to_c(t_mine + 8 * qq, c);
-            const float4 da = lds128(dp + 32u * qq), db = lds128(dp + 32u * qq + 16u);
-            y[4 * qq] = __fmul2_rn(c[0], make_float2(da.x, da.y));
-            y[4 * qq + 1] = __fmul2_rn(c[1], make_float2(da.z, da.w));
-            y[4 * qq + 2] = __fmul2_rn(c[2], make_float2(db.x, db.y));
-            y[4 * qq + 3] = __fmul2_rn(c[3], make_float2(db.z, db.w));
+            for (int c8 = 0; c8 < I8_CPT / 8; c8 += 2) {
+              tmem_wait_ld();
+              ld_retired(ra);
+              ld_regions8(t_mine + 8 * (c8 + 1), rb);
+              regions8_to_y(ra, lds128(dp + 32u * c8), lds128(dp + 32u * c8 + 16u), y + 4 * c8);
+              tmem_wait_ld();
+              ld_retired(rb);
+              if (c8 + 2 < I8_CPT / 8) ld_regions8(t_mine + 8 * (c8 + 2), ra);
+              regions8_to_y(rb, lds128(dp + 32u * (c8 + 1)), lds128(dp + 32u * (c8 + 1) + 16u), y + 4 * (c8 + 1));
+            }
           }
         }
         first = false;
+        F8T(2, tstep);
         float pm = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pm = fmaxf(pm, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
-        const uint32_t redp = red0 + par * (TM * 8);
-        asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
-        named_bar(pair_bar, 64);
-        uint32_t m2[2];
-        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
-        par ^= 1;
-        const float M = __uint_as_float(max(m2[0], m2[1]));
+        for (int i = 0; i < I8_CPT / 2; ++i) pm = fmaxf(pm, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
+        float M = pm;
+        if (I8_NCG == 2) {                          // the row's other half: exchanged through shared memory
+          const uint32_t redp = red0 + par * (TM * 8);
+          asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cgp), "r"(__float_as_uint(pm)) : "memory");
+          named_bar(pair_bar, 64);
+          uint32_t m2[2];
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(m2[0]), "=r"(m2[1]) : "r"(redp) : "memory");
+          par ^= 1;
+          M = __uint_as_float(max(m2[0], m2[1]));
+        }
+        F8T(3, tstep);
         const int sig = M > 0.f ? row_sigma(M) : 0;
         const float2 scl = make_float2(pow2f(sig), pow2f(sig)), scl8 = make_float2(pow2f(sig - 8), pow2f(sig - 8));
         if (M > 0.f) E += 32 - sig - tau;
         // X = rint(y 2^sigma) in [-2^23, 2^23): bytes 2, 1, 0 = digits x0 (s8), x1, x2 (u8);
-        // words of 4 consecutive k per digit (7 byte permutes per 4 elements)
-        uint32_t w0[8], w1[8], w2[8];
+        // words of 4 consecutive k per digit (7 byte permutes per 4 elements), 16 k per store
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          uint32_t X0, X1, X2, X3;
-          rint24x2(y[2 * u], scl, scl8, X0, X1);
-          rint24x2(y[2 * u + 1], scl, scl8, X2, X3);
-          const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
-          const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
-          w2[u] = prmt(p01, p23, 0x5410u);
-          w1[u] = prmt(p01, p23, 0x7632u);
-          w0[u] = prmt(q01, q23, 0x5410u);
+        for (int c16 = 0; c16 < I8_CPT / 16; ++c16) {
+          uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+          for (int uu = 0; uu < 4; ++uu) {
+            const int u = 4 * c16 + uu;
+            uint32_t X0, X1, X2, X3;
+            if ((I8_F2I_MASK >> (u & 7)) & 1) {     // this group rounds on the XU pipe (cvt.rni)
+              const float2 v0 = __fmul2_rn(y[2 * u], scl), v1 = __fmul2_rn(y[2 * u + 1], scl);
+              X0 = (uint32_t)__float2int_rn(v0.x), X1 = (uint32_t)__float2int_rn(v0.y);
+              X2 = (uint32_t)__float2int_rn(v1.x), X3 = (uint32_t)__float2int_rn(v1.y);
+            } else {
+              rint24x2(y[2 * u], scl, scl8, X0, X1);
+              rint24x2(y[2 * u + 1], scl, scl8, X2, X3);
+            }
+            const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
+            const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
+            w2[uu] = prmt(p01, p23, 0x5410u);
+            w1[uu] = prmt(p01, p23, 0x7632u);
+            w0[uu] = prmt(q01, q23, 0x5410u);
+          }
+          sts128u(a_c[c16], w0[0], w0[1], w0[2], w0[3]);
+          sts128u(a_c[c16] + I8_A_TILE, w1[0], w1[1], w1[2], w1[3]);
+          sts128u(a_c[c16] + 2 * I8_A_TILE, w2[0], w2[1], w2[2], w2[3]);
         }
-        sts128u(a_c0, w0[0], w0[1], w0[2], w0[3]);
-        sts128u(a_c1, w0[4], w0[5], w0[6], w0[7]);
-        sts128u(a_c0 + I8_A_TILE, w1[0], w1[1], w1[2], w1[3]);
-        sts128u(a_c1 + I8_A_TILE, w1[4], w1[5], w1[6], w1[7]);
-        sts128u(a_c0 + 2 * I8_A_TILE, w2[0], w2[1], w2[2], w2[3]);
-        sts128u(a_c1 + 2 * I8_A_TILE, w2[4], w2[5], w2[6], w2[7]);
+        F8T(4, tstep);
         fence_async_smem();                         // the digits -> visible to the tensor core
         tc_fence_before();
+        F8T(5, tstep);
         named_bar(3 + g, I8_EPI);                   // the slot's three digit tiles are complete
+        F8T(6, tstep);
         if (issuer) {
           tc_fence_after();
           mma6_i8_commit(slot_base, ad, bd, dbar);
         }
+        F8T(7, tstep);
+        ++tstep;
       }
     }
-    float2 cfin[16];
+    float2 cfin[I8_CPT / 2];
     if (!first) {                                   // D of the tile's last step
       if (issuer) {
         if (lane == 0) mbar_wait(dbar, ph);
@@ -423,7 +511,7 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
       ph ^= 1;
       tc_fence_after();
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
+      for (int qq = 0; qq < I8_CPT / 8; ++qq) {
         float2 c[4];
         regions_to_c(t_mine + 8 * qq, c);
 #pragma unroll
@@ -431,13 +519,13 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
       }
     } else {                                        // an empty head block: the identity
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        cfin[k] = make_float2(32 * cgp + 2 * k == j ? 1.f : 0.f, 32 * cgp + 2 * k + 1 == j ? 1.f : 0.f);
+      for (int k = 0; k < I8_CPT / 2; ++k)
+        cfin[k] = make_float2(I8_CPT * cgp + 2 * k == j ? 1.f : 0.f, I8_CPT * cgp + 2 * k + 1 == j ? 1.f : 0.f);
     }
     if (ok) {
-      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + 32 * cgp);
+      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH + I8_CPT * cgp);
 #pragma unroll
-      for (int k4 = 0; k4 < 8; ++k4)
+      for (int k4 = 0; k4 < I8_CPT / 4; ++k4)
         dst[k4] = make_float4(ldexpf(cfin[2 * k4].x, E), ldexpf(cfin[2 * k4].y, E), ldexpf(cfin[2 * k4 + 1].x, E),
                               ldexpf(cfin[2 * k4 + 1].y, E));
     }
@@ -751,6 +839,11 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8_kernel(LeafArgs a, int C
 
 }  // namespace
 
+#ifdef BPPSA_F8_TRACE
+extern "C" int bppsa_debug_f8_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_f8_trace, sizeof(g_f8_trace));
+}
+#endif
 #ifdef BPPSA_I8_TRACE
 extern "C" int bppsa_debug_i8_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, g_i8_trace, sizeof(g_i8_trace));
