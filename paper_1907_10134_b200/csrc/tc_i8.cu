@@ -39,10 +39,11 @@
 // tensor pipe.  The epilogue (4 s32 regions -> fp32 -> y -> row max -> 3
 // digit bytes) is ~11 instructions per element and sets the pace: ~1500
 // cycles per tile-step at C4, both the FMA and the ALU pipe ~60 % busy
-// (ncu, profiles/r02_tc_fold_i8_ncu.md).  Rounding to the 24-bit X: half of
-// the 4-column groups on the FMA pipe (rint24x2), half with cvt.rni on the XU
-// pipe (I8_F2I_MASK = 0xAA; all-FMA 46.2 ms, all-XU 47.2, half 44.0 at C4:
-// the pipes balance).  A single-FFMA magic-number rounding (X < 2^22 with a
+// (ncu, profiles/r02_tc_fold_i8_ncu.md).  Rounding to the 24-bit X: some of
+// the 4-column groups on the FMA pipe (rint24x2), the rest with cvt.rni on
+// the XU pipe (I8_F2I_MASK; this two-slot kernel at C4: all-FMA 46.2 ms,
+// all-XU 47.2, half 44.0 -- the pipes balance; the default ring kernel
+// further below: 0xAA ~ 0xEE ~ 0xFF ~ 40 ms).  A single-FFMA magic-number rounding (X < 2^22 with a
 // non-power-of-two row scale, 40.8 ms) was measured and rejected: 22-bit X
 // doubled the norm-preserving error at T = 65536 (8.5e-5 vs 4.0e-5, worst
 // block 1.05e-4 > the gate) and non-power-of-two scales break the integer
@@ -50,7 +51,10 @@
 // Measured too (scripts/tc_i8_rate2.cu): an i8 MMA costs ~180 (TS) / ~250
 // (SS) cycles whatever N (64..256) and whether or not consecutive MMAs share
 // an accumulator, so the 6 MMAs per step are the tensor floor (~920 cycles
-// issue -> D ready in the fold's trace, scripts/f8_trace.py).  Tried and slower: 16 epilogue warps
+// issue -> D ready in the fold's trace, scripts/f8_trace.py).  This two-slot
+// kernel is the fallback (-DBPPSA_FOLD_TWO_SLOT); the default is the ring
+// kernel tc_fold_i8r_kernel below (4 tiles over 2 accumulators, 40 ms).
+// Tried and slower: 16 epilogue warps
 // alternating between the two slots of a 4-sample super-tile with a
 // dedicated issuer warp (62 ms vs 46 ms at C4): one slot's epilogue then
 // cannot overlap the other's; and each 8-warp group alternating the two
@@ -95,7 +99,7 @@ constexpr int I8_OFF_BAR = I8_OFF_RED + NSLOT * 2 * TM * 8;
 constexpr int I8_SMEM = I8_OFF_BAR + 64 + 1024;
 constexpr uint32_t TMEM_COLS = 512;
 #ifndef I8_F2I_MASK
-#define I8_F2I_MASK 0xAA                            // groups of 4 columns rounded with cvt.rni (XU) instead of rint24x2
+#define I8_F2I_MASK 0xEE                            // groups of 4 columns rounded with cvt.rni (XU) instead of rint24x2
 #endif
 
 // K-major SWIZZLE_64B tile with 64-byte rows: the 16-byte chunk index is XORed
@@ -540,6 +544,319 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
 
 
 // ---------------------------------------------------------------------------
+// The same fold with FOUR tiles in flight over TWO accumulators (the "ring").
+// In the two-slot kernel above a slot holds its 256 accumulator columns from
+// the MMA issue until its epilogue has read them AND produced the next digits,
+// so the tensor pipe idles whenever an epilogue (~2000 cycles) outlasts the
+// other slot's MMAs (~920): 40 % tensor-pipe activity (ncu).  Here a tile group
+// releases its accumulator as soon as the regions are converted to y (fp32 in
+// registers), and the two accumulators are handed out by TICKETS: when a
+// group's digits are complete, its first warp takes ticket it = atomicAdd(
+// &ticket, 1) and uses accumulator it % 2 once the holder of ticket it - 2 has
+// released it (rel[it % 2] >= 4 (it / 2): a monotonic release count per
+// accumulator; an mbarrier phase parity would alias once three tickets are
+// outstanding on one accumulator), so a ready group never waits
+// behind a slower one (a strict round robin did: 44.5 ms at C4 with three
+// groups and an issuer warp).  The group's own warps learn the accumulator
+// from which of d_full[g][0 / 1] the MMA commit completes.  mbarrier-only
+// synchronisation between groups; a group = 4 warps, thread = chain row x 64
+// columns (no row-max exchange).  4 groups = 512 threads (128 registers).
+// ---------------------------------------------------------------------------
+#ifndef R_NT_DEF
+#define R_NT_DEF 4
+#endif
+constexpr int R_NT = R_NT_DEF;                      // tile groups
+#ifndef R_PIPE_DEF
+#define R_PIPE_DEF 1
+#endif
+constexpr bool R_PIPE = R_PIPE_DEF;
+constexpr int R_WPS = 4, R_EPI = 32 * R_WPS;        // warps per group
+constexpr int R_THREADS = R_NT * R_EPI;
+#ifndef R_HCH_DEF
+#define R_HCH_DEF 24
+#endif
+constexpr int R_HCH = R_HCH_DEF;                    // steps of h staged per chunk
+constexpr int R_H_BYTES = 2 * R_HCH * TH * 4;
+constexpr int R_OFF_A = I8_B_BYTES;                 // [group][digit] tiles
+constexpr int R_OFF_H = R_OFF_A + R_NT * 3 * I8_A_TILE;
+constexpr int R_OFF_BAR = R_OFF_H + R_NT * 2 * R_H_BYTES;
+constexpr int R_SMEM = R_OFF_BAR + 256 + 1024;
+static_assert(R_SMEM <= 232448, "ring fold shared memory");
+
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok)
+               : "r"(bar), "r"(parity)
+               : "memory");
+  return ok != 0;
+}
+
+__global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                                 long long n_out, long long q0) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + R_OFF_BAR);
+  uint64_t* d_full = bars;                          // [R_NT][2]
+  uint32_t* rel = reinterpret_cast<uint32_t*>(bars + 2 * R_NT);   // [2] warps that released each accumulator
+  uint32_t* ticket = rel + 2;
+  uint32_t* tmem_slot = ticket + 1;
+  uint32_t* wred = tmem_slot + 1;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+  const long long nq = n_out - q0;
+  const int nbp = (B + 1) / 2;
+  const long long ntiles = (long long)nbp * nq;
+
+  if (threadIdx.x == 0) wred[0] = 0;
+  __syncthreads();
+  int tau;
+  w_digits(a.W, smem, wred, &tau);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < 2 * R_NT; ++i) mbar_init(su32(&d_full[i]), 1);
+      rel[0] = rel[1] = 0;
+      *ticket = 0;
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int g = warp / R_WPS, wl = warp % R_WPS;    // tile group g: 4 warps, thread = row x 64 columns
+  const int row = wl * 32 + lane;
+  const int et = wl * 32 + lane;
+  const uint32_t t_lane = (uint32_t)(wl * 32) << 16;
+  const uint32_t a_tiles = su32(smem + R_OFF_A + g * 3 * I8_A_TILE);
+  uint32_t a_c[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) a_c[c] = a_tiles + (uint32_t)(row * 64 + ((c ^ ((row >> 1) & 3)) << 4));
+  uint64_t ad[6], bd[2];
+  {
+    const uint32_t bb = su32(smem);
+#pragma unroll
+    for (int dgt = 0; dgt < 3; ++dgt)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) ad[2 * dgt + ks] = sdesc64(a_tiles + (uint32_t)(dgt * I8_A_TILE + 32 * ks));
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) bd[ks] = sdesc64(bb + (uint32_t)(32 * ks));
+  }
+  char* const hsb0 = smem + R_OFF_H + (2 * g) * R_H_BYTES;
+  auto hsb = [&](int c) { return reinterpret_cast<float*>(hsb0 + c * R_H_BYTES); };
+  const uint32_t dfull0 = su32(&d_full[2 * g]);     // + 8 b: this group's commit barrier for accumulator b
+  uint32_t fph = 0;                                 // phase bits of d_full[g][0 / 1]
+  int cur = 0;                                      // the accumulator of this group's outstanding batch
+  const long long rowB = (long long)B * TH;
+  auto issue_chunk = [&](long long tx, long long scx, float* hb) {
+    const long long qx = q0 + tx / nbp;
+    const int bpx = (int)(tx % nbp);
+    const int nx = (int)min((long long)R_HCH, min(qx * C + (long long)C, S) - scx);
+    for (int e = et; e < 2 * nx * 16; e += R_EPI) {
+      const int bb2 = e / (nx * 16), rem = e % (nx * 16), st = rem / 16, ch = rem % 16;
+      const uint32_t dst = su32(hb + (bb2 * R_HCH + st) * TH + ch * 4);
+      const int bs = bpx * 2 + bb2;
+      if (bs < B)
+        cp_async16(dst, a.h + (long long)a.seg.time_of(scx + st) * rowB + (long long)bs * TH + ch * 4);
+      else
+        sts128(dst, 0.f, 0.f, 0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto tile_s0 = [&](long long tx) {
+    const long long qx = q0 + tx / nbp;
+    return (a.seg.head && qx == 0) ? 1LL : qx * C;
+  };
+  // the group's digits are complete: warp 0 takes a ticket and issues the batch
+  auto issue = [&]() {
+    named_bar(1 + R_NT + g, R_EPI);
+    if (wl == 0) {
+      uint32_t it = 0;
+      if (lane == 0) {
+        it = atomicAdd(ticket, 1u);
+        const uint32_t need = (it >> 1) * R_WPS, ra = su32(&rel[it & 1]);
+        uint32_t v;
+        while (true) {
+          asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(ra) : "memory");
+          if (v >= need) break;
+          __nanosleep(20);
+        }
+      }
+      __syncwarp();
+      it = __shfl_sync(0xffffffffu, it, 0);
+      tc_fence_after();
+      mma6_i8_commit(tmem + 256u * (it & 1), ad, bd, dfull0 + 8u * (it & 1));
+    }
+  };
+  // wait for the group's outstanding batch; returns its TMEM base for this warp's lanes
+  auto wait_d = [&]() {
+    int bsel = 0;
+    if (lane == 0) {
+      while (true) {
+        if (mbar_test(dfull0, fph & 1)) { bsel = 0; break; }
+        if (mbar_test(dfull0 + 8u, (fph >> 1) & 1)) { bsel = 1; break; }
+      }
+    }
+    __syncwarp();
+    bsel = __shfl_sync(0xffffffffu, bsel, 0);
+    fph ^= 1u << bsel;
+    cur = bsel;
+    tc_fence_after();
+    return tmem + 256u * (uint32_t)bsel + t_lane;
+  };
+  auto release_d = [&]() {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;\n" ::"r"(su32(&rel[cur])) : "memory");
+  };
+  int cb = 0;
+  {
+    const long long t0 = R_NT * (long long)blockIdx.x + g;
+    if (t0 < ntiles) issue_chunk(t0, tile_s0(t0), hsb(0));
+  }
+  for (long long tau_t = R_NT * (long long)blockIdx.x + g; tau_t < ntiles; tau_t += R_NT * (long long)gridDim.x) {
+    const long long q = q0 + tau_t / nbp;
+    const int bp = (int)(tau_t % nbp);
+    const int b = bp * 2 + (row >> 6);
+    const int j = row & 63;
+    const bool ok = b < B;
+    const long long s0 = (a.seg.head && q == 0) ? 1 : q * C, s1 = min(q * C + (long long)C, S);
+    int E = 0;                                      // chain row = c 2^E
+    bool first = true;
+    for (long long sc = s0; sc < s1; sc += R_HCH) {
+      const int n = (int)min((long long)R_HCH, s1 - sc);
+      float* hs = hsb(cb);
+      const uint32_t hs_s = su32(hs);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      named_bar(1 + g, R_EPI);                      // copies landed; the previous chunk is consumed
+      for (int e = et; e < 2 * n * 16; e += R_EPI) {   // d = 1 - h^2 in place
+        const int bb2 = e / (n * 16), rem = e % (n * 16), st = rem / 16, ch = rem % 16;
+        const uint32_t p = hs_s + 4u * ((bb2 * R_HCH + st) * TH + ch * 4);
+        const float4 h4 = lds128(p);
+        sts128(p, fmaf(-h4.x, h4.x, 1.f), fmaf(-h4.y, h4.y, 1.f), fmaf(-h4.z, h4.z, 1.f), fmaf(-h4.w, h4.w, 1.f));
+      }
+      named_bar(1 + g, R_EPI);
+      {
+        const long long tn = tau_t + R_NT * (long long)gridDim.x;
+        if (sc + R_HCH < s1) issue_chunk(tau_t, sc + R_HCH, hsb(cb ^ 1));
+        else if (tn < ntiles) issue_chunk(tn, tile_s0(tn), hsb(cb ^ 1));
+      }
+      cb ^= 1;
+      uint32_t dp = hs_s + 4u * ((row >> 6) * R_HCH * TH);
+      for (int st = 0; st < n; ++st, dp += 4u * TH) {
+        float2 y[32];
+        if (first) {
+#pragma unroll
+          for (int q4 = 0; q4 < 16; ++q4) {
+            const float4 d4 = lds128(dp + 16u * q4);
+            const int k0 = 4 * q4;
+            y[2 * q4] = make_float2(k0 == j && ok ? d4.x : 0.f, k0 + 1 == j && ok ? d4.y : 0.f);
+            y[2 * q4 + 1] = make_float2(k0 + 2 == j && ok ? d4.z : 0.f, k0 + 3 == j && ok ? d4.w : 0.f);
+          }
+        } else {
+          const uint32_t td = wait_d();
+          if (R_PIPE) {                             // TMEM loads one 8-column chunk ahead (64 registers)
+            uint32_t ra[32], rb[32];
+            ld_regions8(td, ra);
+#pragma unroll
+            for (int c8 = 0; c8 < 8; c8 += 2) {
+              tmem_wait_ld();
+              ld_retired(ra);
+              ld_regions8(td + 8 * (c8 + 1), rb);
+              regions8_to_y(ra, lds128(dp + 32u * c8), lds128(dp + 32u * c8 + 16u), y + 4 * c8);
+              tmem_wait_ld();
+              ld_retired(rb);
+              if (c8 + 2 < 8) ld_regions8(td + 8 * (c8 + 2), ra);
+              regions8_to_y(rb, lds128(dp + 32u * (c8 + 1)), lds128(dp + 32u * (c8 + 1) + 16u), y + 4 * (c8 + 1));
+            }
+          } else {
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+              uint32_t ra[32];
+              ld_regions8(td + 8 * c8, ra);
+              tmem_wait_ld();
+              ld_retired(ra);
+              regions8_to_y(ra, lds128(dp + 32u * c8), lds128(dp + 32u * c8 + 16u), y + 4 * c8);
+            }
+          }
+          release_d();
+        }
+        first = false;
+        float M = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) M = fmaxf(M, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
+        const int sig = M > 0.f ? row_sigma(M) : 0;
+        const float2 scl = make_float2(pow2f(sig), pow2f(sig)), scl8 = make_float2(pow2f(sig - 8), pow2f(sig - 8));
+        if (M > 0.f) E += 32 - sig - tau;
+#pragma unroll
+        for (int c16 = 0; c16 < 4; ++c16) {
+          uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+          for (int uu = 0; uu < 4; ++uu) {
+            const int u = 4 * c16 + uu;
+            uint32_t X0, X1, X2, X3;
+            if ((I8_F2I_MASK >> (u & 7)) & 1) {
+              const float2 v0 = __fmul2_rn(y[2 * u], scl), v1 = __fmul2_rn(y[2 * u + 1], scl);
+              X0 = (uint32_t)__float2int_rn(v0.x), X1 = (uint32_t)__float2int_rn(v0.y);
+              X2 = (uint32_t)__float2int_rn(v1.x), X3 = (uint32_t)__float2int_rn(v1.y);
+            } else {
+              rint24x2(y[2 * u], scl, scl8, X0, X1);
+              rint24x2(y[2 * u + 1], scl, scl8, X2, X3);
+            }
+            const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
+            const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
+            w2[uu] = prmt(p01, p23, 0x5410u);
+            w1[uu] = prmt(p01, p23, 0x7632u);
+            w0[uu] = prmt(q01, q23, 0x5410u);
+          }
+          sts128u(a_c[c16], w0[0], w0[1], w0[2], w0[3]);
+          sts128u(a_c[c16] + I8_A_TILE, w1[0], w1[1], w1[2], w1[3]);
+          sts128u(a_c[c16] + 2 * I8_A_TILE, w2[0], w2[1], w2[2], w2[3]);
+        }
+        fence_async_smem();                         // the digits -> visible to the tensor core
+        tc_fence_before();
+        issue();
+      }
+    }
+    float2 cfin[32];
+    if (!first) {                                   // D of the tile's last step
+      const uint32_t td = wait_d();
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        float2 c[4];
+        regions_to_c(td + 8 * qq, c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cfin[4 * qq + i] = c[i];
+      }
+      release_d();
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 32; ++kk) cfin[kk] = make_float2(2 * kk == j ? 1.f : 0.f, 2 * kk + 1 == j ? 1.f : 0.f);
+    }
+    if (ok) {
+      float4* dst = reinterpret_cast<float4*>(agg_out + (((long long)b * n_out + q) * TH + j) * TH);
+#pragma unroll
+      for (int k4 = 0; k4 < 16; ++k4)
+        dst[k4] = make_float4(ldexpf(cfin[2 * k4].x, E), ldexpf(cfin[2 * k4].y, E), ldexpf(cfin[2 * k4 + 1].x, E),
+                              ldexpf(cfin[2 * k4 + 1].y, E));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Level-0 DOWN-walk on the integer tensor cores (the down-sweep's GEMV chains,
 // every down-sweep op is a vector times the transposed Jacobians).
 // Chain (b, q) starts from the carry of block q (the seed for the head
@@ -857,6 +1174,15 @@ cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long lon
   const long long ntiles = (long long)((a.seg.B + 1) / 2) * (n_out - q0);
   const int grid = (int)std::min<long long>((ntiles + 1) / 2, num_sms);
   if (grid <= 0) return cudaSuccess;
+#ifndef BPPSA_FOLD_TWO_SLOT
+  {
+    const int gr = (int)std::min<long long>((ntiles + R_NT - 1) / R_NT, num_sms);
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_fold_i8r_kernel), R_SMEM);
+    if (e != cudaSuccess) return e;
+    tc_fold_i8r_kernel<<<gr, R_THREADS, R_SMEM, st>>>(a, C, agg_out, n_out, q0);
+    return cudaGetLastError();
+  }
+#endif
   cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(tc_fold_i8_kernel), I8_SMEM);
   if (e != cudaSuccess) return e;
   tc_fold_i8_kernel<<<grid, I8_NT, I8_SMEM, st>>>(a, C, agg_out, n_out, q0);
