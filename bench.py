@@ -339,8 +339,8 @@ def run_ours(args):
         i8_peak = 2.0 * pk["bf16_tflops"]
         peak = i8_peak / 9.0
         result["roofline"] = {"bound": "tensor",
-                              "kernel": "tc_fold_i8_kernel (level-0 fused fold, tcgen05 kind::i8, exact s32 "
-                                        "accumulation of 8-bit digit products)",
+                              "kernel": "tc_fold_i8r_kernel (level-0 fused fold, tcgen05 kind::i8, exact s32 "
+                                        "accumulation of 8-bit digit products; 4 tiles over 2 TMEM accumulators)",
                               "achieved": round(achieved, 3), "peak": round(peak, 2),
                               "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                               # the ncu capture is of the single-GPU launch (T = 2^20)

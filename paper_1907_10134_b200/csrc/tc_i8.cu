@@ -557,9 +557,11 @@ __global__ void __launch_bounds__(I8_NT, 1) tc_fold_i8_kernel(LeafArgs a, int C,
 // accumulator; an mbarrier phase parity would alias once three tickets are
 // outstanding on one accumulator), so a ready group never waits
 // behind a slower one (a strict round robin did: 44.5 ms at C4 with three
-// groups and an issuer warp).  The group's own warps learn the accumulator
-// from which of d_full[g][0 / 1] the MMA commit completes.  mbarrier-only
-// synchronisation between groups; a group = 4 warps, thread = chain row x 64
+// groups and an issuer warp).  Warp 0 takes the ticket when its own digits
+// are stored and publishes it % 2 in bufsel (by round parity) before the
+// group's digit barrier, so the group's warps know their accumulator (polling
+// two commit barriers instead spent 17 % of the warp samples in the spin
+// loop).  mbarrier / release-count synchronisation between groups; a group = 4 warps, thread = chain row x 64
 // columns (no row-max exchange).  4 groups = 512 threads (128 registers).
 // ---------------------------------------------------------------------------
 #ifndef R_NT_DEF
@@ -583,13 +585,15 @@ constexpr int R_OFF_BAR = R_OFF_H + R_NT * 2 * R_H_BYTES;
 constexpr int R_SMEM = R_OFF_BAR + 256 + 1024;
 static_assert(R_SMEM <= 232448, "ring fold shared memory");
 
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-               : "=r"(ok)
-               : "r"(bar), "r"(parity)
-               : "memory");
-  return ok != 0;
+// try_wait with a suspend-time hint: the waiting lane sleeps in the barrier
+// unit instead of re-issuing the probe
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+#ifndef R_NO_SLEEP
+  asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra W_%=;\n}\n" ::"r"(
+                   bar), "r"(parity), "r"(1000000u) : "memory");
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 
 __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
@@ -597,10 +601,11 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
   extern __shared__ uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + R_OFF_BAR);
-  uint64_t* d_full = bars;                          // [R_NT][2]
-  uint32_t* rel = reinterpret_cast<uint32_t*>(bars + 2 * R_NT);   // [2] warps that released each accumulator
+  uint64_t* d_full = bars;                          // [R_NT]
+  uint32_t* rel = reinterpret_cast<uint32_t*>(bars + R_NT);   // [2] warps that released each accumulator
   uint32_t* ticket = rel + 2;
-  uint32_t* tmem_slot = ticket + 1;
+  uint32_t* bufsel = ticket + 1;                    // [R_NT][2] accumulator of a group's batch (by round parity)
+  uint32_t* tmem_slot = bufsel + 2 * R_NT;
   uint32_t* wred = tmem_slot + 1;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int B = a.seg.B;
@@ -615,7 +620,7 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
   w_digits(a.W, smem, wred, &tau);
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < 2 * R_NT; ++i) mbar_init(su32(&d_full[i]), 1);
+      for (int i = 0; i < R_NT; ++i) mbar_init(su32(&d_full[i]), 1);
       rel[0] = rel[1] = 0;
       *ticket = 0;
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -651,9 +656,9 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
   }
   char* const hsb0 = smem + R_OFF_H + (2 * g) * R_H_BYTES;
   auto hsb = [&](int c) { return reinterpret_cast<float*>(hsb0 + c * R_H_BYTES); };
-  const uint32_t dfull0 = su32(&d_full[2 * g]);     // + 8 b: this group's commit barrier for accumulator b
-  uint32_t fph = 0;                                 // phase bits of d_full[g][0 / 1]
-  int cur = 0;                                      // the accumulator of this group's outstanding batch
+  const uint32_t dfull = su32(&d_full[g]);
+  uint32_t kr = 0;                                  // this group's MMA rounds so far
+  int cur = 0;                                      // the accumulator of the group's outstanding batch
   const long long rowB = (long long)B * TH;
   auto issue_chunk = [&](long long tx, long long scx, float* hb) {
     const long long qx = q0 + tx / nbp;
@@ -674,13 +679,22 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
     const long long qx = q0 + tx / nbp;
     return (a.seg.head && qx == 0) ? 1LL : qx * C;
   };
-  // the group's digits are complete: warp 0 takes a ticket and issues the batch
+  // this warp's digits are stored: warp 0 takes the group's ticket (written to
+  // bufsel by round parity), the group syncs, warp 0 issues once the
+  // accumulator is released
   auto issue = [&]() {
-    named_bar(1 + R_NT + g, R_EPI);
+    uint32_t it = 0;
     if (wl == 0) {
-      uint32_t it = 0;
       if (lane == 0) {
         it = atomicAdd(ticket, 1u);
+        bufsel[2 * g + (kr & 1)] = it & 1;
+      }
+      it = __shfl_sync(0xffffffffu, it, 0);
+    }
+    named_bar(1 + R_NT + g, R_EPI);
+    cur = (int)*reinterpret_cast<volatile uint32_t*>(&bufsel[2 * g + (kr & 1)]);
+    if (wl == 0) {
+      if (lane == 0) {
         const uint32_t need = (it >> 1) * R_WPS, ra = su32(&rel[it & 1]);
         uint32_t v;
         while (true) {
@@ -690,26 +704,17 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
         }
       }
       __syncwarp();
-      it = __shfl_sync(0xffffffffu, it, 0);
       tc_fence_after();
-      mma6_i8_commit(tmem + 256u * (it & 1), ad, bd, dfull0 + 8u * (it & 1));
+      mma6_i8_commit(tmem + 256u * (uint32_t)cur, ad, bd, dfull);
     }
   };
   // wait for the group's outstanding batch; returns its TMEM base for this warp's lanes
   auto wait_d = [&]() {
-    int bsel = 0;
-    if (lane == 0) {
-      while (true) {
-        if (mbar_test(dfull0, fph & 1)) { bsel = 0; break; }
-        if (mbar_test(dfull0 + 8u, (fph >> 1) & 1)) { bsel = 1; break; }
-      }
-    }
+    if (lane == 0) mbar_wait_sleep(dfull, kr & 1);
     __syncwarp();
-    bsel = __shfl_sync(0xffffffffu, bsel, 0);
-    fph ^= 1u << bsel;
-    cur = bsel;
+    ++kr;
     tc_fence_after();
-    return tmem + 256u * (uint32_t)bsel + t_lane;
+    return tmem + 256u * (uint32_t)cur + t_lane;
   };
   auto release_d = [&]() {
     tc_fence_before();

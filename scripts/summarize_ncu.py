@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise ncu outputs brought back in gpurun_out/ into profiles/ (tracked).
 
-  python scripts/summarize_ncu.py ROUND LAUNCHES_CSV [REPORT.ncu-rep KERNEL_KEY] ...
+  python scripts/summarize_ncu.py ROUND LAUNCHES_CSV|- [REPORT.ncu-rep KERNEL_KEY] ...
 
 Writes profiles/<ROUND>_launches.md (per-kernel share of the step from the
 `--metrics gpu__time_duration.sum` launch list), profiles/<ROUND>_<key>_ncu.md
@@ -42,6 +42,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__occupancy_limit_registers", "smsp__issue_active.avg.pct_of_peak_sustained_active",
@@ -90,7 +92,8 @@ def report(path, key, rnd):
 if __name__ == "__main__":
     rnd = sys.argv[1]
     os.makedirs(PROF, exist_ok=True)
-    launches(sys.argv[2], rnd)
+    if sys.argv[2] != "-":
+        launches(sys.argv[2], rnd)
     rest = sys.argv[3:]
     for i in range(0, len(rest), 2):
         report(rest[i], rest[i + 1], rnd)
