@@ -28,12 +28,15 @@ def launches(path, rnd):
     agg = defaultdict(list)
     for r in data:
         agg[r[ki].split("(")[0].replace("void ", "")[:70]].append(float(r[vi].replace(",", "")) * UNIT[r[ui]])
-    tot = sum(sum(v) for v in agg.values())
+    ours = {k: v for k, v in agg.items() if k.startswith("bppsa::")}
+    tot = sum(sum(v) for v in ours.values())
     out = [f"# {rnd}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)", "",
-           f"source: {os.path.basename(path)}; cold-cache serialised launches — compare SHARES, not absolutes.", "",
-           "| kernel | launches | avg ms | total ms | share |", "|---|---|---|---|---|"]
+           f"source: {os.path.basename(path)}; cold-cache serialised launches — compare SHARES, not absolutes.",
+           "Shares are of the library's (bppsa::) kernels; the rest is the bench's input build (cuDNN forward).",
+           "", "| kernel | launches | avg ms | total ms | share |", "|---|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-        out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.4f} | {sum(v):.3f} | {sum(v) / tot:.1%} |")
+        sh = f"{sum(v) / tot:.1%}" if k in ours else "(input build)"
+        out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.4f} | {sum(v):.3f} | {sh} |")
     open(os.path.join(PROF, f"{rnd}_launches.md"), "w").write("\n".join(out) + "\n")
     print("\n".join(out))
 
