@@ -349,6 +349,20 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n,
                                    int up_levels, int down_levels,
                                    long long max_contributions,
                                    bppsa_csr_plan** plan);
+/* The same schedule analysis WITHOUT the numeric plan (host only: no
+ * contribution lists, no device memory, no CUDA call): product patterns by a
+ * bitset Gustavson product, contribution pairs in closed form
+ * sum_k nnz(L[:, k]) nnz(R[k, :]).  For schedules whose contribution lists do
+ * not fit, e.g. the paper's (u, dl) = (3, 4) on the 97 %-pruned
+ * VGG-11 (9.1e10 pairs; DESIGN reading 22).  Answers bppsa_csr_plan_info
+ * (contributions = the pairs the numeric plan would hold) and
+ * bppsa_csr_plan_steps with the same records bppsa_csr_plan_create gives;
+ * bppsa_csr_plan_workspace_size and bppsa_csr_scan return NOT_SUPPORTED.
+ * Errors as plan_create; NOT_SUPPORTED when a product's bit rows exceed
+ * 16 GB or its output 2^31 entries.                                         */
+bppsa_status bppsa_csr_plan_create_symbolic(const bppsa_csr_pattern* chain, int n,
+                                            int up_levels, int down_levels,
+                                            bppsa_csr_plan** plan);
 void bppsa_csr_plan_destroy(bppsa_csr_plan* plan);
 /* Workspace for batch B given which elements carry per-sample data.        */
 bppsa_status bppsa_csr_plan_workspace_size(const bppsa_csr_plan* plan, int B,

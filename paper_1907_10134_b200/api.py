@@ -67,6 +67,7 @@ class _CsrPat(C.Structure):
 _ll, _pp = C.c_longlong, C.POINTER(_vp)
 EXPORTS.update({
     "bppsa_csr_plan_create": (_i, [C.POINTER(_CsrPat), _i, _i, _i, _ll, C.POINTER(_vp)]),
+    "bppsa_csr_plan_create_symbolic": (_i, [C.POINTER(_CsrPat), _i, _i, _i, C.POINTER(_vp)]),
     "bppsa_csr_plan_destroy": (None, [_vp]),
     "bppsa_csr_plan_workspace_size": (_i, [_vp, _i, C.POINTER(_i), C.POINTER(_sz)]),
     "bppsa_csr_plan_info": (_i, [_vp, C.POINTER(_ll), C.POINTER(_ll), C.POINTER(_i)]),
@@ -546,9 +547,7 @@ def csr_identity_build(d, device=None, stream=None):
     return ip, ix
 
 
-def csr_plan_create(patterns, up_levels: int, down_levels: int, max_contributions: int = 0) -> CsrPlan:
-    """patterns: [(rows, cols, indptr int64 ndarray, indices int32 ndarray)] for
-    J_1^T .. J_n^T (time order)."""
+def _csr_pattern_array(patterns):
     import numpy as np
     n = len(patterns)
     keep = []
@@ -558,11 +557,30 @@ def csr_plan_create(patterns, up_levels: int, down_levels: int, max_contribution
         ix = np.ascontiguousarray(ix, dtype=np.int32)
         keep += [ip, ix]
         arr[k] = _CsrPat(rows, cols, int(ip[-1]), ip.ctypes.data, ix.ctypes.data)
+    return arr, keep
+
+
+def csr_plan_create(patterns, up_levels: int, down_levels: int, max_contributions: int = 0) -> CsrPlan:
+    """patterns: [(rows, cols, indptr int64 ndarray, indices int32 ndarray)] for
+    J_1^T .. J_n^T (time order)."""
+    arr, keep = _csr_pattern_array(patterns)
     h = _vp()
-    _check(_lib.bppsa_csr_plan_create(arr, n, up_levels, down_levels, max_contributions, C.byref(h)),
+    _check(_lib.bppsa_csr_plan_create(arr, len(patterns), up_levels, down_levels, max_contributions, C.byref(h)),
            "bppsa_csr_plan_create")
     dims = [patterns[0][0]] + [p[1] for p in patterns]
-    return CsrPlan(h, n, dims)
+    return CsrPlan(h, len(patterns), dims)
+
+
+def csr_plan_create_symbolic(patterns, up_levels: int, down_levels: int) -> CsrPlan:
+    """bppsa_csr_plan_create_symbolic: the schedule's static analysis only
+    (info / steps; host-only, no device memory), for schedules whose
+    contribution lists do not fit."""
+    arr, keep = _csr_pattern_array(patterns)
+    h = _vp()
+    _check(_lib.bppsa_csr_plan_create_symbolic(arr, len(patterns), up_levels, down_levels, C.byref(h)),
+           "bppsa_csr_plan_create_symbolic")
+    dims = [patterns[0][0]] + [p[1] for p in patterns]
+    return CsrPlan(h, len(patterns), dims)
 
 
 def csr_scan(plan: CsrPlan, data, batched, seed, grads=None, ws=None, stream=None):

@@ -61,6 +61,7 @@ struct DevPat {
 
 struct bppsa_csr_plan {
   int n = 0, u = 0, dl = 0;
+  bool symbolic = false;      // bppsa_csr_plan_create_symbolic: steps / info only, no numeric plan
   std::vector<bppsa::HCSR> pats;
   std::vector<bppsa::DevPat> dpats;
   std::vector<bppsa::Buf> bufs;
@@ -184,6 +185,61 @@ bool plan_product(const HCSR& L, const HCSR& R, long long cap, HostProduct* P) {
   };
   par(fill);
   P->cptr[nnz] = ncon;
+  return true;
+}
+
+// Symbolic product L @ R without contribution lists (bppsa_csr_plan_create_
+// symbolic): pairs in closed form, sum_k nnz(L[:, k]) nnz(R[k, :]) (the
+// number of (left, right) entry pairs the numeric SpGEMM would touch), and the
+// output pattern by a bitset Gustavson product: every row of R as a bit row,
+// output row i = OR of the bit rows of R selected by L's row i (cost nnz(L) x
+// cols / 64 word ORs; multi-threaded over row ranges, thread-count independent).
+bool symbolic_product(const HCSR& L, const HCSR& R, HCSR* out, long long* pairs) {
+  std::vector<long long> colL(L.cols, 0);
+  for (int k : L.indices) ++colL[k];
+  long long pc = 0;
+  for (int k = 0; k < L.cols; ++k) pc += colL[k] * (R.indptr[k + 1] - R.indptr[k]);
+  *pairs = pc;
+  const int rows = L.rows, cols = R.cols, W = (cols + 63) / 64;
+  if ((double)R.rows * W * 8 > 16e9 || (double)rows * W * 8 > 16e9) return false;   // bit rows > 16 GB
+  std::vector<unsigned long long> rb((size_t)R.rows * W, 0ull), ob((size_t)rows * W, 0ull);
+  for (int k = 0; k < R.rows; ++k)
+    for (long long q = R.indptr[k]; q < R.indptr[k + 1]; ++q)
+      rb[(size_t)k * W + (R.indices[q] >> 6)] |= 1ull << (R.indices[q] & 63);
+  const int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<long long> row_nnz(rows, 0);
+  auto work = [&](int r0, int r1) {
+    for (int i = r0; i < r1; ++i) {
+      unsigned long long* o = &ob[(size_t)i * W];
+      for (long long p = L.indptr[i]; p < L.indptr[i + 1]; ++p) {
+        const unsigned long long* r = &rb[(size_t)L.indices[p] * W];
+        for (int w = 0; w < W; ++w) o[w] |= r[w];
+      }
+      long long nz = 0;
+      for (int w = 0; w < W; ++w) nz += __builtin_popcountll(o[w]);
+      row_nnz[i] = nz;
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    const int chunk = (rows + nth - 1) / nth;
+    for (int t = 0; t < nth; ++t) {
+      const int r0 = t * chunk, r1 = std::min(rows, r0 + chunk);
+      if (r0 < r1) th.emplace_back(work, r0, r1);
+    }
+    for (auto& x : th) x.join();
+  }
+  out->rows = rows;
+  out->cols = cols;
+  out->indptr.assign(rows + 1, 0);
+  for (int i = 0; i < rows; ++i) out->indptr[i + 1] = out->indptr[i] + row_nnz[i];
+  if (out->indptr[rows] >= (1ll << 31)) return false;
+  out->indices.resize(out->indptr[rows]);
+  for (int i = 0; i < rows; ++i) {
+    long long e = out->indptr[i];
+    for (int w = 0; w < W; ++w)
+      for (unsigned long long b = ob[(size_t)i * W + w]; b; b &= b - 1) out->indices[e++] = w * 64 + __builtin_ctzll(b);
+  }
   return true;
 }
 
@@ -406,8 +462,8 @@ using namespace bppsa;
 
 extern "C" {
 
-bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up_levels, int down_levels,
-                                   long long max_contributions, bppsa_csr_plan** out_plan) {
+static bppsa_status csr_plan_create_impl(const bppsa_csr_pattern* chain, int n, int up_levels, int down_levels,
+                                         long long max_contributions, bool symbolic, bppsa_csr_plan** out_plan) {
   if (!chain || !out_plan || n < 1 || n > 64) return fail(BPPSA_ERR_INVALID_ARGUMENT, "need 1 <= n <= 64 and non-NULL arguments");
   const int L = 64 - __builtin_clzll((unsigned long long)n);      // ceil(log2(n+1))
   const int u = up_levels, dl = down_levels;
@@ -415,6 +471,7 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
     return fail(BPPSA_ERR_INVALID_ARGUMENT, "need 0 <= up_levels <= L-1 and down_levels in {u, u+1}, <= L");
   const long long cap = max_contributions > 0 ? max_contributions : (1ll << 31);
   std::unique_ptr<bppsa_csr_plan> P(new bppsa_csr_plan());
+  P->symbolic = symbolic;
   P->n = n;
   P->u = u;
   P->dl = dl;
@@ -481,6 +538,31 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
       const int l = (int)(i + (1ll << d) - 1), r = (int)std::min<long long>(i + (1ll << (d + 1)) - 1, n);
       if (is_vec(slot[l])) {
         slot[r] = spmv(slot[r], slot[l]);
+      } else if (symbolic) {
+        const Buf& bl = P->bufs[slot[r]];   // left factor of the product a[r] a[l]
+        const Buf& br = P->bufs[slot[l]];
+        HCSR prod;
+        long long pairs = 0;
+        if (!symbolic_product(P->pats[bl.pat], P->pats[br.pat], &prod, &pairs))
+          return fail(BPPSA_ERR_NOT_SUPPORTED, "symbolic product at level " + std::to_string(d) +
+                                                   " exceeds the bit-row memory bound or 2^31 output entries");
+        P->contributions += pairs;
+        {
+          const HCSR& A = P->pats[bl.pat];
+          const HCSR& Bm = P->pats[br.pat];
+          P->steps.push_back(bppsa_csr_step{BPPSA_CSR_STEP_MM, phase, level, 0, 2 * pairs,
+                                            2ll * A.rows * A.cols * Bm.cols});
+        }
+        Buf pb;
+        pb.kind = B_PROD;
+        pb.size = prod.nnz();
+        pb.deps = bl.deps | br.deps;
+        P->pats.push_back(std::move(prod));
+        pb.pat = (int)P->pats.size() - 1;
+        P->bufs.push_back(pb);
+        const int out = (int)P->bufs.size() - 1;
+        P->ops.push_back(Op{OP_SPGEMM, out, slot[r], slot[l], -1});
+        slot[r] = out;
       } else {
         HostProduct hp;
         const Buf& bl = P->bufs[slot[r]];   // left factor of the product a[r] a[l]
@@ -579,6 +661,7 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
   // device copies of every pattern used by an SpMV
   P->dpats.resize(P->pats.size());
   for (const Op& op : P->ops) {
+    if (symbolic) break;
     if (op.kind != OP_SPMV) continue;
     const int pid = P->bufs[op.a].pat;
     if (P->dpats[pid].indptr) continue;
@@ -590,10 +673,21 @@ bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up
   return BPPSA_OK;
 }
 
+bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up_levels, int down_levels,
+                                   long long max_contributions, bppsa_csr_plan** out_plan) {
+  return csr_plan_create_impl(chain, n, up_levels, down_levels, max_contributions, false, out_plan);
+}
+
+bppsa_status bppsa_csr_plan_create_symbolic(const bppsa_csr_pattern* chain, int n, int up_levels, int down_levels,
+                                            bppsa_csr_plan** out_plan) {
+  return csr_plan_create_impl(chain, n, up_levels, down_levels, 0, true, out_plan);
+}
+
 void bppsa_csr_plan_destroy(bppsa_csr_plan* plan) { delete plan; }
 
 bppsa_status bppsa_csr_plan_workspace_size(const bppsa_csr_plan* plan, int B, const int* batched, size_t* bytes) {
   if (!plan || !bytes || B < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (plan->symbolic) return fail(BPPSA_ERR_NOT_SUPPORTED, "a symbolic plan has no numeric scan");
   std::vector<size_t> off;
   layout(*plan, B, batched, &off, bytes);
   return BPPSA_OK;
@@ -620,6 +714,7 @@ bppsa_status bppsa_csr_plan_steps(const bppsa_csr_plan* plan, bppsa_csr_step* st
 bppsa_status bppsa_csr_scan(const bppsa_csr_plan* plan, int B, const float* const* data, const int* batched,
                             const float* seed, float* const* grads, void* ws, size_t ws_bytes, void* stream) {
   if (!plan || !data || !seed || !grads || B < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (plan->symbolic) return fail(BPPSA_ERR_NOT_SUPPORTED, "a symbolic plan has no numeric scan");
   const bppsa_csr_plan& P = *plan;
   for (int k = 0; k < P.n; ++k)
     if (!data[k]) return fail(BPPSA_ERR_INVALID_ARGUMENT, "data[" + std::to_string(k) + "] is NULL");
