@@ -261,6 +261,21 @@ bppsa_status bppsa_exchange_ack(int rank, int world, unsigned* const* peer_acks,
                                 unsigned epoch, void* stream);
 bppsa_status bppsa_exchange_wait(const unsigned* flags, int rank, int world,
                                  unsigned epoch, void* stream);
+/* bppsa_scan_shard_up with the publish FUSED into the up-sweep's top level
+ * (SURVEY 8(e)): the CTAs of the last fold store the shard aggregate straight
+ * into mailbox[p][epoch & 1][rank] of every rank p and the last CTA to finish
+ * release-stores `epoch` into flags[p][rank] (the protocol, back-pressure
+ * wait on acks and argument meanings of bppsa_exchange_publish; n = B*H*H).
+ * `aggregate` [B][H*H] also receives the local copy.  A shard whose plan has
+ * one level (its level-0 kernel is the top) falls back to a separate publish
+ * launch.  Follow with bppsa_exchange_wait, bppsa_scan_shard_down on
+ * mailbox[epoch & 1] and bppsa_exchange_ack, exactly as after _publish.     */
+bppsa_status bppsa_scan_shard_up_publish(const bppsa_jac* jac, const float* seed,
+                                         float* aggregate, void* ws, size_t ws_bytes,
+                                         const bppsa_scan_opts* opts, int rank, int world,
+                                         float* const* peer_mailboxes,
+                                         unsigned* const* peer_flags, unsigned* counter,
+                                         const unsigned* acks, unsigned epoch, void* stream);
 
 
 /* ---------------------------------------------------------------------------

@@ -53,6 +53,8 @@ EXPORTS = {
     "bppsa_gru_gates": (_i, [_i, _i, _i, _i] + [_vp] * 12 + [_vp]),
     "bppsa_scan_affine": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_scan_shard_up": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
+    "bppsa_scan_shard_up_publish": (_i, [C.POINTER(_Jac), _vp, _vp, _vp, _sz, C.POINTER(_Opts), _i, _i, _vp, _vp,
+                                         _vp, _vp, C.c_uint, _vp]),
     "bppsa_scan_shard_down": (_i, [C.POINTER(_Jac), _vp, _vp, _i, _i, _vp, _vp, _vp, _sz, C.POINTER(_Opts), _vp]),
     "bppsa_weight_grads_workspace_size": (_i, [_i, _i, _i, _i, C.POINTER(_sz)]),
     "bppsa_weight_grads_rnn": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -350,6 +352,25 @@ def scan_shard_up(jac: Jacobians, seed: torch.Tensor | None, aggregate: torch.Te
     o = _opts("blocked", block0, block, trace, leaf_impl)
     _check(_lib.bppsa_scan_shard_up(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(aggregate, "aggregate"),
                                     ws.data_ptr(), ws.numel(), C.byref(o), _stream(stream)), "bppsa_scan_shard_up")
+    return aggregate
+
+
+def scan_shard_up_publish(jac: Jacobians, seed: torch.Tensor | None, aggregate: torch.Tensor, ws: torch.Tensor,
+                          rank: int, world: int, peer_mailboxes: torch.Tensor, peer_flags: torch.Tensor,
+                          counter: torch.Tensor, acks: torch.Tensor, epoch: int, block0: int = 0, block: int = 0,
+                          stream=None, trace: LaunchTrace | None = None, leaf_impl="auto"):
+    """bppsa_scan_shard_up_publish: the shard up-sweep with the peer-memory
+    publish fused into its top level (arguments of exchange_publish)."""
+    dev = aggregate.device
+    _req(seed, (jac.B, jac.H), "seed", dev)
+    if aggregate.numel() != jac.B * jac.H * jac.H:
+        raise ValueError(f"aggregate must hold B*H*H = {jac.B * jac.H * jac.H} floats")
+    _ws(ws, dev)
+    o = _opts("blocked", block0, block, trace, leaf_impl)
+    _check(_lib.bppsa_scan_shard_up_publish(C.byref(jac.desc), _ptr(seed, "seed"), _ptr(aggregate, "aggregate"),
+                                            ws.data_ptr(), ws.numel(), C.byref(o), rank, world,
+                                            peer_mailboxes.data_ptr(), peer_flags.data_ptr(), counter.data_ptr(),
+                                            acks.data_ptr(), epoch, _stream(stream)), "bppsa_scan_shard_up_publish")
     return aggregate
 
 

@@ -328,7 +328,9 @@ float* level_agg(const Plan& p, char* ws, int l) { return reinterpret_cast<float
 // replaces the storage of level L (used by shard_up to write the aggregate
 // straight into the caller's buffer).
 bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan& p, char* ws, float* top_out,
-                    cudaStream_t st, Tracer& tr, const float* e_aff = nullptr) {
+                    cudaStream_t st, Tracer& tr, const float* e_aff = nullptr, const Publish* pub = nullptr,
+                    bool* published = nullptr) {
+  if (published) *published = false;
   const int H = j.H, B = j.B;
   const Seg seg{j.T, j.B, j.H, head};
   for (int l = 0; l < p.L; ++l) {
@@ -358,7 +360,9 @@ bppsa_status run_up(const bppsa_jac& j, int head, const float* seed, const Plan&
     } else {
       const MatAcc A = (l == 0) ? dense_acc(j, head, reinterpret_cast<float*>(ws + p.dense_off), seed)
                                 : level_acc(p, ws, l, H);
-      e = launch_fold_up(A, H, B, p.n[l], p.C[l], head, dst, p.n[l + 1], st);
+      const bool top = l + 1 == p.L && pub;       // the carry exchange fused into the top level
+      e = launch_fold_up(A, H, B, p.n[l], p.C[l], head, dst, p.n[l + 1], st, top ? pub : nullptr);
+      if (top && published) *published = true;
     }
     tr.end(st);
     if (e != cudaSuccess) return cuda_status(e, "up-sweep launch");
@@ -685,6 +689,58 @@ bppsa_status bppsa_scan_shard_up(const bppsa_jac* jac, const float* seed, float*
   if (p.L == 0) return fail(BPPSA_ERR_INVALID_ARGUMENT, "internal: empty shard plan");
   // the top level (one aggregate per sample) goes straight into `aggregate`
   s = run_up(*jac, head, seed, p, w, aggregate, st, tr);
+  report_launches(opts, tr);
+  return s;
+}
+
+bppsa_status bppsa_scan_shard_up_publish(const bppsa_jac* jac, const float* seed, float* aggregate, void* ws,
+                                         size_t ws_bytes, const bppsa_scan_opts* opts, int rank, int world,
+                                         float* const* peer_mailboxes, unsigned* const* peer_flags,
+                                         unsigned* counter, const unsigned* acks, unsigned epoch, void* stream) {
+  bppsa_status s = check_jac(jac);
+  if (s != BPPSA_OK) return s;
+  REQUIRE_DEV(aggregate, "aggregate");
+  if (world < 1 || rank < 0 || rank >= world || epoch == 0)
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "need 0 <= rank < world, epoch >= 1");
+  if ((seed != nullptr) != (rank == world - 1))
+    return fail(BPPSA_ERR_INVALID_ARGUMENT, "exactly the last rank (holding t = T-1) passes the seed");
+  if (seed) REQUIRE_DEV(seed, "seed");
+  REQUIRE_DEV(peer_mailboxes, "peer_mailboxes");
+  REQUIRE_DEV(peer_flags, "peer_flags");
+  REQUIRE_DEV(counter, "counter");
+  REQUIRE_DEV(acks, "acks");
+  if (opts && opts->mode != BPPSA_SCAN_BLOCKED) return fail(BPPSA_ERR_NOT_SUPPORTED, "shards use the BLOCKED mode");
+  const int head = seed ? 1 : 0;
+  Plan p;
+  s = make_plan(*jac, head, opts, true, &p);
+  if (s != BPPSA_OK) return s;
+  demote_unaligned(*jac, &p, seed, nullptr, nullptr);
+  s = check_ws(p, ws, ws_bytes);
+  if (s != BPPSA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  Tracer tr = tracer_from(opts);
+  s = prepare_dense(*jac, p, w, st, tr);
+  if (s != BPPSA_OK) return s;
+  if (p.L == 0) return fail(BPPSA_ERR_INVALID_ARGUMENT, "internal: empty shard plan");
+  Publish pub;
+  pub.peers = peer_mailboxes;
+  pub.flags = peer_flags;
+  pub.counter = counter;
+  pub.acks = acks;
+  pub.epoch = epoch;
+  pub.rank = rank;
+  pub.world = world;
+  pub.n = (long long)jac->B * jac->H * jac->H;
+  bool fused = false;
+  s = run_up(*jac, head, seed, p, w, aggregate, st, tr, nullptr, &pub, &fused);
+  if (s == BPPSA_OK && !fused) {                  // one-level shard: its level-0 kernel wrote the aggregate
+    tr.begin(st);
+    cudaError_t e = launch_exchange_publish(aggregate, pub.n, rank, world, peer_mailboxes, peer_flags, counter,
+                                            acks, epoch, num_sms(), st);
+    tr.end(st);
+    if (e != cudaSuccess) s = cuda_status(e, "exchange publish");
+  }
   report_launches(opts, tr);
   return s;
 }

@@ -121,9 +121,23 @@ cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry,
                              float* vec_out = nullptr, float* head_out = nullptr,
                              long long head_bstride = 0);
 
+// The carry exchange fused into the up-sweep's top level (SURVEY 8(e) "fused
+// variant"): the fold's CTAs store the shard aggregate straight into every
+// rank's mailbox slot [epoch & 1][rank] and the last CTA to finish raises the
+// epoch flag in every rank (same protocol and back-pressure as exchange.cu).
+struct Publish {
+  float* const* peers = nullptr;      // [world] mailboxes [2][world][n]
+  unsigned* const* flags = nullptr;   // [world] flag arrays [world]
+  unsigned* counter = nullptr;        // this rank's CTA counter (0 between epochs)
+  const unsigned* acks = nullptr;     // this rank's ack words [world]
+  unsigned epoch = 0;
+  int rank = 0, world = 1;
+  long long n = 0;                    // floats per rank slot (B * H * H)
+};
+
 // explicit level fold / walk
 cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, int head,
-                           float* agg_out, long long n_out, cudaStream_t st);
+                           float* agg_out, long long n_out, cudaStream_t st, const Publish* pub = nullptr);
 // out_mode 0: out[b][s][H] (carry array with n slots); 1: grad_h via seg time map
 // addv / vec_out / head_out: the affine terms as for launch_leaf_down
 cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, int head,

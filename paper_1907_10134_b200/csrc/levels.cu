@@ -51,10 +51,16 @@ __device__ __forceinline__ void gemm_step(const float* __restrict__ As, const fl
     for (int y = 0; y < TN; ++y) Pn[(ti * TM + x) * HP + tj * TN + y] = acc[x][y];
 }
 
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int HP, int TM, int TN>
 __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A, int H, long long n, int C,
                                                                        int head, float* __restrict__ agg_out,
-                                                                       long long n_out) {
+                                                                       long long n_out, Publish pub) {
   using Tl = Tile<HP, TM, TN>;
   extern __shared__ __align__(16) float smem[];
   // one A buffer (the next A_s waits in registers) and two P buffers: 48 KB
@@ -68,6 +74,9 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
   const bool vec = head && q == 0;
   const int HH = H * H;
   for (int e = tid; e < 3 * HP * HP; e += Tl::NT) smem[e] = 0.f;
+  if (pub.peers && pub.epoch > 2 && tid == 0)       // the readers are done with slot (epoch - 2) & 1
+    for (int r = 0; r < pub.rank; ++r)
+      while ((int)(ld_acquire_sys_u32(pub.acks + r) - (pub.epoch - 2)) < 0) __nanosleep(256);
   __syncthreads();
   long long s;
   if (vec) {
@@ -139,13 +148,34 @@ __global__ void __launch_bounds__(Tile<HP, TM, TN>::NT) fold_up_kernel(MatAcc A,
     }
   }
   __syncthreads();
-  float* dst = agg_out + ((long long)b * n_out + q) * HH;
+  const long long off = ((long long)b * n_out + q) * HH;
+  float* dst = agg_out + off;
   if (vec) {
     for (int i = tid; i < H; i += Tl::NT) dst[i] = Pb[pc][i * HP];
   } else {
     for (int e = tid; e < HH; e += Tl::NT) {   // (i, j) -> j*H + i
       const int j = e / H, i = e % H;
       dst[e] = Pb[pc][i * HP + j];
+    }
+  }
+  if (pub.peers) {                             // fused publish: P2P stores into every rank's mailbox
+    const long long slot = ((long long)(pub.epoch & 1u) * pub.world + pub.rank) * pub.n + off;
+    const int cnt = vec ? H : HH;
+    for (int e = tid; e < cnt; e += Tl::NT) {
+      const float v = vec ? Pb[pc][e * HP] : Pb[pc][(e % H) * HP + e / H];
+      for (int p = 0; p < pub.world; ++p) pub.peers[p][slot + e] = v;
+    }
+    __threadfence_system();                    // this CTA's stores, before the count
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned total = gridDim.x * gridDim.y;
+      if (atomicAdd(pub.counter, 1u) == total - 1) {   // the last CTA: every store is performed
+        __threadfence_system();
+        for (int p = 0; p < pub.world; ++p)
+          asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(pub.flags[p] + pub.rank), "r"(pub.epoch)
+                       : "memory");
+        *pub.counter = 0u;
+      }
     }
   }
 }
@@ -292,7 +322,7 @@ constexpr int kWarps = 4;
 
 template <int HP, int TM, int TN>
 cudaError_t fold_impl(const MatAcc& A, int H, int B, long long n, int C, int head, float* agg_out,
-                      long long n_out, cudaStream_t st) {
+                      long long n_out, cudaStream_t st, const Publish* pub) {
   using Tl = Tile<HP, TM, TN>;
   const size_t smem = 3ull * HP * HP * sizeof(float);
   auto k = fold_up_kernel<HP, TM, TN>;
@@ -301,7 +331,7 @@ cudaError_t fold_impl(const MatAcc& A, int H, int B, long long n, int C, int hea
     if (e != cudaSuccess) return e;
   }
   dim3 grid((unsigned)n_out, (unsigned)B);
-  k<<<grid, Tl::NT, smem, st>>>(A, H, n, C, head, agg_out, n_out);
+  k<<<grid, Tl::NT, smem, st>>>(A, H, n, C, head, agg_out, n_out, pub ? *pub : Publish{});
   return cudaGetLastError();
 }
 
@@ -591,14 +621,14 @@ __global__ void carry_combine_kernel(const float* __restrict__ gathered, int ran
 }  // namespace
 
 cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, int head, float* agg_out,
-                           long long n_out, cudaStream_t st) {
-  if (H == 20) return fold_impl<20, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st);
-  if (H <= 32) return fold_impl<32, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st);
+                           long long n_out, cudaStream_t st, const Publish* pub) {
+  if (H == 20) return fold_impl<20, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st, pub);
+  if (H <= 32) return fold_impl<32, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st, pub);
   // many blocks (level 1 at C4: 1040 CTAs): 8 x 8 register tiles, 64 threads
   // per GEMM, half the shared-memory reads per FMA (the 4 x 4 form was
   // LSU / MIO-throttled); few blocks: 4 x 4, 256 threads, shorter chains
-  if ((long long)n_out * B >= 4LL * 148) return fold_impl<64, 8, 8>(A, H, B, n, C, head, agg_out, n_out, st);
-  return fold_impl<64, 4, 4>(A, H, B, n, C, head, agg_out, n_out, st);
+  if ((long long)n_out * B >= 4LL * 148) return fold_impl<64, 8, 8>(A, H, B, n, C, head, agg_out, n_out, st, pub);
+  return fold_impl<64, 4, 4>(A, H, B, n, C, head, agg_out, n_out, st, pub);
 }
 
 cudaError_t launch_walk_down(const MatAcc& A, int H, int B, long long n, int C, int head,

@@ -7,7 +7,9 @@ t = T-1 and the seed (the "head" shard, first in scan order).  Protocol:
        rank < G-1:  M_r = J_lo^T ... J_{hi-1}^T   [B, H*H] column-major
        rank = G-1:  V   = grad_h[lo-1]            [B, H] in the first H floats
   2. all-gather of the aggregates over NCCL (torch.distributed; NVLink on the
-     8xB200 box) — the only data-path collective
+     8xB200 box) — the only data-path collective; or, with a PeerExchange,
+     P2P stores into every rank's mailbox from the up-sweep's own top-level
+     kernel (bppsa_scan_shard_up_publish) and a flag wait — no NCCL
   3. carry for rank r: M_{r+1} ... M_{G-2} V and the local down-sweep on the
      device                                                     (bppsa_scan_shard_down)
   4. (caller) all-reduce of the weight gradients.
@@ -47,6 +49,15 @@ class CudaShardBackend:
         B, H = self.jac.B, self.jac.H
         agg = torch.empty((B, H * H), dtype=torch.float32, device="cuda")
         self.api.scan_shard_up(self.jac, seed, agg, self.ws, self.block0, self.block)
+        return agg
+
+    def up_publish(self, seed, ex: "PeerExchange"):
+        """The up-sweep with the peer-memory publish fused into its top level
+        (bppsa_scan_shard_up_publish) for epoch ex.epoch."""
+        B, H = self.jac.B, self.jac.H
+        agg = torch.empty((B, H * H), dtype=torch.float32, device="cuda")
+        self.api.scan_shard_up_publish(self.jac, seed, agg, self.ws, ex.rank, ex.world, ex.mail_ptrs, ex.flag_ptrs,
+                                       ex.counter, ex.acks, ex.epoch, self.block0, self.block)
         return agg
 
     def down(self, seed, gathered, rank, world, grad_h=None, want_init=False):
@@ -100,6 +111,15 @@ class PeerExchange:
         self.epoch = 0
         dist.barrier(group=group)
 
+    def up_and_exchange(self, backend, seed) -> torch.Tensor:
+        """The fused form: the backend's up-sweep publishes into the mailboxes
+        from its own top-level kernel (no separate publish launch), then the
+        wait; returns the gathered view like `exchange`."""
+        self.epoch += 1
+        backend.up_publish(seed, self)
+        self.api.exchange_wait(self.flags, self.rank, self.world, self.epoch)
+        return self.mail[self.epoch & 1]
+
     def exchange(self, agg: torch.Tensor) -> torch.Tensor:
         """Publish this rank's aggregate, wait for the later ranks'; returns the
         gathered [world, B, H*H] view (valid for kernels after this call)."""
@@ -114,7 +134,7 @@ class PeerExchange:
         self.api.exchange_ack(self.rank, self.world, self.ack_ptrs, self.epoch)
 
 
-def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None, exchange=None):
+def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None, exchange=None, fused: bool = True):
     """Run the 3-step protocol on this rank.  `seed` must be given on the last
     rank only (it holds t = T-1).  Returns (local grad_h, J_lo^T grad_h[lo])."""
     rank = dist.get_rank(group)
@@ -122,15 +142,19 @@ def sharded_scan(backend, seed, group=None, want_init: bool = False, grad_h=None
     head = rank == world - 1
     if head != (seed is not None):
         raise ValueError("exactly the last rank passes the seed")
-    agg = backend.up(seed)
-    if world > 1 and exchange is not None:               # peer-memory exchange (no NCCL)
+    if world > 1 and exchange is not None and fused and hasattr(backend, "up_publish"):
+        # peer-memory exchange fused into the up-sweep's top level (no NCCL, no publish launch)
+        gathered = exchange.up_and_exchange(backend, seed).view(world, backend.jac.B, backend.jac.H ** 2)
+    elif world > 1 and exchange is not None:             # peer-memory exchange (no NCCL)
+        agg = backend.up(seed)
         gathered = exchange.exchange(agg).view((world,) + tuple(agg.shape))
     elif world > 1:
+        agg = backend.up(seed)
         flat = torch.empty((world * agg.shape[0],) + tuple(agg.shape[1:]), dtype=agg.dtype, device=agg.device)
         dist.all_gather_into_tensor(flat, agg.contiguous(), group=group)    # concat form (NCCL and gloo)
         gathered = flat.view((world,) + tuple(agg.shape))
     else:
-        gathered = agg.unsqueeze(0)
+        gathered = backend.up(seed).unsqueeze(0)
     out = backend.down(seed, None if head else gathered, rank, world, grad_h=grad_h, want_init=want_init)
     if world > 1 and exchange is not None:
         exchange.release()

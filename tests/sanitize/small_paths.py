@@ -2,7 +2,7 @@
 (tests/test_gpu_sanitizer.py): the exact-integer fold and walk, the 3xFP16 /
 3xTF32 folds and the TMA walk, the CUDA-core leaves and levels, the tcgen05
 weight gradients, the GRU path, the affine scan, the CSR SpGEMM scan and the
-peer-exchange kernels (one rank).  Exits non-zero on a wrong result."""
+peer-exchange kernels and the publish fused into the shard up-sweep (one rank).  Exits non-zero on a wrong result."""
 import os
 import sys
 
@@ -66,14 +66,26 @@ def main():
         api.exchange_wait(flags, 0, 1, ep)
         api.exchange_ack(0, 1, ap, ep)
     torch.cuda.synchronize()
+    if not torch.equal(mail[1, 0], agg):
+        sys.exit(3)
+    # the publish fused into the shard up-sweep's top level (epochs 4, 5)
+    ws = api.workspace(api.scan_workspace_size(jac, "blocked", 64, 8))
+    ref_agg = torch.empty(n, device="cuda")
+    api.scan_shard_up(jac, cu(w.g), ref_agg, ws, 64, 8)
+    agg2 = torch.empty(n, device="cuda")
+    for ep in (4, 5):
+        api.scan_shard_up_publish(jac, cu(w.g), agg2, ws, 0, 1, mp, fp, counter, acks, ep, 64, 8)
+        api.exchange_wait(flags, 0, 1, ep)
+        api.exchange_ack(0, 1, ap, ep)
+    torch.cuda.synchronize()
+    if not torch.equal(mail[1, 0, :H * 1], ref_agg[:H]) or not torch.equal(agg2[:H], ref_agg[:H]):
+        sys.exit(4)
     ref = outs["ffma"].cpu().numpy()
     for impl in ("int8", "tensor", "tensor_tf32"):
         err = float(np.abs(outs[impl].cpu().numpy() - ref).max() / np.abs(ref).max())
         if not err < 1e-4:
             print(f"{impl}: rel err {err:.2e}")
             sys.exit(2)
-    if not torch.equal(mail[1, 0], agg):
-        sys.exit(3)
     print("small paths ok")
 
 

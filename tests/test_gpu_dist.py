@@ -21,7 +21,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, T, B, H, q, peer=False):
+def _worker(rank, world, port, T, B, H, q, peer=False, norm=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -30,6 +30,10 @@ def _worker(rank, world, port, T, B, H, q, peer=False):
         from paper_1907_10134_b200 import api
         from paper_1907_10134_b200.dist import CudaShardBackend, PeerExchange, shard_bounds, sharded_scan
         w = W.rnn_workload(T, B, H, seed=21)
+        if norm:       # norm-preserving: every shard's carry matters (realistic gradients vanish in ~35 steps)
+            f = W.norm_preserving_rnn(T, B, H, seed=22)
+            w.h, w.g = f["h"], f["g"]
+            w.params["W_hh"] = f["W_hh"]
         lo, hi = shard_bounds(T, world)[rank]
         h = torch.from_numpy(w.h[lo:hi]).cuda()
         x = torch.from_numpy(w.x[lo:hi]).cuda()
@@ -38,7 +42,7 @@ def _worker(rank, world, port, T, B, H, q, peer=False):
         seed = torch.from_numpy(w.g).cuda() if rank == world - 1 else None
         ex = PeerExchange(B, H) if peer else None
         for _ in range(3 if peer else 1):       # several epochs through the double-buffered mailboxes
-            grad, init = sharded_scan(be, seed, want_init=(rank == 0), exchange=ex)
+            grad, init = sharded_scan(be, seed, want_init=(rank == 0), exchange=ex, fused=(peer != "publish"))
             dist.barrier()
         h_init = torch.from_numpy(w.h[lo - 1]).cuda() if lo > 0 else None
         dWih, dWhh, db = api.weight_grads_rnn(x, h, grad, h_init=h_init)
@@ -59,18 +63,27 @@ def _worker(rank, world, port, T, B, H, q, peer=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,peer", [(2, False), (3, False), (2, True), (3, True)])
-def test_sharded_cuda_path_one_gpu(world, peer):
-    """peer=True: the aggregates travel through bppsa_exchange_publish / _wait
-    (CUDA IPC mailboxes, here on one device) instead of the all-gather."""
+@pytest.mark.parametrize("world,peer,norm", [(2, False, False), (3, False, False), (2, "fused", False),
+                                             (3, "fused", False), (3, "publish", False), (2, False, True),
+                                             (3, "fused", True), (3, "publish", True)])
+def test_sharded_cuda_path_one_gpu(world, peer, norm):
+    """peer: the aggregates travel through the CUDA IPC mailboxes (here on one
+    device) instead of the all-gather — "fused": published by the up-sweep's
+    own top-level kernel (bppsa_scan_shard_up_publish), "publish": a separate
+    bppsa_exchange_publish launch.  norm: the norm-preserving family, where
+    every shard's carry reaches the earlier shards."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 30000, 16, 64, q, peer)) for r in range(world)]
+    T, B = (6000, 4) if norm else (30000, 16)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, B, 64, q, peer, norm)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(300)
         assert p.exitcode == 0
     e_grad, e_init, e_w = q.get(timeout=5)
-    assert e_grad <= 1e-4 and e_init <= 1e-4 and e_w <= 1e-4, (e_grad, e_init, e_w)
+    # weight gradients (sums over all T*B rows) are gated on the realistic
+    # family: on the norm-preserving one the grad_h errors are correlated along
+    # time and their sums cancel far less than the terms (fp32 BP alike)
+    assert e_grad <= 1e-4 and e_init <= 1e-4 and (norm or e_w <= 1e-4), (e_grad, e_init, e_w)
