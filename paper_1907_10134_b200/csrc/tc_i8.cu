@@ -232,6 +232,22 @@ __device__ __forceinline__ void regions_to_c(uint32_t t0, float2 (&c)[4]) {
                       make_float2(__int2float_rn(S0), __int2float_rn(S1)));
   }
 }
+// c' for 16 columns from the four regions (one x16 load per region)
+__device__ __forceinline__ void regions_to_c16(uint32_t t0, float2 (&c)[8]) {
+  uint32_t r0[16], r1[16], r2[16], r3[16];
+  tmem_ld16(t0, r0);
+  tmem_ld16(t0 + 64, r1);
+  tmem_ld16(t0 + 128, r2);
+  tmem_ld16(t0 + 192, r3);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int S0 = (int)r0[2 * i] * 256 + (int)r1[2 * i], S1 = (int)r0[2 * i + 1] * 256 + (int)r1[2 * i + 1];
+    const int T0 = (int)r2[2 * i] * 256 + (int)r3[2 * i], T1 = (int)r2[2 * i + 1] * 256 + (int)r3[2 * i + 1];
+    c[i] = __ffma2_rn(make_float2(__int2float_rn(T0), __int2float_rn(T1)), make_float2(0x1p-16f, 0x1p-16f),
+                      make_float2(__int2float_rn(S0), __int2float_rn(S1)));
+  }
+}
 // Four regions x 8 columns (t0 + 64 r + [0, 8)) into r[8 r + i], asynchronously:
 // the registers are written when tcgen05.wait::ld retires, so every wait is
 // followed by ld_retired(), an empty asm that "modifies" the registers the
@@ -578,6 +594,10 @@ constexpr int R_NT = R_NT_DEF;                      // tile groups
 #define R_PIPE_DEF 1
 #endif
 constexpr bool R_PIPE = R_PIPE_DEF;
+#ifndef R_X16_DEF
+#define R_X16_DEF 0
+#endif
+constexpr bool R_X16 = R_X16_DEF;
 constexpr int R_WPS = 4, R_EPI = 32 * R_WPS;        // warps per group
 constexpr int R_THREADS = R_NT * R_EPI;
 #ifndef R_HCH_DEF
@@ -773,7 +793,21 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
           }
         } else {
           const uint32_t td = wait_d();
-          if (R_PIPE) {                             // TMEM loads one 8-column chunk ahead (64 registers)
+          if (R_X16) {                              // x16 loads, one 16-column chunk at a time (64 registers)
+#pragma unroll
+            for (int c16 = 0; c16 < 4; ++c16) {
+              float2 c[8];
+              regions_to_c16(td + 16 * c16, c);
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const float4 da = lds128(dp + 64u * c16 + 32u * h2), db = lds128(dp + 64u * c16 + 32u * h2 + 16u);
+                y[8 * c16 + 4 * h2] = __fmul2_rn(c[4 * h2], make_float2(da.x, da.y));
+                y[8 * c16 + 4 * h2 + 1] = __fmul2_rn(c[4 * h2 + 1], make_float2(da.z, da.w));
+                y[8 * c16 + 4 * h2 + 2] = __fmul2_rn(c[4 * h2 + 2], make_float2(db.x, db.y));
+                y[8 * c16 + 4 * h2 + 3] = __fmul2_rn(c[4 * h2 + 3], make_float2(db.z, db.w));
+              }
+            }
+          } else if (R_PIPE) {                      // TMEM loads one 8-column chunk ahead (64 registers)
             uint32_t ra[32], rb[32];
             ld_regions8(td, ra);
 #pragma unroll
