@@ -595,7 +595,7 @@ constexpr int R_NT = R_NT_DEF;                      // tile groups
 #endif
 constexpr bool R_PIPE = R_PIPE_DEF;
 #ifndef R_X16_DEF
-#define R_X16_DEF 0
+#define R_X16_DEF 1
 #endif
 constexpr bool R_X16 = R_X16_DEF;
 constexpr int R_WPS = 4, R_EPI = 32 * R_WPS;        // warps per group
