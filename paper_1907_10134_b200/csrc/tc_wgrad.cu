@@ -11,10 +11,12 @@
 //                    and h_prev is one contiguous 8 KB run each; NS stages
 //                    ahead, mbarrier complete_tx);
 //   warp 9, lane 0   issues the MMAs (NBUF operand buffers in flight);
-//   warps 0..7       converters: warp w owns TMEM lanes 32*(w&3).. (= A rows)
-//                    and K columns [16*(w>>2), +16) of the chunk.  Each thread
-//                    forms delta and the hi/lo splits for its 16 rows, stores
-//                    A with tcgen05.st and its B row into the SW128 tile.
+//   warps 0..7       converters: thread = (column i, 8-row group) of the
+//                    chunk; it forms delta ONCE and stores both A rows (delta
+//                    hi / lo) and both B rows (h_prev hi / lo) into K-major
+//                    SW128 tiles in shared memory (SS MMAs).  r02: A moved out
+//                    of TMEM — there its hi and lo rows sat in different lane
+//                    quadrants, so two threads formed each delta (2.2 ms).
 // Synchronisation is mbarrier-only: full/empty per stage, a_full/freeb per
 // A/B buffer.  The accumulator is flushed into fp32 registers every FLUSH
 // chunks so the tensor core's truncating accumulation never spans more than
@@ -34,19 +36,26 @@ constexpr int H = 64, KC = 32, MROWS = 128, NCONV = 256, NTH = NCONV + 64;   // 
 constexpr int FLUSH = 32;                           // chunks per accumulation window
 constexpr long long PART_ROWS = 16384;              // rows per part (512 chunks)
 constexpr int MAXI = 4;
-constexpr int NS = 4;                               // staging depth (chunks, power of 2)
-constexpr int NBUF = 4;                             // A (TMEM) / B (SMEM) operand buffers
+#ifndef WG_NS
+#define WG_NS 4
+#endif
+#ifndef WG_NBUF
+#define WG_NBUF 3
+#endif
+constexpr int NS = WG_NS;                           // staging depth (chunks)
+constexpr int NBUF = WG_NBUF;                       // A / B operand buffer pairs (shared memory)
 constexpr int ROW_BYTES = H * 4;
 constexpr int SB = 3 * KC * ROW_BYTES;              // h, g, h_prev rows: 24 KB per stage
 constexpr int XB = KC * MAXI * 4;                   // x rows: 512 B per stage
-constexpr int B_BYTES = MROWS * KC * 4;             // 16 KB per B buffer
+constexpr int B_BYTES = MROWS * KC * 4;             // 16 KB per operand tile (A or B)
 constexpr int OFF_STAGE = 0;
-constexpr int OFF_BT = NS * SB;                     // 1024-B aligned (SW128 tiles)
-constexpr int OFF_X = OFF_BT + NBUF * B_BYTES;
+constexpr int OFF_BT = NS * SB;                     // 1024-B aligned (SW128 tiles): [buf][A | B]
+constexpr int OFF_X = OFF_BT + NBUF * 2 * B_BYTES;
 constexpr int OFF_BAR = OFF_X + NS * XB;
 constexpr int SMEM = OFF_BAR + (2 * NS + 2 * NBUF + 2) * 8 + 1024;
 static_assert(OFF_BT % 1024 == 0, "SW128 B tiles must be 1024-B aligned");
-constexpr uint32_t TMEM_COLS = 256;                 // D at [0,128), A buffer b at [128+32b, +32)
+static_assert(SMEM <= 232448, "tc_wgrad shared memory");
+constexpr uint32_t TMEM_COLS = 128;                 // D at [0, 128)
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) |
                            ((uint32_t)(MROWS >> 4) << 24);
 
@@ -99,14 +108,6 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
-          taddr),
-      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
-      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
-      : "memory");
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   asm volatile(
@@ -162,54 +163,51 @@ struct Bars {
   __device__ uint32_t freeb(int b) const { return b0 + 8u * (2 * NS + NBUF + b); }
 };
 
-// One chunk's rows for this thread: A values (delta hi or lo) and B values
-// (h_prev hi or lo) of rows 16*grp .. 16*grp+15 (base = stage + column i +
-// 16*grp rows); rows >= n are zero, h_prev rows < nlow (before h_0 with no
-// h_init) are zero.  IX = number of input columns (hi threads only).
-template <bool LO, int IX, bool FULL, bool SPLIT>
-__device__ __forceinline__ void convert_rows(uint32_t base, uint32_t xbase, int n, int nlow, float (&av)[16],
-                                             float (&bh)[8], float (&bl)[8], float& dbias, float (&dih)[MAXI],
-                                             uint32_t hp_lo, uint32_t hp_hi, int nsplit) {
-  // A: delta hi (or lo) of all 16 rows (TMEM lanes are per warp quadrant, so
-  // the hi and lo rows of a column belong to different threads and each forms
-  // delta); B: h_prev hi AND lo of 8 of the 16 rows (B is in shared memory,
-  // any thread may write both rows) — the hi thread rows 0..7, the lo thread
-  // rows 8..15, so h_prev is loaded and split once
-  constexpr int R0 = LO ? 8 : 0;
+// One chunk's 8 rows of this thread's column i (rows 8 kg .. 8 kg + 7 of the
+// chunk; base = stage + column i + those rows): delta = (1 - h^2) g once, its
+// tf32 hi / lo (A rows i and 64 + i), h_prev hi / lo (B rows i and 64 + i),
+// and the dbias / dW_ih partials.  Rows >= n are zero, h_prev rows < nlow
+// (before h_0 with no h_init) are zero.  SPLIT: h_prev rows < nsplit come
+// from hp_lo (the previous chunk), the rest from hp_hi.
+template <int IX, bool FULL, bool SPLIT>
+__device__ __forceinline__ void convert8(uint32_t base, uint32_t xbase, int n, int nlow, float (&ah)[8],
+                                         float (&al)[8], float (&bh)[8], float (&bl)[8], float& dbias,
+                                         float (&dih)[MAXI], uint32_t hp_lo, uint32_t hp_hi, int nsplit) {
 #pragma unroll
-  for (int rr = 0; rr < 16; ++rr) {
+  for (int rr = 0; rr < 8; ++rr) {
     const float hv = lds(base + rr * ROW_BYTES), gv = lds(base + (KC + rr) * ROW_BYTES);
     float d = (1.f - hv * hv) * gv;
     if (!FULL) d = rr < n ? d : 0.f;
-    const float dhi = tf32_hi(d);
-    av[rr] = LO ? d - dhi : dhi;
-    if (rr >= R0 && rr < R0 + 8) {
-      // h_prev row rr: rows < nsplit from hp_lo, the rest from hp_hi (see
-      // converters); !SPLIT: every row from hp_lo
-      float hp = lds(!SPLIT ? hp_lo + rr * ROW_BYTES
-                            : (rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES));
-      if (!FULL) hp = (rr < n && rr >= nlow) ? hp : 0.f;
-      const float phi = tf32_hi(hp);
-      bh[rr - R0] = phi;
-      bl[rr - R0] = hp - phi;
-    }
-    if (!LO) {
-      dbias += d;
+    ah[rr] = tf32_hi(d);
+    al[rr] = d - ah[rr];
+    float hp = lds(!SPLIT ? hp_lo + rr * ROW_BYTES
+                          : (rr < nsplit ? hp_lo + rr * ROW_BYTES : hp_hi + (rr - nsplit) * ROW_BYTES));
+    if (!FULL) hp = (rr < n && rr >= nlow) ? hp : 0.f;
+    bh[rr] = tf32_hi(hp);
+    bl[rr] = hp - bh[rr];
+    dbias += d;
 #pragma unroll
-      for (int j = 0; j < IX; ++j) {
-        float xv = lds(xbase + 4 * (rr * IX + j));
-        if (!FULL) xv = rr < n ? xv : 0.f;
-        dih[j] = fmaf(d, xv, dih[j]);
-      }
+    for (int j = 0; j < IX; ++j) {
+      float xv = lds(xbase + 4 * (rr * IX + j));
+      if (!FULL) xv = rr < n ? xv : 0.f;
+      dih[j] = fmaf(d, xv, dih[j]);
     }
   }
 }
 
-template <bool LO, int IX>
+// Converter thread (column i = 32 (warp & 1) + lane, row group kg = warp >> 1
+// of each 32-row chunk) forms delta ONCE and writes both its A rows (delta hi
+// / lo, K-major SW128 tile in shared memory) and both B rows (h_prev hi / lo).
+// The flush mapping is the accumulator's: warp w reads TMEM lanes 32 (w & 3)
+// (D rows), columns 64 (w >> 2) (D column half); for every warp that is row
+// i of slab (w & 2) + (w >> 2), and the slab also receives the warp's
+// dbias / dW_ih partials of column i over its row group (4 partials per part
+// and column, summed by wgrad_reduce_rnn with the slabs).
+template <int IX>
 __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br, uint32_t tmem, int warp,
                                            int lane) {
-  const int wq = warp & 3, grp = warp >> 2;
-  const int m = 32 * wq + lane, i = m & 63;
+  const int wq = warp & 3, grp = warp >> 2;          // flush: D lanes 32 wq.., D columns 64 grp..
+  const int kg = warp >> 1, i = 32 * (warp & 1) + lane;   // convert: rows 8 kg.., column i
   const uint32_t tl = tmem + ((uint32_t)(32 * wq) << 16);
   const int NB = H + IX + 1;
   const bool reuse = w.B <= KC;
@@ -236,35 +234,36 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
     const int lowB = w.h_init ? 0 : (int)max(0ll, min((long long)rows_here, (long long)w.B - r0));
     for (int c = 0; c < nch; ++c, ++cg) {
       const uint32_t b = cg % NBUF, s = cg % NS;
-      const int n = min(KC, rows_here - c * KC) - 16 * grp;        // valid rows of my half
-      const int nlow = lowB - c * KC - 16 * grp;                     // h_prev rows before h_0
+      const int n = min(KC, rows_here - c * KC) - 8 * kg;         // valid rows of my 8
+      const int nlow = lowB - c * KC - 8 * kg;                      // h_prev rows before h_0
       mbar_wait(br.full(s), (cg / NS) & 1);
-      const uint32_t base = s0 + OFF_STAGE + s * SB + 4u * i + 16u * grp * ROW_BYTES;
-      const uint32_t xbase = s0 + OFF_X + s * XB + 4u * 16 * grp * IX;
+      const uint32_t base = s0 + OFF_STAGE + s * SB + 4u * i + 8u * kg * ROW_BYTES;
+      const uint32_t xbase = s0 + OFF_X + s * XB + 4u * 8 * kg * IX;
       // h_prev = h shifted back by B rows: with B <= KC every chunk but a part's
       // first reads it from its own h rows and the previous chunk's (still
       // staged: a stage is released one chunk late), no third copy
       uint32_t hp_lo, hp_hi;
       int nsplit;
       if (reuse && c > 0) {
-        const int r0 = 16 * grp - w.B;                    // chunk-relative row of my first h_prev
+        const int rf = 8 * kg - w.B;                      // chunk-relative row of my first h_prev
         const uint32_t prev = s0 + OFF_STAGE + ((cg - 1) % NS) * SB + 4u * i;
-        hp_lo = prev + (uint32_t)((KC + r0) * ROW_BYTES);   // rows r0 .. -1 of the previous chunk
-        hp_hi = s0 + OFF_STAGE + s * SB + 4u * i + (uint32_t)(max(r0, 0) * ROW_BYTES);
-        nsplit = max(0, -r0);
+        hp_lo = prev + (uint32_t)((KC + rf) * ROW_BYTES);   // rows rf .. -1 of the previous chunk
+        hp_hi = s0 + OFF_STAGE + s * SB + 4u * i + (uint32_t)(max(rf, 0) * ROW_BYTES);
+        nsplit = max(0, -rf);
       } else {
         hp_lo = base + 2 * KC * ROW_BYTES;
         hp_hi = hp_lo;
         nsplit = 0;
       }
-      float av[16], bh[8], bl[8];
-      if (nsplit == 0 || nsplit >= 16) {               // my 16 h_prev rows are contiguous
+      float ah[8], al[8], bh[8], bl[8];
+      const bool full = n >= 8 && nlow <= 0;
+      if (nsplit == 0 || nsplit >= 8) {                // my 8 h_prev rows are contiguous
         const uint32_t hp = nsplit == 0 ? hp_hi : hp_lo;
-        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, false>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp, hp, 16);
-        else convert_rows<LO, IX, false, false>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp, hp, 16);
+        if (full) convert8<IX, true, false>(base, xbase, n, nlow, ah, al, bh, bl, dbias, dih, hp, hp, 8);
+        else convert8<IX, false, false>(base, xbase, n, nlow, ah, al, bh, bl, dbias, dih, hp, hp, 8);
       } else {
-        if (n >= 16 && nlow <= 0) convert_rows<LO, IX, true, true>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp_lo, hp_hi, nsplit);
-        else convert_rows<LO, IX, false, true>(base, xbase, n, nlow, av, bh, bl, dbias, dih, hp_lo, hp_hi, nsplit);
+        if (full) convert8<IX, true, true>(base, xbase, n, nlow, ah, al, bh, bl, dbias, dih, hp_lo, hp_hi, nsplit);
+        else convert8<IX, false, true>(base, xbase, n, nlow, ah, al, bh, bl, dbias, dih, hp_lo, hp_hi, nsplit);
       }
       if (!reuse) {
         mbar_arrive(br.empty(s));
@@ -280,15 +279,15 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
         mbar_wait(br.freeb(b), ((cg - NBUF) / NBUF) & 1);
         tc_after();
       }
-      tmem_st16(tl + 128 + 32 * b + 16 * grp, av);
-      const uint32_t bt = s0 + OFF_BT + b * B_BYTES;
-      const int kb = 16 * grp + (LO ? 8 : 0);    // this thread's 8 K columns, rows i (hi) and 64 + i (lo)
+      const uint32_t at = s0 + OFF_BT + b * 2 * B_BYTES, bt = at + B_BYTES;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        sts4(bt + sw_off(i, kb + 4 * q), bh[4 * q], bh[4 * q + 1], bh[4 * q + 2], bh[4 * q + 3]);
-        sts4(bt + sw_off(64 + i, kb + 4 * q), bl[4 * q], bl[4 * q + 1], bl[4 * q + 2], bl[4 * q + 3]);
+        const int kk = 8 * kg + 4 * q;
+        sts4(at + sw_off(i, kk), ah[4 * q], ah[4 * q + 1], ah[4 * q + 2], ah[4 * q + 3]);
+        sts4(at + sw_off(64 + i, kk), al[4 * q], al[4 * q + 1], al[4 * q + 2], al[4 * q + 3]);
+        sts4(bt + sw_off(i, kk), bh[4 * q], bh[4 * q + 1], bh[4 * q + 2], bh[4 * q + 3]);
+        sts4(bt + sw_off(64 + i, kk), bl[4 * q], bl[4 * q + 1], bl[4 * q + 2], bl[4 * q + 3]);
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       tc_before();
       mbar_arrive(br.a_full(b));
@@ -299,13 +298,14 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
     tc_after();
     flush();
     tc_before();
-    const int slab = (LO ? 2 : 0) + grp;
-    float* dst = w.ws + ((part * 4 + slab) * (long long)H + i) * NB;
+    const int slab = (wq & 2) + grp;
+    const int row = (32 * wq + lane) & 63;           // == i: the slab row this thread writes
+    float* dst = w.ws + ((part * 4 + slab) * (long long)H + row) * NB;
 #pragma unroll
     for (int k = 0; k < 64; ++k) dst[k] = acc[k];
 #pragma unroll
-    for (int j = 0; j < IX; ++j) dst[H + j] = LO ? 0.f : dih[j];
-    dst[H + IX] = LO ? 0.f : dbias;
+    for (int j = 0; j < IX; ++j) dst[H + j] = dih[j];
+    dst[H + IX] = dbias;
   }
 }
 
@@ -386,13 +386,13 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
         const int b = (int)(mm.cg % NBUF);
         mbar_wait(br.a_full(b), (uint32_t)((mm.cg / NBUF) & 1));
         tc_after();
-        const uint32_t bt = s0 + OFF_BT + b * B_BYTES;
+        const uint32_t at = s0 + OFF_BT + b * 2 * B_BYTES, bt = at + B_BYTES;
 #pragma unroll
         for (int kk = 0; kk < KC / 8; ++kk) {
           const uint32_t acc = !((mm.c % FLUSH) == 0 && kk == 0);
           asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                       " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
-                       "r"(tmem + 128 + 32 * b + 8 * kk), "l"(sdesc(bt + 32 * kk)), "r"(IDESC), "r"(acc));
+                       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                       "l"(sdesc(at + 32 * kk)), "l"(sdesc(bt + 32 * kk)), "r"(IDESC), "r"(acc));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          br.freeb(b)) : "memory");
@@ -400,21 +400,13 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
       }
     }
     __syncwarp();
-  } else if ((warp & 3) >= 2) {
-    switch (w.I) {     // lo rows ignore x; NB (the slab row length) still depends on I
-      case 0: converters<true, 0>(w, s0, br, tmem, warp, lane); break;
-      case 1: converters<true, 1>(w, s0, br, tmem, warp, lane); break;
-      case 2: converters<true, 2>(w, s0, br, tmem, warp, lane); break;
-      case 3: converters<true, 3>(w, s0, br, tmem, warp, lane); break;
-      default: converters<true, 4>(w, s0, br, tmem, warp, lane); break;
-    }
   } else {
     switch (w.I) {
-      case 0: converters<false, 0>(w, s0, br, tmem, warp, lane); break;
-      case 1: converters<false, 1>(w, s0, br, tmem, warp, lane); break;
-      case 2: converters<false, 2>(w, s0, br, tmem, warp, lane); break;
-      case 3: converters<false, 3>(w, s0, br, tmem, warp, lane); break;
-      default: converters<false, 4>(w, s0, br, tmem, warp, lane); break;
+      case 0: converters<0>(w, s0, br, tmem, warp, lane); break;
+      case 1: converters<1>(w, s0, br, tmem, warp, lane); break;
+      case 2: converters<2>(w, s0, br, tmem, warp, lane); break;
+      case 3: converters<3>(w, s0, br, tmem, warp, lane); break;
+      default: converters<4>(w, s0, br, tmem, warp, lane); break;
     }
   }
   tc_before();
