@@ -43,10 +43,11 @@ def c4_block0(world: int) -> int:
     """Level-0 block per rank for time shards of 2^20 / world steps, measured
     on one B200 (DESIGN "Multi-GPU"): the int8 walk runs one 128-chain tile per
     SM for block0 dependent steps, so its time is ~ceil(tiles / 148) x block0
-    step times; the level-1 fold shrinks with fewer blocks.  Shard up + down:
-    N = 1: 1024 48.8 / 512 49.1 / 256 49.6 ms (full scan); N = 2 (T = 2^19):
-    256 25.2 / 512 24.8 / 1024 25.5; N = 4: 128 13.2 / 256 12.8 / 512 13.0;
-    N = 8: 64 7.26 / 128 6.89 / 256 6.78."""
+    step times; the level-1 fold shrinks with fewer blocks.  Full scan of the
+    shard, ring fold (scripts/block0_sweep.py, r02): N = 1: 512 44.00 / 1024
+    43.67 / 2048 44.89 ms; N = 2 (T = 2^19): 256 22.27 / 512 21.88 / 1024
+    22.13; N = 4: 128 11.32 / 256 10.91 / 512 11.13; N = 8: 128 5.87 / 256
+    5.68 / 512 6.78."""
     return {1: 1024, 2: 512}.get(world, 256)
 SMALL = {   # secondary configs (N = 1 sweep): (T, B, H, block0, block)
     "c1": dict(T=1000, B=16, H=20, block0=8, block=8),
