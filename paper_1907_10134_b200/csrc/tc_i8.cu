@@ -48,10 +48,9 @@
 // doubled the norm-preserving error at T = 65536 (8.5e-5 vs 4.0e-5, worst
 // block 1.05e-4 > the gate) and non-power-of-two scales break the integer
 // families' bit-exactness (scripts/prec_ab.py, scripts/ozaki_sim2.py).
-// Measured too (scripts/tc_i8_rate2.cu): an i8 MMA costs ~180 (TS) / ~250
-// (SS) cycles whatever N (64..256) and whether or not consecutive MMAs share
-// an accumulator, so the 6 MMAs per step are the tensor floor (~920 cycles
-// issue -> D ready in the fold's trace, scripts/f8_trace.py).  This two-slot
+// MMA cost with precomputed descriptors (scripts/tc_i8_rate2.cu): M = 128,
+// K = 32 i8: N = 64 78, N = 128 92, N = 256 156 cycles per MMA, so the six
+// MMAs of a step are ~744 cycles of tensor pipe; the epilogue bounds.  This two-slot
 // kernel is the fallback (-DBPPSA_FOLD_TWO_SLOT); the default is the ring
 // kernel tc_fold_i8r_kernel below (4 tiles over 2 accumulators, 40 ms).
 // Tried and slower: 16 epilogue warps
