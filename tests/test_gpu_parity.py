@@ -158,6 +158,21 @@ def test_rnn_int8_norm_preserving(lib, B, blocks):
     assert et <= TOL and et <= max(3 * ef, 2e-5)
 
 
+@pytest.mark.parametrize("T,B,blocks", [(3001, 33, (7, 4)), (1500, 64, (24, 8)), (999, 128, (1000, 32)),
+                                         (5000, 9, (2048, 16)), (257, 2, (2, 2))])
+def test_rnn_int8_ring_shapes(lib, T, B, blocks):
+    """The ring fold's ticket schedule (4 tile groups over 2 accumulators)
+    under uneven work: many tiles per group (B = 64, 128), odd B, blocks longer
+    than T, 2-step blocks, ragged tails — against the oracle and the FFMA
+    engine on the norm-preserving family."""
+    f = W.norm_preserving_rnn(T, B, 64, seed=T + B)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    gt, it = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1])
+    gf, i_f = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1], leaf_impl="ffma")
+    et, ef = rel_pair(gt, ref, it, ref_init), rel_pair(gf, ref, i_f, ref_init)
+    assert et <= TOL and et <= max(3 * ef, 2e-5), (et, ef)
+
+
 def test_rnn_config1(lib):
     """C1: tanh RNN, H = 20, B = 16, T = 1000."""
     w = W.rnn_workload(1000, 16, 20, seed=0)
