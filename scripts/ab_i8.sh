@@ -7,6 +7,6 @@ for v in "$@"; do
   (cd $D && BPPSA_NVCC_EXTRA="$v" python paper_1907_10134_b200/build.py --force > /dev/null 2>&1 || echo "build failed: $v")
   [ -z "$NOPREC" ] && (cd $D && python scripts/prec_ab.py 4096 | sed "s/^/[$v] /")
   for rep in 1 2; do
-    echo "[$v]" $(cd $D && python scripts/kbench.py c4b1024 | grep -o "kernels \[[0-9.]*\|wgrad [0-9.]*")
+    echo "[$v]" $(cd $D && python scripts/kbench.py c4b1024 | grep -o 'kernels \[[0-9., ]*\]\|wgrad [0-9.]*')
   done
 done
