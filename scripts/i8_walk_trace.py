@@ -21,7 +21,7 @@ torch.cuda.synchronize()
 buf = np.zeros((12, 2048), dtype=np.int64)
 import ctypes  # noqa: E402
 api._lib.bppsa_debug_i8_trace(buf.ctypes.data_as(ctypes.c_void_p))
-names = ["step start", "copy_out issued", "h landed", "pm stored", "exchanged", "digits packed", "MMA done (issuer)",
+names = ["step start", "staged+stored", "h landed", "pm stored", "exchanged", "digits packed", "digits in TMEM",
          "A barrier", "D ready", "regions -> v"]
 d = buf[:, 100:500].astype(np.float64)
 for i, nm in enumerate(names):
