@@ -654,12 +654,14 @@ static bppsa_status scan_impl(const bppsa_jac* jac, const float* seed, const flo
 
 bppsa_status bppsa_scan(const bppsa_jac* jac, const float* seed, float* grad_h, float* grad_h_init, void* ws,
                         size_t ws_bytes, const bppsa_scan_opts* opts, void* stream) {
+  NvtxRange nvtx_("bppsa_scan");
   return scan_impl(jac, seed, nullptr, grad_h, grad_h_init, ws, ws_bytes, opts, stream);
 }
 
 bppsa_status bppsa_scan_affine(const bppsa_jac* jac, const float* seed, const float* e, float* grad_h,
                                float* grad_h_init, void* ws, size_t ws_bytes, const bppsa_scan_opts* opts,
                                void* stream) {
+  NvtxRange nvtx_("bppsa_scan_affine");
   REQUIRE_DEV(e, "e");
   const int mode = opts ? opts->mode : BPPSA_SCAN_BLOCKED;
   if (mode != BPPSA_SCAN_BLOCKED && mode != BPPSA_SCAN_LINEAR)
@@ -669,6 +671,7 @@ bppsa_status bppsa_scan_affine(const bppsa_jac* jac, const float* seed, const fl
 
 bppsa_status bppsa_scan_shard_up(const bppsa_jac* jac, const float* seed, float* aggregate, void* ws,
                                  size_t ws_bytes, const bppsa_scan_opts* opts, void* stream) {
+  NvtxRange nvtx_("bppsa_scan_shard_up");
   bppsa_status s = check_jac(jac);
   if (s != BPPSA_OK) return s;
   REQUIRE_DEV(aggregate, "aggregate");
@@ -697,6 +700,7 @@ bppsa_status bppsa_scan_shard_up_publish(const bppsa_jac* jac, const float* seed
                                          size_t ws_bytes, const bppsa_scan_opts* opts, int rank, int world,
                                          float* const* peer_mailboxes, unsigned* const* peer_flags,
                                          unsigned* counter, const unsigned* acks, unsigned epoch, void* stream) {
+  NvtxRange nvtx_("bppsa_scan_shard_up_publish");
   bppsa_status s = check_jac(jac);
   if (s != BPPSA_OK) return s;
   REQUIRE_DEV(aggregate, "aggregate");
@@ -748,6 +752,7 @@ bppsa_status bppsa_scan_shard_up_publish(const bppsa_jac* jac, const float* seed
 bppsa_status bppsa_scan_shard_down(const bppsa_jac* jac, const float* seed, const float* gathered, int rank,
                                    int world, float* grad_h, float* grad_h_init, void* ws, size_t ws_bytes,
                                    const bppsa_scan_opts* opts, void* stream) {
+  NvtxRange nvtx_("bppsa_scan_shard_down");
   bppsa_status s = check_jac(jac);
   if (s != BPPSA_OK) return s;
   if (world < 1 || rank < 0 || rank >= world) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad rank/world");
@@ -833,6 +838,7 @@ bppsa_status bppsa_weight_grads_workspace_size(int T, int B, int H, int I, size_
 bppsa_status bppsa_weight_grads_rnn(int T, int B, int H, int I, const float* x, const float* h,
                                     const float* h_init, const float* grad_h, float* dW_ih, float* dW_hh, float* db,
                                     void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bppsa_weight_grads_rnn");
   size_t need;
   bppsa_status s = bppsa_weight_grads_workspace_size(T, B, H, I, &need);
   if (s != BPPSA_OK) return s;
@@ -915,6 +921,7 @@ bppsa_status bppsa_weight_grads_gru(int T, int B, int H, int I, const float* x, 
                                     const float* r, const float* z, const float* n, const float* M,
                                     const float* grad_h, float* dW_ih3, float* dW_hh3, float* db_ih3,
                                     float* db_hh3, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bppsa_weight_grads_gru");
   size_t need;
   bppsa_status s = bppsa_weight_grads_workspace_size(T, B, H, I, &need);
   if (s != BPPSA_OK) return s;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -10,6 +11,13 @@
 #include "../../include/bppsa.h"
 
 namespace bppsa {
+
+// NVTX range around every C-ABI entry point (header-only nvtx3: free when no
+// profiler is attached; named ranges in nsys / ncu timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ---------------------------------------------------------------------------
 // Error plumbing (thread-local detail string, status codes; no exceptions

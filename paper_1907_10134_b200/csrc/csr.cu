@@ -675,11 +675,13 @@ static bppsa_status csr_plan_create_impl(const bppsa_csr_pattern* chain, int n, 
 
 bppsa_status bppsa_csr_plan_create(const bppsa_csr_pattern* chain, int n, int up_levels, int down_levels,
                                    long long max_contributions, bppsa_csr_plan** out_plan) {
+  NvtxRange nvtx_("bppsa_csr_plan_create");
   return csr_plan_create_impl(chain, n, up_levels, down_levels, max_contributions, false, out_plan);
 }
 
 bppsa_status bppsa_csr_plan_create_symbolic(const bppsa_csr_pattern* chain, int n, int up_levels, int down_levels,
                                             bppsa_csr_plan** out_plan) {
+  NvtxRange nvtx_("bppsa_csr_plan_create_symbolic");
   return csr_plan_create_impl(chain, n, up_levels, down_levels, 0, true, out_plan);
 }
 
@@ -713,6 +715,7 @@ bppsa_status bppsa_csr_plan_steps(const bppsa_csr_plan* plan, bppsa_csr_step* st
 
 bppsa_status bppsa_csr_scan(const bppsa_csr_plan* plan, int B, const float* const* data, const int* batched,
                             const float* seed, float* const* grads, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bppsa_csr_scan");
   if (!plan || !data || !seed || !grads || B < 1) return fail(BPPSA_ERR_INVALID_ARGUMENT, "bad arguments");
   if (plan->symbolic) return fail(BPPSA_ERR_NOT_SUPPORTED, "a symbolic plan has no numeric scan");
   const bppsa_csr_plan& P = *plan;
