@@ -70,6 +70,9 @@
 // 8 epilogue warps per slot (thread = chain row x 32 columns); the row max of
 // y is exchanged between the row's two threads through shared memory.
 #include <algorithm>
+#include <cstdlib>
+
+#include <cuda.h>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -1198,6 +1201,320 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8_kernel(LeafArgs a, int C
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// The int8 walk with TMA (the default when B <= 128): the same arithmetic as
+// tc_walk_i8_kernel, the data movement of the opt-in 3xFP16 walk.  A tile is
+// G = 128 / B whole groups of B chains (G consecutive level-0 blocks, all
+// samples), so the h rows of one step are one 5D box {32, 2, B, 1, G} (block
+// 0's tile and blocks whose box would leave the view: 3D boxes per group),
+// loaded by TMA into a ring of SWIZZLE_128B stages two steps ahead; every
+// thread overwrites the h slice it consumed with v (the exclusive output
+// grad_h[t]) and the issuer TMA-stores the stage with the same box — the
+// stores are asynchronous bulk operations, so the grad_h write-back no longer
+// blocks the epilogue under memory back-pressure (the cp.async / STG walk
+// above: ~2000 of ~3950 cycles per step).  One tile per CTA at a time, 16
+// warps (thread = chain row x 16 columns, row max over 4 threads), digits in
+// TMEM (TS form), D of step st read at the start of step st + 1.
+// ---------------------------------------------------------------------------
+constexpr int WT_NST = 3;                           // ring stages
+constexpr int WT_STAGE = TM * 256;                  // [128 rows][2 halves][128 B]
+constexpr int WT_OFF_RING = I8_B_BYTES;
+constexpr int WT_OFF_RED = WT_OFF_RING + WT_NST * WT_STAGE;   // [parity][128 rows][4] u32
+constexpr int WT_OFF_BAR = WT_OFF_RED + 2 * TM * 16;
+constexpr int WT_SMEM = WT_OFF_BAR + 64 + 1024;
+
+__global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, const __grid_constant__ CUtensorMap h3,
+                                                              const __grid_constant__ CUtensorMap h5,
+                                                              const __grid_constant__ CUtensorMap g3,
+                                                              const __grid_constant__ CUtensorMap g5, int C,
+                                                              const float* __restrict__ carry, long long nblk,
+                                                              float* __restrict__ grad_init, int G) {
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(smem + WT_OFF_BAR);
+  uint64_t* h_full = d_full + 1;                    // [WT_NST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_full + WT_NST);
+  uint32_t* wred = tmem_slot + 1;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int B = a.seg.B;
+  const long long S = a.seg.S();
+
+  if (threadIdx.x == 0) wred[0] = 0;
+  for (int e = threadIdx.x; e < WT_NST * WT_STAGE / 16; e += WK_EPI)
+    sts128(su32(smem + WT_OFF_RING) + 16u * e, 0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  int tau;
+  w_digits(a.W, smem, wred, &tau);
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(su32(&d_full[0]), 1);
+      for (int k = 0; k < WT_NST; ++k) mbar_init(su32(&h_full[k]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&h3)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&h5)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&g3)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&g5)) : "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int quad = warp & 3, row = quad * 32 + lane, cq = warp >> 2;   // columns [16 cq, 16 cq + 16)
+  const bool issuer = warp == 0;
+  const uint32_t t_mine = tmem + ((uint32_t)(quad * 32) << 16) + 16 * cq;
+  const uint32_t a_mine = tmem + ((uint32_t)(quad * 32) << 16) + WK_A_COL + 4 * cq;
+  const uint32_t ring = su32(smem + WT_OFF_RING);
+  const int half = cq >> 1;
+  const uint32_t hrow_off = (uint32_t)(row * 256 + half * 128);         // my half-row in a stage
+  const int swz = (2 * row + half) & 7;                                 // its 128-byte line's swizzle
+  const int c0 = (cq & 1) * 4;                                           // my first 16-byte chunk of the line
+  const uint32_t red0 = su32(smem + WT_OFF_RED) + (uint32_t)(row * 16);
+  const uint32_t dbar = su32(&d_full[0]), hbar0 = su32(&h_full[0]);
+  uint64_t bd[2];
+  {
+    const uint32_t bb = __shfl_sync(0xffffffffu, su32(smem), 0);
+    bd[0] = sdesc64(bb);
+    bd[1] = sdesc64(bb + 32);
+  }
+  const uint32_t a_tile = __shfl_sync(0xffffffffu, tmem + WK_A_COL, 0);
+  uint32_t dph = 0, par = 0, gs = 0;
+  // tile row = j B + b holds group r = G-1-j (block q = qb + r), sample b: the
+  // 5D box delivers the groups of one step in decreasing q order
+  const int jrow = row / B, bsm = row % B, grp = G - 1 - jrow;
+  // view of the time axis as (block c4, step c3): t = c4 C + c3 = Tm - q C - st
+  const long long Tm = (long long)a.seg.T - 1 + a.seg.head;
+  const int A_blk = (int)(Tm / C), R_off = (int)(Tm % C);
+  // tiles: [0] = block 0 alone; [1 .. nfull] = G blocks each whose merged box
+  // stays inside the view at every step; then the remaining blocks two per tile
+  const long long nfull = A_blk > 1 ? (A_blk - 1) / G : 0;
+  const long long rem0 = 1 + nfull * G;
+  const long long ntiles = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
+
+  for (long long tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+    const bool merged = tt >= 1 && tt <= nfull;
+    const long long qb = tt == 0 ? 0 : (merged ? 1 + (tt - 1) * G : rem0 + 2 * (tt - nfull - 1));
+    const int ng = tt == 0 ? 1 : (merged ? G : (int)min(2LL, nblk - qb));   // groups in this tile
+    const long long q = qb + grp;
+    const bool valid = jrow < G && grp < ng;
+    const bool head = a.seg.head && q == 0;
+    const long long s_start = head ? 1 : q * C, s1 = min(q * C + C, S);
+    const int len = valid ? (int)(s1 - s_start) : 0;
+    const bool total = valid && grad_init != nullptr && s1 == S;
+    const int nJ = total ? len : max(len - 1, 0);          // J applications of this chain
+    float2 v[8];                                    // this thread's 16 columns of the chain (true scale)
+    {
+      const float* src = head ? a.seed + (long long)bsm * TH : carry + ((long long)bsm * nblk + q) * TH;
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const float4 f = valid ? __ldg(reinterpret_cast<const float4*>(src + 16 * cq) + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[2 * k4] = make_float2(f.x, f.y);
+        v[2 * k4 + 1] = make_float2(f.z, f.w);
+      }
+    }
+    long long my_ss = 0, my_len = 0;                 // issuer lane r: group r's slot start and length
+    const bool my_on = lane < ng;
+    if (my_on) {
+      const long long qr = qb + lane;
+      my_ss = (a.seg.head && qr == 0) ? 1 : qr * C;
+      my_len = min(qr * C + C, S) - my_ss;
+    }
+    const uint32_t my_dst = (uint32_t)((G - 1 - lane) * B * 256);
+    auto c5 = [&](int st, int& c3, int& c4) {
+      c3 = R_off - st;
+      c4 = A_blk - (int)(qb + G - 1);
+      if (c3 < 0) { c3 += C; c4 -= 1; }
+      return merged;
+    };
+    auto issue_loads = [&](int st, uint32_t gstep) {       // all lanes of the issuer warp
+      const uint32_t stage = ring + (gstep % WT_NST) * WT_STAGE;
+      const uint32_t bar = hbar0 + 8u * (gstep % WT_NST);
+      int c3, c4;
+      if (c5(st, c3, c4)) {
+        if (lane == 0) {
+          mbar_arrive_tx(bar, 256u * (uint32_t)(B * G));
+          asm volatile(
+              "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+              "%6}], [%7];\n" ::"r"(stage),
+              "l"(reinterpret_cast<uint64_t>(&h5)), "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(bar)
+              : "memory");
+        }
+      } else {
+        uint32_t bytes = 0;
+        for (int r = 0; r < ng; ++r) {
+          const long long qr = qb + r;
+          const long long ss = (a.seg.head && qr == 0) ? 1 : qr * C, se = min(qr * C + C, S);
+          if (st < se - ss) bytes += 256u * (uint32_t)B;
+        }
+        if (lane == 0) mbar_arrive_tx(bar, bytes);
+        __syncwarp();
+        if (my_on && st < my_len)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+              "[%5];\n" ::"r"(stage + my_dst),
+              "l"(reinterpret_cast<uint64_t>(&h3)), "r"(0), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(bar)
+              : "memory");
+      }
+    };
+    auto issue_stores = [&](int st, uint32_t gstep) {
+      const uint32_t stage = ring + (gstep % WT_NST) * WT_STAGE;
+      int c3, c4;
+      if (c5(st, c3, c4)) {
+        if (lane == 0)
+          asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(
+                           reinterpret_cast<uint64_t>(&g5)),
+                       "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(stage)
+                       : "memory");
+      } else if (my_on && st < my_len) {
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                         reinterpret_cast<uint64_t>(&g3)),
+                     "r"(0), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(stage + my_dst)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    };
+    if (issuer) {
+      // the stages about to be refilled were last stored from by this warp
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      issue_loads(0, gs);
+      if (C > 1) issue_loads(1, gs + 1);
+      __syncwarp();
+    }
+    float f_prev = 0.f;                              // v = D f after the previous step's MMAs
+    for (int st = 0; st < C; ++st, ++gs) {
+      const int tz = (int)(tt / gridDim.x) * C + st;
+      (void)tz;
+      if (warp == 0) I8T(0, tz);
+      if (issuer) {                                  // D of step st-1 and h of step st
+        if (lane == 0) {
+          if (st > 0) mbar_wait(dbar, dph);
+          mbar_wait(hbar0 + 8u * (gs % WT_NST), (gs / WT_NST) & 1);
+        }
+        __syncwarp();
+      }
+      named_bar(2, WK_EPI);
+      if (warp == 0) I8T(1, tz);
+      if (st > 0) {
+        dph ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          float2 c[4];
+          regions_to_c(t_mine + 8 * qq, c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[4 * qq + i] = __fmul2_rn(c[i], make_float2(f_prev, f_prev));
+        }
+        if (total && st == len) {                    // dl/dh_init = J_0^T grad_h[0]
+          float4* dst = reinterpret_cast<float4*>(grad_init + (long long)bsm * TH + 16 * cq);
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) dst[k4] = make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+        }
+      }
+      // y = d o v from the staged, swizzled h slice; grad_h[t(s)] = v written in its place
+      const uint32_t stg = ring + (gs % WT_NST) * WT_STAGE + hrow_off;
+      const bool apply = st < nJ;
+      float2 y[8];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t hp = stg + (uint32_t)(((c0 + c) ^ swz) << 4);
+        const float4 h4 = lds128(hp);
+        sts128(hp, v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
+        const float2 d0 = make_float2(fmaf(-h4.x, h4.x, 1.f), fmaf(-h4.y, h4.y, 1.f));
+        const float2 d1 = make_float2(fmaf(-h4.z, h4.z, 1.f), fmaf(-h4.w, h4.w, 1.f));
+        y[2 * c] = apply ? __fmul2_rn(d0, v[2 * c]) : make_float2(0.f, 0.f);
+        y[2 * c + 1] = apply ? __fmul2_rn(d1, v[2 * c + 1]) : make_float2(0.f, 0.f);
+      }
+      if (warp == 0) I8T(2, tz);
+      float pm = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pm = fmaxf(pm, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
+      const uint32_t redp = red0 + par * (TM * 16);
+      asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(redp + 4u * cq), "r"(__float_as_uint(pm)) : "memory");
+      named_bar(3 + quad, 128);                      // the row's four threads (warps quad + 4 cq)
+      uint32_t m4[4];
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(m4[0]), "=r"(m4[1]), "=r"(m4[2]), "=r"(m4[3])
+                   : "r"(redp)
+                   : "memory");
+      par ^= 1;
+      if (warp == 0) I8T(3, tz);
+      const float M = __uint_as_float(max(max(m4[0], m4[1]), max(m4[2], m4[3])));
+      const int sig = M > 0.f ? row_sigma(M) : 0;
+      const float2 scl = make_float2(pow2f(sig), pow2f(sig)), scl8 = make_float2(pow2f(sig - 8), pow2f(sig - 8));
+      f_prev = M > 0.f ? exp2i(32 - sig - tau) : 0.f;
+      uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t X0, X1, X2, X3;
+        rint24x2(y[2 * u], scl, scl8, X0, X1);
+        rint24x2(y[2 * u + 1], scl, scl8, X2, X3);
+        const uint32_t p01 = prmt(X0, X1, 0x5140u), p23 = prmt(X2, X3, 0x5140u);
+        const uint32_t q01 = prmt(X0, X1, 0x0062u), q23 = prmt(X2, X3, 0x0062u);
+        w2[u] = prmt(p01, p23, 0x5410u);
+        w1[u] = prmt(p01, p23, 0x7632u);
+        w0[u] = prmt(q01, q23, 0x5410u);
+      }
+      tmem_st4(a_mine, w0[0], w0[1], w0[2], w0[3]);
+      tmem_st4(a_mine + 16, w1[0], w1[1], w1[2], w1[3]);
+      tmem_st4(a_mine + 32, w2[0], w2[1], w2[2], w2[3]);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      fence_async_smem();                            // grad_h rows (stored long before) -> visible to the TMA store
+      tc_fence_before();
+      if (warp == 0) I8T(4, tz);
+      named_bar(1, WK_EPI);                          // digits complete, stage consumed and rewritten
+      if (warp == 0) I8T(5, tz);
+      if (issuer) {
+        tc_fence_after();
+        mma6_i8_ts_commit(tmem, a_tile, bd, dbar);
+        issue_stores(st, gs);
+        if (st + 2 < C) {
+          // stage (gs + 2) % 3 was stored from at step st - 1: its reads must be done
+          asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+          issue_loads(st + 2, gs + 2);
+        }
+        __syncwarp();
+      }
+      if (warp == 0) I8T(6, tz);
+    }
+    // D of the last step (keeps the barrier phase; grad_init if the chain ends here)
+    if (issuer) {
+      if (lane == 0) mbar_wait(dbar, dph);
+      __syncwarp();
+    }
+    named_bar(2, WK_EPI);
+    dph ^= 1;
+    tc_fence_after();
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq) {                 // tcgen05.ld is warp-aligned: every lane loads
+      float2 c[4];
+      regions_to_c(t_mine + 8 * qq, c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[4 * qq + i] = __fmul2_rn(c[i], make_float2(f_prev, f_prev));
+    }
+    if (total && len == C) {
+      float4* dst = reinterpret_cast<float4*>(grad_init + (long long)bsm * TH + 16 * cq);
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) dst[k4] = make_float4(v[2 * k4].x, v[2 * k4].y, v[2 * k4 + 1].x, v[2 * k4 + 1].y);
+    }
+    tc_fence_before();
+    named_bar(2, WK_EPI);                            // the D reads are done before the next tile's MMAs
+  }
+  if (issuer) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // the last stores have landed
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 }  // namespace
 
 #ifdef BPPSA_F8_TRACE
@@ -1234,9 +1551,29 @@ cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long lon
 }
 
 // Level-0 walk of an RNN H = 64 segment on the integer tensor cores.
+cudaError_t make_walk_map(const float* base, int T, int B, int C, long long A, bool five, int G, CUtensorMap* map);
+
 cudaError_t launch_tc_walk_i8(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                               float* grad_init, int num_sms, cudaStream_t st) {
   if (a.seg.H != TH) return cudaErrorInvalidValue;
+  static const bool cpasync = std::getenv("BPPSA_WALK_I8_CPASYNC") != nullptr;   // dev aid: the cp.async walk
+  if (a.seg.B <= TM && !cpasync) {
+    const int B = a.seg.B, G = TM / B;
+    const long long Tm = (long long)a.seg.T - 1 + a.seg.head;
+    CUtensorMap maps[4];
+    cudaError_t e = cudaSuccess;
+    for (int m = 0; m < 4 && e == cudaSuccess; ++m)
+      e = make_walk_map(m < 2 ? a.h : grad_h, a.seg.T, B, C, Tm / C, m % 2 == 1, G, &maps[m]);
+    if (e != cudaSuccess) return e;
+    const long long A = Tm / C, nfull = A > 1 ? (A - 1) / G : 0, rem0 = 1 + nfull * G;
+    const long long nt = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
+    const int gridw = (int)std::min<long long>(nt, num_sms);
+    e = smem_attr_once(reinterpret_cast<const void*>(tc_walk_i8t_kernel), WT_SMEM);
+    if (e != cudaSuccess) return e;
+    tc_walk_i8t_kernel<<<gridw, WK_EPI, WT_SMEM, st>>>(a, maps[0], maps[1], maps[2], maps[3], C, carry, nblk,
+                                                       grad_init, G);
+    return cudaGetLastError();
+  }
   const long long ntiles = ((long long)a.seg.B * nblk + TM - 1) / TM;
   const int grid = (int)std::min<long long>(ntiles, num_sms);
   if (grid <= 0) return cudaSuccess;

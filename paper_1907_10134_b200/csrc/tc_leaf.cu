@@ -1767,8 +1767,8 @@ cudaError_t launch_tc_leaf_up(const LeafArgs& a, int C, float* agg_out, long lon
 // or 5D {32, 2, B, C, A} (time t = c4 C + c3, t < A C) with box {32, 2, B, 1,
 // G} (one step of G consecutive blocks).  The driver entry point is fetched
 // through the runtime, so nothing links against libcuda.
-static cudaError_t make_walk_map(const float* base, int T, int B, int C, long long A, bool five, int G,
-                                 CUtensorMap* map) {
+cudaError_t make_walk_map(const float* base, int T, int B, int C, long long A, bool five, int G,
+                          CUtensorMap* map) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);

@@ -21,8 +21,13 @@ torch.cuda.synchronize()
 buf = np.zeros((12, 2048), dtype=np.int64)
 import ctypes  # noqa: E402
 api._lib.bppsa_debug_i8_trace(buf.ctypes.data_as(ctypes.c_void_p))
-names = ["step start", "staged+stored", "h landed", "pm stored", "exchanged", "digits packed", "digits in TMEM",
-         "A barrier", "D ready", "regions -> v"]
+import os as _os
+if _os.environ.get("WT"):      # the TMA walk's events
+    names = ["step top", "D+h ready (bar)", "y + v stored", "exchanged", "digits in TMEM", "digit barrier",
+             "MMA+TMA issued", "-", "-", "-"]
+else:
+    names = ["step start", "staged+stored", "h landed", "pm stored", "exchanged", "digits packed", "digits in TMEM",
+             "A barrier", "D ready", "regions -> v"]
 d = buf[:, 100:500].astype(np.float64)
 for i, nm in enumerate(names):
     print(f"  {nm:16s} {np.median(d[i] - d[0]):8.0f}")
