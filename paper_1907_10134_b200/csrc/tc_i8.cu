@@ -298,8 +298,16 @@ __device__ __forceinline__ void regions8_to_y(const uint32_t (&r)[32], float4 da
 __device__ long long g_f8_trace[16][4096];
 #define F8T(ev, i) \
   if (blockIdx.x == 0 && issuer && lane == 0 && (i) < 4096) g_f8_trace[g * 8 + (ev)][i] = clock64();
+// the ring fold: [group * 8 + event][step of the group] on CTA 0, each group's warp 0 lane 0
+__device__ long long g_r8_trace[32][4096];
+#define R8T(ev, i) \
+  if (blockIdx.x == 0 && wl == 0 && lane == 0 && (i) < 4096) g_r8_trace[g * 8 + (ev)][i] = clock64();
+#define R8V(ev, i, val) \
+  if (blockIdx.x == 0 && wl == 0 && lane == 0 && (i) < 4096) g_r8_trace[g * 8 + (ev)][i] = (val);
 #else
 #define F8T(ev, i)
+#define R8T(ev, i)
+#define R8V(ev, i, val)
 #endif
 #ifdef BPPSA_I8_TRACE
 // dev aid: clock64 per step on CTA 0 (warp 0, lane 0): [event][step]
@@ -600,6 +608,10 @@ constexpr bool R_PIPE = R_PIPE_DEF;
 #define R_X16_DEF 1
 #endif
 constexpr bool R_X16 = R_X16_DEF;
+#ifndef R_LATE_D_DEF
+#define R_LATE_D_DEF 1
+#endif
+constexpr bool R_LATE_D = R_LATE_D_DEF;             // y = c o d after the accumulator release (38.3 vs 38.8 ms)
 constexpr int R_WPS = 4, R_EPI = 32 * R_WPS;        // warps per group
 constexpr int R_THREADS = R_NT * R_EPI;
 #ifndef R_HCH_DEF
@@ -686,7 +698,10 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
   auto hsb = [&](int c) { return reinterpret_cast<float*>(hsb0 + c * R_H_BYTES); };
   const uint32_t dfull = su32(&d_full[g]);
   uint32_t kr = 0;                                  // this group's MMA rounds so far
-  int cur = 0;                                      // the accumulator of the group's outstanding batch
+  int cur = 0;
+#ifdef BPPSA_F8_TRACE
+  int nstep = 0;                                    // trace index
+#endif                                      // the accumulator of the group's outstanding batch
   const long long rowB = (long long)B * TH;
   auto issue_chunk = [&](long long tx, long long scx, float* hb) {
     const long long qx = q0 + tx / nbp;
@@ -713,14 +728,21 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
   auto issue = [&]() {
     uint32_t it = 0;
     if (wl == 0) {
-      if (lane == 0) {
-        it = atomicAdd(ticket, 1u);
-        bufsel[2 * g + (kr & 1)] = it & 1;
+      if (lane == 0) {                              // shared-window atomics (a generic atomicAdd is an ATOM.E)
+        asm volatile("atom.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(it) : "r"(su32(ticket)) : "memory");
+        asm volatile("st.shared::cta.u32 [%0], %1;\n" ::"r"(su32(&bufsel[2 * g + (kr & 1)])), "r"(it & 1u) : "memory");
       }
       it = __shfl_sync(0xffffffffu, it, 0);
     }
+    R8T(3, nstep);
     named_bar(1 + R_NT + g, R_EPI);
-    cur = (int)*reinterpret_cast<volatile uint32_t*>(&bufsel[2 * g + (kr & 1)]);
+    R8T(4, nstep);
+    R8V(6, nstep, (long long)it);
+    {
+      uint32_t cs;
+      asm volatile("ld.shared::cta.u32 %0, [%1];\n" : "=r"(cs) : "r"(su32(&bufsel[2 * g + (kr & 1)])) : "memory");
+      cur = (int)cs;
+    }
     if (wl == 0) {
       if (lane == 0) {
         const uint32_t need = (it >> 1) * R_WPS, ra = su32(&rel[it & 1]);
@@ -732,14 +754,17 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
         }
       }
       __syncwarp();
+      R8T(5, nstep);
       tc_fence_after();
       mma6_i8_commit(tmem + 256u * (uint32_t)cur, ad, bd, dfull);
     }
   };
   // wait for the group's outstanding batch; returns its TMEM base for this warp's lanes
   auto wait_d = [&]() {
+    R8T(0, nstep);
     if (lane == 0) mbar_wait_sleep(dfull, kr & 1);
     __syncwarp();
+    R8T(1, nstep);
     ++kr;
     tc_fence_after();
     return tmem + 256u * (uint32_t)cur + t_lane;
@@ -748,6 +773,7 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
     tc_fence_before();
     __syncwarp();
     if (lane == 0) asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;\n" ::"r"(su32(&rel[cur])) : "memory");
+    R8T(2, nstep);
   };
   int cb = 0;
   {
@@ -798,6 +824,10 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
           if (R_X16) {                              // x16 loads, one 16-column chunk at a time (64 registers)
 #pragma unroll
             for (int c16 = 0; c16 < 4; ++c16) {
+              if (R_LATE_D) {                       // c only: the accumulator is released sooner
+                regions_to_c16(td + 16 * c16, *reinterpret_cast<float2(*)[8]>(y + 8 * c16));
+                continue;
+              }
               float2 c[8];
               regions_to_c16(td + 16 * c16, c);
 #pragma unroll
@@ -834,6 +864,14 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
             }
           }
           release_d();
+          if (R_X16 && R_LATE_D) {                  // y = c o d after the release
+#pragma unroll
+            for (int q4 = 0; q4 < 16; ++q4) {
+              const float4 d4 = lds128(dp + 16u * q4);
+              y[2 * q4] = __fmul2_rn(y[2 * q4], make_float2(d4.x, d4.y));
+              y[2 * q4 + 1] = __fmul2_rn(y[2 * q4 + 1], make_float2(d4.z, d4.w));
+            }
+          }
         }
         first = false;
         float M = 0.f;
@@ -870,6 +908,9 @@ __global__ void __launch_bounds__(R_THREADS, 1) tc_fold_i8r_kernel(LeafArgs a, i
         fence_async_smem();                         // the digits -> visible to the tensor core
         tc_fence_before();
         issue();
+#ifdef BPPSA_F8_TRACE
+        ++nstep;
+#endif
       }
     }
     float2 cfin[32];
@@ -1520,6 +1561,9 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
 #ifdef BPPSA_F8_TRACE
 extern "C" int bppsa_debug_f8_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, g_f8_trace, sizeof(g_f8_trace));
+}
+extern "C" int bppsa_debug_r8_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_r8_trace, sizeof(g_r8_trace));
 }
 #endif
 #ifdef BPPSA_I8_TRACE
