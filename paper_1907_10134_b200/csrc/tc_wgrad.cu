@@ -18,7 +18,15 @@
 //                    of TMEM — there its hi and lo rows sat in different lane
 //                    quadrants, so two threads formed each delta (2.2 ms).
 // Synchronisation is mbarrier-only: full/empty per stage, a_full/freeb per
-// A/B buffer.  The accumulator is flushed into fp32 registers every FLUSH
+// A/B buffer.  What bounds it (r02g, dev-aid macros WG_NO_LOAD / NO_CONV /
+// NO_MMA / NO_FENCE that strip one stage each, timing only): 2.18 ms whole;
+// 2.06 without the HBM reads, 1.54 without the conversion, 1.30 with
+// neither, 0.85 with no MMAs and no proxy fence either -- the converter /
+// MMA pipeline, not HBM, sets the pace: per 32-row chunk ~104 KB of shared
+// memory traffic (16 KB bulk writes, 24 KB of h / g / h_prev reads, 32 KB of
+// split operands written and read again by the SS MMAs) plus the handshakes.
+// 16 converter warps (4 rows each) measured 2.47 ms (spills at 96
+// registers), more stages 2.33-2.38, one arrival per warp 2.24.  The accumulator is flushed into fp32 registers every FLUSH
 // chunks so the tensor core's truncating accumulation never spans more than
 // FLUSH*4 MMAs.  dW_ih and db accumulate on the CUDA cores.  Rows are split
 // into fixed parts (a function of K only); each part writes four slabs
@@ -40,7 +48,7 @@ constexpr int MAXI = 4;
 #define WG_NS 4
 #endif
 #ifndef WG_NBUF
-#define WG_NBUF 3
+#define WG_NBUF 2                                   // 2.18-2.23 ms at C4 vs 2.27-2.41 with 3 (r02g A/B)
 #endif
 constexpr int NS = WG_NS;                           // staging depth (chunks)
 constexpr int NBUF = WG_NBUF;                       // A / B operand buffer pairs (shared memory)
@@ -256,7 +264,15 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
         nsplit = 0;
       }
       float ah[8], al[8], bh[8], bl[8];
+#ifdef WG_NO_CONV                                   // dev aid: the pipeline without the conversion (timing only)
+      const bool full = false;
+      if (true) {
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) ah[rr] = al[rr] = bh[rr] = bl[rr] = 0.f;
+      } else
+#else
       const bool full = n >= 8 && nlow <= 0;
+#endif
       if (nsplit == 0 || nsplit >= 8) {                // my 8 h_prev rows are contiguous
         const uint32_t hp = nsplit == 0 ? hp_hi : hp_lo;
         if (full) convert8<IX, true, false>(base, xbase, n, nlow, ah, al, bh, bl, dbias, dih, hp, hp, 8);
@@ -288,7 +304,9 @@ __device__ __forceinline__ void converters(const TWArgs& w, uint32_t s0, Bars br
         sts4(bt + sw_off(i, kk), bh[4 * q], bh[4 * q + 1], bh[4 * q + 2], bh[4 * q + 3]);
         sts4(bt + sw_off(64 + i, kk), bl[4 * q], bl[4 * q + 1], bl[4 * q + 2], bl[4 * q + 3]);
       }
+#ifndef WG_NO_FENCE                                 // (dev aid: timing only)
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
       tc_before();
       mbar_arrive(br.a_full(b));
     }
@@ -364,6 +382,11 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
           float* xd = reinterpret_cast<float*>(smem + OFF_X + s * XB);
           for (int e = 0; e < n * w.I; ++e) xd[e] = xs[e];
         }
+#ifdef WG_NO_LOAD                                   // dev aid: the pipeline without HBM reads (timing only)
+        mbar_arrive(br.full(s));
+        ld.next(w.rows);
+        continue;
+#endif
         mbar_expect_tx(br.full(s), tx);
         bulk_g2s(st, w.h + rb * H, (uint32_t)n * ROW_BYTES, br.full(s));
         bulk_g2s(st + KC * ROW_BYTES, w.g + rb * H, (uint32_t)n * ROW_BYTES, br.full(s));
@@ -387,6 +410,11 @@ __global__ void __launch_bounds__(NTH, 1) tc_wgrad_kernel(TWArgs w) {
         mbar_wait(br.a_full(b), (uint32_t)((mm.cg / NBUF) & 1));
         tc_after();
         const uint32_t at = s0 + OFF_BT + b * 2 * B_BYTES, bt = at + B_BYTES;
+#ifdef WG_NO_MMA                                    // dev aid: the pipeline without the MMAs (timing only)
+        mbar_arrive(br.freeb(b));
+        mm.next(w.rows);
+        continue;
+#endif
 #pragma unroll
         for (int kk = 0; kk < KC / 8; ++kk) {
           const uint32_t acc = !((mm.c % FLUSH) == 0 && kk == 0);
