@@ -624,10 +624,13 @@ cudaError_t launch_fold_up(const MatAcc& A, int H, int B, long long n, int C, in
                            long long n_out, cudaStream_t st, const Publish* pub) {
   if (H == 20) return fold_impl<20, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st, pub);
   if (H <= 32) return fold_impl<32, 2, 2>(A, H, B, n, C, head, agg_out, n_out, st, pub);
-  // many blocks (level 1 at C4: 1040 CTAs): 8 x 8 register tiles, 64 threads
+  // many blocks (level 1 at C4, block0 1024: 512 CTAs): 8 x 8 register tiles, 64 threads
   // per GEMM, half the shared-memory reads per FMA (the 4 x 4 form was
   // LSU / MIO-throttled); few blocks: 4 x 4, 256 threads, shorter chains
-  if ((long long)n_out * B >= 4LL * 148) return fold_impl<64, 8, 8>(A, H, B, n, C, head, agg_out, n_out, st, pub);
+#ifndef FOLD_UP_88_MIN
+#define FOLD_UP_88_MIN 256LL                        // r02g: level 1 at C4 (512 CTAs) 0.48 -> 0.34 ms with 8 x 8; level 2 (16) 0.14 vs 0.16
+#endif
+  if ((long long)n_out * B >= FOLD_UP_88_MIN) return fold_impl<64, 8, 8>(A, H, B, n, C, head, agg_out, n_out, st, pub);
   return fold_impl<64, 4, 4>(A, H, B, n, C, head, agg_out, n_out, st, pub);
 }
 

@@ -1,7 +1,14 @@
 """compute-sanitizer tier: memcheck, racecheck and synccheck over
 small runs of every hand-written kernel family (tests/sanitize/small_paths.py:
 the tcgen05 / TMA / mbarrier kernels, the CUDA-core levels, the CSR scan and
-the peer-exchange release/acquire kernels).  Zero reported errors."""
+the peer-exchange release/acquire kernels).  Zero reported errors.
+
+Opt-in (BPPSA_SANITIZER=1): the GPU pool closed compute-sanitizer during r02g
+(runs under it elsewhere had left GPUs needing a reset), so the default -m gpu
+tier does not start it.  All three tools ran clean on every r02a-r02f GPU
+tier (profiles/r02*_pytest_gpu.log, 360 passed each); out-of-bounds and race
+coverage otherwise comes from the parity tests' small ragged cases against the
+oracle."""
 import os
 import re
 import shutil
@@ -23,6 +30,8 @@ def _sanitizer():
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_sanitizer_clean(tool):
+    if os.environ.get("BPPSA_SANITIZER") != "1":
+        pytest.skip("compute-sanitizer tier is opt-in (BPPSA_SANITIZER=1): closed on the GPU pool since r02g")
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
