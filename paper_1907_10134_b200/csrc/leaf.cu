@@ -471,6 +471,109 @@ __global__ void __launch_bounds__(128) leaf_down_kernel(LeafArgs a, int C, const
 
 constexpr int kWarpsPerCta = 4;
 
+// L2 prefetch of the h row of step ss (a row of H <= 32 floats spans at most two 128-B lines)
+__device__ __forceinline__ void prefetch_row_l2(const float* hr, int H) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(hr));
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(hr + H - 1));
+}
+constexpr int kRowPF = 8;                            // steps of L2 prefetch ahead of the register row
+
+// Level-0 fold for the tanh RNN at H <= 32 with one CHAIN per lane (r02g).
+// leaf_up_kernel maps lanes to the H output rows, which leaves 12 of 32 lanes
+// idle at H = 20; here lane = column chain j of block (b, q) (the H chains of
+// a block on consecutive lanes share the block's h rows through L1), x = d o c
+// lives in the lane's registers and W (zero-padded to HT x HT) is read from
+// shared memory as warp-wide broadcasts.  Same arithmetic in the same order as
+// leaf_up_kernel (x_k = d_k c_k, c'_i = sum over k = 0.. of fma(x_k, W[k][i], .)),
+// so the results are bit-identical.  Output: column j of the block aggregate
+// (column-major, as launch_leaf_up); the head block's single chain is the seed.
+template <int HT>
+__global__ void __launch_bounds__(128) leaf_up_lc_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
+                                                        long long n_out, long long q0, long long nq) {
+  __shared__ __align__(16) float Ws[HT][HT];       // Ws[k][i] = W[k][i]
+  const int H = a.seg.H, B = a.seg.B;
+  for (int e = threadIdx.x; e < HT * HT; e += blockDim.x) {
+    const int k = e / HT, i = e % HT;
+    Ws[k][i] = (k < H && i < H) ? __ldg(a.W + (long long)k * H + i) : 0.f;
+  }
+  __syncthreads();
+  const long long chain = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (chain >= (long long)B * nq * H) return;
+  const int col = (int)(chain % H);
+  const long long rest = chain / H;
+  const long long q = q0 + rest % nq;
+  const int b = (int)(rest / nq);
+  const bool vec = a.seg.head && q == 0;
+  if (vec && col > 0) return;                        // the head block carries one chain: the seed
+  const long long S = a.seg.S();
+  const long long s1 = min(q * C + (long long)C, S);
+  long long s = vec ? 1 : q * C;
+  float c[HT];
+#pragma unroll
+  for (int i = 0; i < HT; ++i)
+    c[i] = vec ? ((i < H) ? __ldg(a.seed + (long long)b * H + i) : 0.f) : (i == col ? 1.f : 0.f);
+  const long long rowB = (long long)B * H;
+  float hn[HT];                                      // the next step's h row (prefetched)
+  // a whole row in HT / 4 float4 loads (rows are 16-B aligned when h is)
+  const bool full = H == HT && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
+  auto load_row = [&](long long ss) {
+    const float* hr = a.h + (long long)a.seg.time_of(ss) * rowB + (long long)b * H;
+    if (full) {
+#pragma unroll
+      for (int k4 = 0; k4 < HT / 4; ++k4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(hr) + k4);
+        hn[4 * k4] = v.x, hn[4 * k4 + 1] = v.y, hn[4 * k4 + 2] = v.z, hn[4 * k4 + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < HT; ++k) hn[k] = k < H ? __ldg(hr + k) : 0.f;
+    }
+  };
+  if (s < s1) load_row(s);
+  for (; s < s1; ++s) {
+    float x[HT];
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+      const float d = 1.f - hn[k] * hn[k];
+      x[k] = d * c[k];
+    }
+    if (s + 1 < s1) load_row(s + 1);
+    if (s + kRowPF < s1 && col == 0)                // one lane of the block prefetches
+      prefetch_row_l2(a.h + (long long)a.seg.time_of(s + kRowPF) * rowB + (long long)b * H, H);
+    float2 acc[HT / 2];
+#pragma unroll
+    for (int p = 0; p < HT / 2; ++p) acc[p] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+      const float2 xk = make_float2(x[k], x[k]);
+#pragma unroll
+      for (int p4 = 0; p4 < HT / 4; ++p4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&Ws[k][4 * p4]);
+        acc[2 * p4] = __ffma2_rn(xk, make_float2(w4.x, w4.y), acc[2 * p4]);
+        acc[2 * p4 + 1] = __ffma2_rn(xk, make_float2(w4.z, w4.w), acc[2 * p4 + 1]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < HT / 2; ++p) {
+      c[2 * p] = acc[p].x;
+      c[2 * p + 1] = acc[p].y;
+    }
+  }
+  float* dst = agg_out + ((long long)b * n_out + q) * H * H + (long long)(vec ? 0 : col) * H;
+#pragma unroll
+  for (int i = 0; i < HT; ++i)
+    if (i < H) dst[i] = c[i];
+}
+
+template <int HT>
+cudaError_t up_lc_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
+                       cudaStream_t st) {
+  const long long chains = (long long)a.seg.B * nq * a.seg.H;
+  if (chains == 0) return cudaSuccess;
+  leaf_up_lc_kernel<HT><<<(unsigned)((chains + 127) / 128), 128, 0, st>>>(a, C, agg_out, n_out, q0, nq);
+  return cudaGetLastError();
+}
+
 template <int CELL, int HT, int NC>
 cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
                     cudaStream_t st) {
@@ -486,6 +589,110 @@ cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, l
   }
   k<<<(unsigned)grid, 32 * kWarpsPerCta, smem, st>>>(a, C, agg_out, n_out, q0, nq);
   return cudaGetLastError();
+}
+
+// Level-0 walk for the tanh RNN at H <= 20 with one CHAIN per lane (r02g):
+// chain (b, q) walks its block from the carry (the seed for the head block),
+// writing the exclusive output grad_h[t(s)] = v at every slot and stepping
+// v <- W^T (d_t o v) with the lane's own registers (leaf_down_kernel spends a
+// warp per chain with 12 of 32 lanes idle at H = 20, and is issue-bound at the
+// occupancy C1-C3 give it).  Same arithmetic and order as leaf_down_kernel's
+// matvec (four partial sums over k mod 4, added in order), so the results are
+// bit-identical.  Plain scans only (no affine term, no vector-only pass).
+template <int HT>
+__global__ void __launch_bounds__(128) leaf_down_lc_kernel(LeafArgs a, int C, const float* __restrict__ carry,
+                                                          long long nblk, float* __restrict__ grad_h,
+                                                          float* __restrict__ grad_init) {
+  __shared__ __align__(16) float Ws[HT][HT];       // Ws[k][i] = W[k][i]
+  const int H = a.seg.H, B = a.seg.B;
+  for (int e = threadIdx.x; e < HT * HT; e += blockDim.x) {
+    const int k = e / HT, i = e % HT;
+    Ws[k][i] = (k < H && i < H) ? __ldg(a.W + (long long)k * H + i) : 0.f;
+  }
+  __syncthreads();
+  const long long task = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (task >= (long long)B * nblk) return;
+  const long long q = task % nblk;
+  const int b = (int)(task / nblk);
+  const long long S = a.seg.S();
+  const long long s0 = q * C, s1 = min(s0 + (long long)C, S);
+  const bool vec = a.seg.head && q == 0;
+  float v[HT];
+#pragma unroll
+  for (int i = 0; i < HT; ++i)
+    v[i] = i < H ? __ldg(vec ? a.seed + (long long)b * H + i : carry + (q + (long long)b * nblk) * H + i) : 0.f;
+  const long long rowB = (long long)B * H;
+  const bool full = H == HT && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(grad_h) & 15) == 0;
+  float hn[HT];
+  auto load_row = [&](long long ss) {
+    const float* hr = a.h + (long long)a.seg.time_of(ss) * rowB + (long long)b * H;
+    if (full) {
+#pragma unroll
+      for (int k4 = 0; k4 < HT / 4; ++k4) {
+        const float4 x4 = __ldg(reinterpret_cast<const float4*>(hr) + k4);
+        hn[4 * k4] = x4.x, hn[4 * k4 + 1] = x4.y, hn[4 * k4 + 2] = x4.z, hn[4 * k4 + 3] = x4.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < HT; ++k) hn[k] = k < H ? __ldg(hr + k) : 0.f;
+    }
+  };
+  long long s = vec ? 1 : s0;
+  if (s < s1) load_row(s);
+  for (; s < s1; ++s) {
+    const long long t = a.seg.time_of(s);
+    float* out = grad_h + t * rowB + (long long)b * H;
+    if (full) {
+#pragma unroll
+      for (int k4 = 0; k4 < HT / 4; ++k4)
+        reinterpret_cast<float4*>(out)[k4] = make_float4(v[4 * k4], v[4 * k4 + 1], v[4 * k4 + 2], v[4 * k4 + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < HT; ++i)
+        if (i < H) out[i] = v[i];
+    }
+    const bool last = s + 1 == s1;
+    const bool total = last && s1 == S && grad_init != nullptr;
+    if (last && !total) break;
+    float x[HT];
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+      const float d = 1.f - hn[k] * hn[k];
+      x[k] = d * v[k];
+    }
+    if (!last) load_row(s + 1);
+    if (s + kRowPF < s1) prefetch_row_l2(a.h + (long long)a.seg.time_of(s + kRowPF) * rowB + (long long)b * H, H);
+    float part[4][HT];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int i = 0; i < HT; ++i) part[p][i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < HT; ++k) {
+#pragma unroll
+      for (int i4 = 0; i4 < HT / 4; ++i4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&Ws[k][4 * i4]);
+        part[k % 4][4 * i4] = fmaf(w4.x, x[k], part[k % 4][4 * i4]);
+        part[k % 4][4 * i4 + 1] = fmaf(w4.y, x[k], part[k % 4][4 * i4 + 1]);
+        part[k % 4][4 * i4 + 2] = fmaf(w4.z, x[k], part[k % 4][4 * i4 + 2]);
+        part[k % 4][4 * i4 + 3] = fmaf(w4.w, x[k], part[k % 4][4 * i4 + 3]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < HT; ++i) {
+      float r = part[0][i];
+      r += part[1][i];
+      r += part[2][i];
+      r += part[3][i];
+      v[i] = r;
+    }
+    if (total) {
+#pragma unroll
+      for (int i = 0; i < HT; ++i)
+        if (i < H) grad_init[(long long)b * H + i] = v[i];
+    }
+  }
 }
 
 struct DownX {   // the affine extras of the level-0 walk
@@ -512,6 +719,10 @@ cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n
                            long long nq, cudaStream_t st) {
   const int H = a.seg.H;
   if (a.kind == BPPSA_JAC_RNN_TANH) {
+#ifndef BPPSA_LEAF_UP_ROWS                           // (the lane-per-row form, for A/B)
+    if (H <= 20) return up_lc_impl<20>(a, C, agg_out, n_out, q0, nq, st);
+    if (H <= 32) return up_lc_impl<32>(a, C, agg_out, n_out, q0, nq, st);
+#endif
     if (H == 20) return up_impl<BPPSA_JAC_RNN_TANH, 20, 20>(a, C, agg_out, n_out, q0, nq, st);
     if (H <= 32) return up_impl<BPPSA_JAC_RNN_TANH, 32, 16>(a, C, agg_out, n_out, q0, nq, st);
     return up_impl<BPPSA_JAC_RNN_TANH, 64, 8>(a, C, agg_out, n_out, q0, nq, st);
@@ -526,6 +737,14 @@ cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry, long 
   const int H = a.seg.H;
   const DownX x{e, vec_out, head_out, head_bstride};
   if (a.kind == BPPSA_JAC_RNN_TANH) {
+#ifndef BPPSA_LEAF_DOWN_ROWS                         // (the warp-per-chain form, for A/B)
+    if (H <= 20 && e == nullptr && vec_out == nullptr) {
+      const long long tasks = (long long)a.seg.B * nblk;
+      if (tasks == 0) return cudaSuccess;
+      leaf_down_lc_kernel<20><<<(unsigned)((tasks + 127) / 128), 128, 0, st>>>(a, C, carry, nblk, grad_h, grad_init);
+      return cudaGetLastError();
+    }
+#endif
     if (H == 20) return down_impl<BPPSA_JAC_RNN_TANH, 20>(a, C, carry, nblk, grad_h, grad_init, st, x);
     if (H <= 32) return down_impl<BPPSA_JAC_RNN_TANH, 32>(a, C, carry, nblk, grad_h, grad_init, st, x);
     return down_impl<BPPSA_JAC_RNN_TANH, 64>(a, C, carry, nblk, grad_h, grad_init, st, x);
