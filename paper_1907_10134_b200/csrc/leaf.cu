@@ -738,9 +738,11 @@ cudaError_t launch_leaf_down(const LeafArgs& a, int C, const float* carry, long 
   const DownX x{e, vec_out, head_out, head_bstride};
   if (a.kind == BPPSA_JAC_RNN_TANH) {
 #ifndef BPPSA_LEAF_DOWN_ROWS                         // (the warp-per-chain form, for A/B)
-    if (H <= 20 && e == nullptr && vec_out == nullptr) {
-      const long long tasks = (long long)a.seg.B * nblk;
-      if (tasks == 0) return cudaSuccess;
+    // one chain per lane pays once there are enough chains to fill the SMs
+    // (C2: 15000 at block0 32); few long chains (LINEAR mode's sequential BP,
+    // C1's 2000) keep the warp-per-chain kernel and its 8-step cp.async ring
+    const long long tasks = (long long)a.seg.B * nblk;
+    if (H <= 20 && e == nullptr && vec_out == nullptr && tasks >= 4096) {
       leaf_down_lc_kernel<20><<<(unsigned)((tasks + 127) / 128), 128, 0, st>>>(a, C, carry, nblk, grad_h, grad_init);
       return cudaGetLastError();
     }

@@ -256,6 +256,19 @@ def test_rnn_integer_family_bit_exact(lib, mode, blocks, H):
     assert np.array_equal(gi.cpu().numpy(), ref_init)
 
 
+@pytest.mark.parametrize("T,blocks", [(20000, (4, 4)), (20001, (8, 2)), (12289, (3, 16))])
+@pytest.mark.parametrize("H", [20, 17])
+def test_rnn_integer_family_bit_exact_many_chains(lib, T, blocks, H):
+    """Enough level-0 chains (B * blocks >= 4096) for the one-chain-per-lane
+    walk (leaf_down_lc_kernel) and fold (leaf_up_lc_kernel), H = 20 (whole-row
+    vector loads) and 17 (scalar tail); ragged last blocks."""
+    f = W.int_rnn_family(T, 3, H, seed=T + H)
+    ref, ref_init = bp.bp_rnn(f["h"], f["W_hh"], f["g"])
+    grad, gi = run_rnn(lib, f["h"], f["W_hh"], f["g"], block0=blocks[0], block=blocks[1])
+    assert np.array_equal(grad.cpu().numpy(), ref)
+    assert np.array_equal(gi.cpu().numpy(), ref_init)
+
+
 def test_rnn_closed_forms(lib):
     """P4: W = 0 -> grad_h[t<T-1] = 0 exactly; h = 0 with an integer W -> powers of W^T."""
     T, B, H = 50, 2, 20
