@@ -766,7 +766,24 @@ def sweep_csr(api, pk=None):
         t_plan = time.perf_counter() - t0
         ws = api.workspace(plan.workspace_size(16, chain.batched))
         grads = [torch.empty((16, d), device="cuda") for d in plan.dims]
-        ms = _time(lambda: api.csr_scan(plan, chain.data, chain.batched, seed, grads=grads, ws=ws), reps=10)
+        run = lambda: api.csr_scan(plan, chain.data, chain.batched, seed, grads=grads, ws=ws)  # noqa: E731
+        ms_eager = _time(run, reps=10)
+        ms_graph = None                         # the launch-bound chains (44-59 kernels): CUDA-graph replay
+        try:
+            gr = torch.cuda.CUDAGraph()
+            s_ = torch.cuda.Stream()
+            s_.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_):
+                run()
+                torch.cuda.synchronize()
+                with torch.cuda.graph(gr, stream=s_, capture_error_mode="relaxed"):
+                    run()
+            torch.cuda.synchronize()
+            ms_graph = _time(gr.replay, reps=10)
+            del gr
+        except Exception as ex:  # noqa: BLE001
+            ms_graph = f"capture failed: {ex}"[:120]
+        ms = ms_graph if not isinstance(ms_graph, (str, type(None))) else ms_eager
         info = plan.info()
         steps = api.csr_plan_steps(plan)       # fig:prune_symbolic static FLOP analysis
         scan_st = [x for x in steps if x["phase"] != "bp"]
@@ -783,7 +800,9 @@ def sweep_csr(api, pk=None):
                     "achieved_gbs": round(c_bytes / (ms * 1e-3) / 1e9, 1), "peak_gbs": hbm,
                     "frac": round(c_bytes / (ms * 1e-3) / 1e9 / hbm, 4)}
         res[f"u{sched[0]}_dl{sched[1]}"] = {
-            "scan_ms": round(ms, 4), "plan_build_s": round(t_plan, 2), "roofline": res_roof,
+            "scan_ms": round(ms, 4), "scan_ms_eager": round(ms_eager, 4),
+            "scan_ms_graph": ms_graph if isinstance(ms_graph, (str, type(None))) else round(ms_graph, 4),
+            "plan_build_s": round(t_plan, 2), "roofline": res_roof,
             "contributions": info["contributions"], "spmv_nnz": info["spmv_nnz"],
             "kernels": info["kernels"], "ws_GB": round(ws.numel() / 1e9, 3),
             "flops_per_sample": {"bppsa_total": sum(x["flops"] for x in scan_st),
