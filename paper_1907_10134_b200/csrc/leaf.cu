@@ -487,9 +487,11 @@ constexpr int kRowPF = 8;                            // steps of L2 prefetch ahe
 // leaf_up_kernel (x_k = d_k c_k, c'_i = sum over k = 0.. of fma(x_k, W[k][i], .)),
 // so the results are bit-identical.  Output: column j of the block aggregate
 // (column-major, as launch_leaf_up); the head block's single chain is the seed.
-template <int HT>
+template <int HT, int NCH>
 __global__ void __launch_bounds__(128) leaf_up_lc_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
                                                         long long n_out, long long q0, long long nq) {
+  // NCH chains per lane (cols jl, jl + L, ..., L = ceil(H / NCH) lanes per
+  // block): each shared-memory W load feeds NCH chains
   __shared__ __align__(16) float Ws[HT][HT];       // Ws[k][i] = W[k][i]
   const int H = a.seg.H, B = a.seg.B;
   for (int e = threadIdx.x; e < HT * HT; e += blockDim.x) {
@@ -497,21 +499,24 @@ __global__ void __launch_bounds__(128) leaf_up_lc_kernel(LeafArgs a, int C, floa
     Ws[k][i] = (k < H && i < H) ? __ldg(a.W + (long long)k * H + i) : 0.f;
   }
   __syncthreads();
-  const long long chain = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (chain >= (long long)B * nq * H) return;
-  const int col = (int)(chain % H);
-  const long long rest = chain / H;
+  const int L = (H + NCH - 1) / NCH;
+  const long long task = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (task >= (long long)B * nq * L) return;
+  const int jl = (int)(task % L);
+  const long long rest = task / L;
   const long long q = q0 + rest % nq;
   const int b = (int)(rest / nq);
   const bool vec = a.seg.head && q == 0;
-  if (vec && col > 0) return;                        // the head block carries one chain: the seed
+  if (vec && jl > 0) return;                         // the head block carries one chain: the seed
   const long long S = a.seg.S();
   const long long s1 = min(q * C + (long long)C, S);
   long long s = vec ? 1 : q * C;
-  float c[HT];
+  float c[NCH][HT];
 #pragma unroll
-  for (int i = 0; i < HT; ++i)
-    c[i] = vec ? ((i < H) ? __ldg(a.seed + (long long)b * H + i) : 0.f) : (i == col ? 1.f : 0.f);
+  for (int u = 0; u < NCH; ++u)
+#pragma unroll
+    for (int i = 0; i < HT; ++i)
+      c[u][i] = vec ? ((u == 0 && i < H) ? __ldg(a.seed + (long long)b * H + i) : 0.f) : (i == jl + u * L ? 1.f : 0.f);
   const long long rowB = (long long)B * H;
   float hn[HT];                                      // the next step's h row (prefetched)
   // a whole row in HT / 4 float4 loads (rows are 16-B aligned when h is)
@@ -531,38 +536,60 @@ __global__ void __launch_bounds__(128) leaf_up_lc_kernel(LeafArgs a, int C, floa
   };
   if (s < s1) load_row(s);
   for (; s < s1; ++s) {
-    float x[HT];
+    float x[NCH][HT];
 #pragma unroll
     for (int k = 0; k < HT; ++k) {
       const float d = 1.f - hn[k] * hn[k];
-      x[k] = d * c[k];
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) x[u][k] = d * c[u][k];
     }
     if (s + 1 < s1) load_row(s + 1);
-    if (s + kRowPF < s1 && col == 0)                // one lane of the block prefetches
+    if (s + kRowPF < s1 && jl == 0)                 // one lane of the block prefetches
       prefetch_row_l2(a.h + (long long)a.seg.time_of(s + kRowPF) * rowB + (long long)b * H, H);
-    float2 acc[HT / 2];
+    float2 acc[NCH][HT / 2];
 #pragma unroll
-    for (int p = 0; p < HT / 2; ++p) acc[p] = make_float2(0.f, 0.f);
+    for (int u = 0; u < NCH; ++u)
+#pragma unroll
+      for (int p = 0; p < HT / 2; ++p) acc[u][p] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < HT; ++k) {
-      const float2 xk = make_float2(x[k], x[k]);
 #pragma unroll
       for (int p4 = 0; p4 < HT / 4; ++p4) {
         const float4 w4 = *reinterpret_cast<const float4*>(&Ws[k][4 * p4]);
-        acc[2 * p4] = __ffma2_rn(xk, make_float2(w4.x, w4.y), acc[2 * p4]);
-        acc[2 * p4 + 1] = __ffma2_rn(xk, make_float2(w4.z, w4.w), acc[2 * p4 + 1]);
+#pragma unroll
+        for (int u = 0; u < NCH; ++u) {
+          const float2 xk = make_float2(x[u][k], x[u][k]);
+          acc[u][2 * p4] = __ffma2_rn(xk, make_float2(w4.x, w4.y), acc[u][2 * p4]);
+          acc[u][2 * p4 + 1] = __ffma2_rn(xk, make_float2(w4.z, w4.w), acc[u][2 * p4 + 1]);
+        }
       }
     }
 #pragma unroll
-    for (int p = 0; p < HT / 2; ++p) {
-      c[2 * p] = acc[p].x;
-      c[2 * p + 1] = acc[p].y;
-    }
-  }
-  float* dst = agg_out + ((long long)b * n_out + q) * H * H + (long long)(vec ? 0 : col) * H;
+    for (int u = 0; u < NCH; ++u)
 #pragma unroll
-  for (int i = 0; i < HT; ++i)
-    if (i < H) dst[i] = c[i];
+      for (int p = 0; p < HT / 2; ++p) {
+        c[u][2 * p] = acc[u][p].x;
+        c[u][2 * p + 1] = acc[u][p].y;
+      }
+  }
+#pragma unroll
+  for (int u = 0; u < NCH; ++u) {
+    const int col = vec ? 0 : jl + u * L;
+    if ((vec && u > 0) || col >= H) continue;
+    float* dst = agg_out + ((long long)b * n_out + q) * H * H + (long long)col * H;
+#pragma unroll
+    for (int i = 0; i < HT; ++i)
+      if (i < H) dst[i] = c[u][i];
+  }
+}
+
+template <int HT, int NCH>
+cudaError_t up_lc_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
+                       cudaStream_t st) {
+  const long long tasks = (long long)a.seg.B * nq * ((a.seg.H + NCH - 1) / NCH);
+  if (tasks == 0) return cudaSuccess;
+  leaf_up_lc_kernel<HT, NCH><<<(unsigned)((tasks + 127) / 128), 128, 0, st>>>(a, C, agg_out, n_out, q0, nq);
+  return cudaGetLastError();
 }
 
 // The GRU form (H <= 20): the J^T of eqn:gru_jcb needs three matrix-vector
@@ -642,14 +669,6 @@ __global__ void __launch_bounds__(128) leaf_up_lc_gru_kernel(LeafArgs a, int C, 
     if (i < H) dst[i] = c[i];
 }
 
-template <int HT>
-cudaError_t up_lc_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
-                       cudaStream_t st) {
-  const long long chains = (long long)a.seg.B * nq * a.seg.H;
-  if (chains == 0) return cudaSuccess;
-  leaf_up_lc_kernel<HT><<<(unsigned)((chains + 127) / 128), 128, 0, st>>>(a, C, agg_out, n_out, q0, nq);
-  return cudaGetLastError();
-}
 
 template <int CELL, int HT, int NC>
 cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
@@ -797,8 +816,11 @@ cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n
   const int H = a.seg.H;
   if (a.kind == BPPSA_JAC_RNN_TANH) {
 #ifndef BPPSA_LEAF_UP_ROWS                           // (the lane-per-row form, for A/B)
-    if (H <= 20) return up_lc_impl<20>(a, C, agg_out, n_out, q0, nq, st);
-    if (H <= 32) return up_lc_impl<32>(a, C, agg_out, n_out, q0, nq, st);
+#ifndef BPPSA_LC_NCH
+#define BPPSA_LC_NCH 2
+#endif
+    if (H <= 20) return up_lc_impl<20, BPPSA_LC_NCH>(a, C, agg_out, n_out, q0, nq, st);
+    if (H <= 32) return up_lc_impl<32, 1>(a, C, agg_out, n_out, q0, nq, st);
 #endif
     if (H == 20) return up_impl<BPPSA_JAC_RNN_TANH, 20, 20>(a, C, agg_out, n_out, q0, nq, st);
     if (H <= 32) return up_impl<BPPSA_JAC_RNN_TANH, 32, 16>(a, C, agg_out, n_out, q0, nq, st);
