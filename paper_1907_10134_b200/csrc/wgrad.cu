@@ -12,6 +12,8 @@
 // (the next stage's operands are loaded while the current one is consumed).
 // Partial tiles go to the workspace and a second kernel sums the parts in a
 // fixed order — deterministic, no float atomics, round-to-nearest FFMA.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bppsa {
@@ -248,7 +250,165 @@ cudaError_t reduce_rnn(const float* ws, long long P, int H, int I, float* dW_ih,
   return cudaGetLastError();
 }
 
+// RNN, H <= 20, I + 1 <= 4 (configs 1-2; r02i): the part's rows go through a
+// cp.async ring of 64-row stages (h, grad_h and h_prev rows as they lie in
+// memory, several stages in flight: the tile kernel above keeps one 32-row
+// stage in flight in registers and sat at 25 % occupancy waiting on loads).
+// Thread = (4 x 4 output tile, row group): ceil(H/4)^2 tiles x SG groups; each
+// forms delta = (1 - h^2) g for its four rows of a on the fly from the staged
+// rows, the tile of column block 0 also the x / bias columns; the row groups
+// are summed in a fixed order at the end (deterministic).
+constexpr int SM_H = 20, SM_TL = SM_H / 4, SM_TILES = SM_TL * SM_TL, SM_SG = 10, SM_NT = 256;
+constexpr int SM_RS = 64, SM_NS = 4, SM_EMAX = 4;
+constexpr int SM_STAGE = 3 * SM_RS * SM_H + SM_RS * SM_EMAX;   // floats: h | g | h_prev | x rows
+__global__ void __launch_bounds__(SM_NT) wgrad_rnn_small_kernel(WArgs w, float* __restrict__ ws) {
+  extern __shared__ __align__(16) float sm[];
+  const int H = w.H, I = w.I, E = w.E;
+  const int part = blockIdx.x, tid = threadIdx.x;
+  const long long r0 = (long long)part * w.rows_per_part;
+  const long long r1 = min(r0 + w.rows_per_part, w.rows);
+  const int nst = (int)((r1 - r0 + SM_RS - 1) / SM_RS);
+  // stage loader: 16-byte cp.async when the rows are 16-byte aligned (H % 4 == 0
+  // and aligned bases: the rows of a stage are one contiguous run per array),
+  // else 4-byte copies
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool v16 = H % 4 == 0 && al16(w.h) && al16(w.g) && (w.h_init == nullptr || al16(w.h_init));
+  const bool x16 = I > 0 && al16(w.x) && (SM_RS * I) % 4 == 0;
+  auto cp4 = [](float* d, const float* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(d)), "l"(g)
+                 : "memory");
+  };
+  auto cp16 = [](float* d, const float* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(d)), "l"(g)
+                 : "memory");
+  };
+  auto load = [&](int k) {
+    if (k < nst) {
+      float* dst = sm + (k % SM_NS) * SM_STAGE;
+      const long long rb = r0 + (long long)k * SM_RS;
+      const int n = (int)min((long long)SM_RS, r1 - rb);
+      const int step = v16 ? 4 : 1;
+      for (int e = tid * step; e < n * H; e += SM_NT * step) {
+        const long long row = rb + e / H;
+        const int c = e % H;
+        const float* hp = row >= w.B ? w.h + (row - w.B) * H + c : (w.h_init ? w.h_init + row * H + c : nullptr);
+        if (v16) {
+          cp16(dst + e, w.h + rb * H + e);
+          cp16(dst + SM_RS * H + e, w.g + rb * H + e);
+          if (hp) cp16(dst + 2 * SM_RS * H + e, hp);
+          else *reinterpret_cast<float4*>(dst + 2 * SM_RS * H + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          cp4(dst + e, w.h + rb * H + e);
+          cp4(dst + SM_RS * H + e, w.g + rb * H + e);
+          if (hp) cp4(dst + 2 * SM_RS * H + e, hp);
+          else dst[2 * SM_RS * H + e] = 0.f;
+        }
+      }
+      if (x16 && n == SM_RS && ((rb * I) & 3) == 0) {   // (parts start anywhere: check the stage's x offset)
+        for (int e = 4 * tid; e < n * I; e += 4 * SM_NT) cp16(dst + 3 * SM_RS * H + e, w.x + rb * I + e);
+      } else {
+        for (int e = tid; e < n * I; e += SM_NT) cp4(dst + 3 * SM_RS * H + e, w.x + rb * I + e);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");   // one group per stage, empty or not
+  };
+  const int tile = tid % SM_TILES, rg = tid / SM_TILES;   // rg < SM_SG for the working threads
+  const int ti = tile / SM_TL, tj = tile % SM_TL;
+  const bool work = rg < SM_SG && 4 * ti < H && 4 * tj < H;
+  float acc[4][4], eacc[4][SM_EMAX];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+#pragma unroll
+    for (int y = 0; y < SM_EMAX; ++y) eacc[x][y] = 0.f;
+  }
+  for (int k = 0; k < SM_NS - 1; ++k) load(k);
+  for (int k = 0; k < nst; ++k) {
+    load(k + SM_NS - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SM_NS - 1) : "memory");
+    __syncthreads();
+    const float* st = sm + (k % SM_NS) * SM_STAGE;
+    const int n = (int)min((long long)SM_RS, r1 - (r0 + (long long)k * SM_RS));
+    if (work) {
+      for (int r = rg; r < n; r += SM_SG) {
+        float dl[4], u[4];
+        if (H == SM_H) {                              // whole 4-column groups: 16-byte shared loads
+          const float4 h4 = *reinterpret_cast<const float4*>(st + r * H + 4 * ti);
+          const float4 g4 = *reinterpret_cast<const float4*>(st + SM_RS * H + r * H + 4 * ti);
+          const float4 u4 = *reinterpret_cast<const float4*>(st + 2 * SM_RS * H + r * H + 4 * tj);
+          dl[0] = (1.f - h4.x * h4.x) * g4.x, dl[1] = (1.f - h4.y * h4.y) * g4.y;
+          dl[2] = (1.f - h4.z * h4.z) * g4.z, dl[3] = (1.f - h4.w * h4.w) * g4.w;
+          u[0] = u4.x, u[1] = u4.y, u[2] = u4.z, u[3] = u4.w;
+        } else {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int a = 4 * ti + x;
+            const float hv = a < H ? st[r * H + a] : 0.f, gv = a < H ? st[SM_RS * H + r * H + a] : 0.f;
+            dl[x] = (1.f - hv * hv) * gv;
+          }
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            const int c = 4 * tj + y;
+            u[y] = c < H ? st[2 * SM_RS * H + r * H + c] : 0.f;
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(dl[x], u[y], acc[x][y]);
+        if (tj == 0) {
+#pragma unroll
+          for (int y = 0; y < SM_EMAX; ++y) {
+            const float ev = y < I ? st[3 * SM_RS * H + r * I + y] : (y == I ? 1.f : 0.f);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) eacc[x][y] = fmaf(dl[x], ev, eacc[x][y]);
+          }
+        }
+      }
+    }
+    __syncthreads();                                   // the stage is refilled next
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  // fixed-order sum over the row groups through shared memory
+  float* red = sm;                                     // [SM_SG][SM_TILES][16 + 4 SM_EMAX]
+  constexpr int RW = 16 + 4 * SM_EMAX;
+  if (rg < SM_SG) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+#pragma unroll
+      for (int y = 0; y < 4; ++y) red[(rg * SM_TILES + tile) * RW + 4 * x + y] = acc[x][y];
+#pragma unroll
+      for (int y = 0; y < SM_EMAX; ++y) red[(rg * SM_TILES + tile) * RW + 16 + SM_EMAX * x + y] = eacc[x][y];
+    }
+  }
+  __syncthreads();
+  const int NB = H + E;
+  float* dst = ws + (long long)part * H * NB;
+  for (int o = tid; o < SM_TILES * RW; o += SM_NT) {
+    const int t = o / RW, j = o % RW, oi = t / SM_TL, oj = t % SM_TL;
+    float sum = 0.f;
+    for (int g2 = 0; g2 < SM_SG; ++g2) sum += red[(g2 * SM_TILES + t) * RW + j];
+    if (j < 16) {
+      const int a = 4 * oi + j / 4, c = 4 * oj + j % 4;
+      if (a < H && c < H) dst[(long long)a * NB + c] = sum;
+    } else if (oj == 0) {
+      const int a = 4 * oi + (j - 16) / SM_EMAX, y = (j - 16) % SM_EMAX;
+      if (a < H && y < E) dst[(long long)a * NB + H + y] = sum;
+    }
+  }
+}
+
 cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream_t st) {
+  if (w.kind == BPPSA_JAC_RNN_TANH && w.H <= SM_H && w.E <= SM_EMAX) {
+    const size_t smem = (size_t)SM_NS * SM_STAGE * sizeof(float);
+    static_assert((size_t)SM_SG * SM_TILES * (16 + 4 * SM_EMAX) <= (size_t)SM_NS * SM_STAGE, "reduction fits");
+    cudaError_t e = cudaFuncSetAttribute(wgrad_rnn_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    wgrad_rnn_small_kernel<<<(unsigned)nparts, SM_NT, smem, st>>>(w, ws);
+    return cudaGetLastError();
+  }
   if (w.H <= 32 && w.E <= 16 && 32 * w.E <= WT<32, 16>::NEA * WT<32, 16>::NT) {
     dim3 grid((unsigned)nparts, (unsigned)((w.NA + 31) / 32));
     wgrad_partial_kernel<32, 16><<<grid, WT<32, 16>::NT, 0, st>>>(w, ws);
@@ -270,8 +430,15 @@ cudaError_t launch_wgrad_rnn(int T, int B, int H, int I, const float* x, const f
   w.T = T; w.B = B; w.H = H; w.I = I; w.kind = BPPSA_JAC_RNN_TANH;
   w.x = x; w.h = h; w.h_init = h_init; w.g = grad_h;
   w.rows = (long long)T * B;
-  w.rows_per_part = (w.rows + nparts - 1) / nparts;
   w.NA = H; w.E = I + 1;
+  // the staged small-H kernel runs fewer, longer parts (three per SM: each
+  // keeps its cp.async ring busy, and the fixed-order reduction has fewer
+  // slabs); still a function of the row count only
+#ifndef WG_SMALL_PARTS
+#define WG_SMALL_PARTS 444LL
+#endif
+  if (H <= SM_H && w.E <= SM_EMAX) nparts = std::min(nparts, (long long)WG_SMALL_PARTS);
+  w.rows_per_part = (w.rows + nparts - 1) / nparts;
   cudaError_t e = run_partials(w, ws, nparts, st);
   if (e != cudaSuccess) return e;
   return reduce_rnn(ws, nparts, H, I, dW_ih, dW_hh, db, st);
