@@ -399,7 +399,140 @@ __global__ void __launch_bounds__(SM_NT) wgrad_rnn_small_kernel(WArgs w, float* 
   }
 }
 
+// GRU, H <= 20, I + 1 <= 16 (config 3; r02i): the same staged scheme.  A =
+// [dR | dZ | dN | dM] (4H rows) from the staged g, z, n, h_prev, r, M rows;
+// U = [h_prev | x | 1] (H + I + 1 <= 36 columns); 4 x 4 tiles over 4H x 36,
+// two row groups; the gate formulas are valA's.
+constexpr int SG_H = 20, SG_RS = 32, SG_NS = 3, SG_UC = 36, SG_XM = 16, SG_NT = 384, SG_G = 2;
+constexpr int SG_TA = 4 * SG_H / 4, SG_TU = SG_UC / 4, SG_TILES = SG_TA * SG_TU;   // 20 x 9 tiles
+constexpr int SG_STAGE = 6 * SG_RS * SG_H + SG_RS * SG_XM;   // g | z | n | hp | r | M rows, x rows
+__global__ void __launch_bounds__(SG_NT) wgrad_gru_small_kernel(WArgs w, float* __restrict__ ws) {
+  extern __shared__ __align__(16) float sm[];
+  const int H = w.H, I = w.I, E = w.E;
+  const int part = blockIdx.x, tid = threadIdx.x;
+  const long long r0 = (long long)part * w.rows_per_part;
+  const long long r1 = min(r0 + w.rows_per_part, w.rows);
+  const int nst = (int)((r1 - r0 + SG_RS - 1) / SG_RS);
+  const float* arr[6] = {w.g, w.z, w.n, w.hp, w.r, w.M};
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  bool v16 = H % 4 == 0;
+#pragma unroll
+  for (int v = 0; v < 6; ++v) v16 = v16 && al16(arr[v]);
+  const bool x16 = I > 0 && I % 4 == 0 && al16(w.x);
+  auto load = [&](int k) {
+    if (k < nst) {
+      float* dst = sm + (k % SG_NS) * SG_STAGE;
+      const long long rb = r0 + (long long)k * SG_RS;
+      const int n = (int)min((long long)SG_RS, r1 - rb);
+      if (v16) {                                       // 16-byte copies (rows of H = 20 floats are aligned)
+        for (int e = 4 * tid; e < n * H; e += 4 * SG_NT)
+#pragma unroll
+          for (int v = 0; v < 6; ++v)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(dst + v * SG_RS * H + e)),
+                         "l"(arr[v] + rb * H + e) : "memory");
+      } else {
+        for (int e = tid; e < n * H; e += SG_NT)
+#pragma unroll
+          for (int v = 0; v < 6; ++v)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(dst + v * SG_RS * H + e)),
+                         "l"(arr[v] + rb * H + e) : "memory");
+      }
+      if (x16) {                                       // x rows of I % 4 == 0 floats: I / 4 chunks per row
+        const int q = I / 4;
+        for (int e = tid; e < n * q; e += SG_NT)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                           (unsigned)__cvta_generic_to_shared(dst + 6 * SG_RS * H + (e / q) * SG_XM + 4 * (e % q))),
+                       "l"(w.x + (rb + e / q) * I + 4 * (e % q)) : "memory");
+      } else {
+        for (int e = tid; e < n * I; e += SG_NT)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                           (unsigned)__cvta_generic_to_shared(dst + 6 * SG_RS * H + (e / I) * SG_XM + e % I)),
+                       "l"(w.x + rb * I + e) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int tile = tid % SG_TILES, rg = tid / SG_TILES;   // rg < SG_G for the working threads
+  const int ta = tile / SG_TU, tu = tile % SG_TU;
+  const bool work = rg < SG_G && 4 * ta < 4 * H && 4 * tu < H + E;
+  float acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+  for (int k = 0; k < SG_NS - 1; ++k) load(k);
+  for (int k = 0; k < nst; ++k) {
+    load(k + SG_NS - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SG_NS - 1) : "memory");
+    __syncthreads();
+    const float* st = sm + (k % SG_NS) * SG_STAGE;
+    const int n = (int)min((long long)SG_RS, r1 - (r0 + (long long)k * SG_RS));
+    float* dA = sm + SG_NS * SG_STAGE;                 // the stage's A rows [row][4H], formed once
+    for (int e = tid; e < n * 4 * H; e += SG_NT) {
+      const int r = e / (4 * H), a = e % (4 * H), gt = a / H, o = r * H + a % H;
+      const float g = st[o], z = st[SG_RS * H + o], nn = st[2 * SG_RS * H + o];
+      const float hp = st[3 * SG_RS * H + o], rr = st[4 * SG_RS * H + o], M = st[5 * SG_RS * H + o];
+      const float dN = g * (1.f - z) * (1.f - nn * nn);
+      dA[e] = gt == 2 ? dN : gt == 1 ? g * (hp - nn) * z * (1.f - z) : gt == 0 ? dN * M * rr * (1.f - rr) : dN * rr;
+    }
+    float* dU = dA + SG_RS * 4 * SG_H;                 // the stage's U rows [row][36]: h_prev | x | 1 | 0
+    for (int e = tid; e < n * SG_UC; e += SG_NT) {
+      const int r = e / SG_UC, c = e % SG_UC;
+      dU[e] = c < H ? st[3 * SG_RS * H + r * H + c]
+                    : (c < H + I ? st[6 * SG_RS * H + r * SG_XM + (c - H)] : (c == H + I ? 1.f : 0.f));
+    }
+    __syncthreads();
+    if (work) {
+      for (int r = rg; r < n; r += SG_G) {
+        float da[4], u[4];
+        {
+          const float4 a4 = *reinterpret_cast<const float4*>(dA + r * 4 * H + 4 * ta);
+          da[0] = a4.x, da[1] = a4.y, da[2] = a4.z, da[3] = a4.w;
+        }
+        {
+          const float4 u4 = *reinterpret_cast<const float4*>(dU + r * SG_UC + 4 * tu);
+          u[0] = u4.x, u[1] = u4.y, u[2] = u4.z, u[3] = u4.w;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(da[x], u[y], acc[x][y]);
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  float* red = sm;                                     // [SG_G][SG_TILES][16]
+  if (rg < SG_G) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) red[(rg * SG_TILES + tile) * 16 + 4 * x + y] = acc[x][y];
+  }
+  __syncthreads();
+  const int NB = H + E;
+  float* dst = ws + (long long)part * w.NA * NB;
+  for (int o = tid; o < SG_TILES * 16; o += SG_NT) {
+    const int t = o / 16, j = o % 16, oa = t / SG_TU, ou = t % SG_TU;
+    float sum = 0.f;
+    for (int g2 = 0; g2 < SG_G; ++g2) sum += red[(g2 * SG_TILES + t) * 16 + j];
+    const int a = 4 * oa + j / 4, c = 4 * ou + j % 4;
+    if (a < w.NA && c < NB) dst[(long long)a * NB + c] = sum;
+  }
+}
+
 cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream_t st) {
+  if (w.kind == BPPSA_JAC_GRU && w.H == SG_H && w.E <= SG_XM + 1 && w.I <= SG_XM && w.H + w.E <= SG_UC) {
+    const size_t smem = (size_t)(SG_NS * SG_STAGE + SG_RS * (4 * SG_H + SG_UC)) * sizeof(float);
+    static_assert((size_t)SG_G * SG_TILES * 16 <= (size_t)SG_NS * SG_STAGE, "reduction fits");
+    cudaError_t e = cudaFuncSetAttribute(wgrad_gru_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    wgrad_gru_small_kernel<<<(unsigned)nparts, SG_NT, smem, st>>>(w, ws);
+    return cudaGetLastError();
+  }
   if (w.kind == BPPSA_JAC_RNN_TANH && w.H <= SM_H && w.E <= SM_EMAX) {
     const size_t smem = (size_t)SM_NS * SM_STAGE * sizeof(float);
     static_assert((size_t)SM_SG * SM_TILES * (16 + 4 * SM_EMAX) <= (size_t)SM_NS * SM_STAGE, "reduction fits");
@@ -457,8 +590,9 @@ cudaError_t launch_wgrad_gru(int T, int B, int H, int I, const float* x, const f
   w.T = T; w.B = B; w.H = H; w.I = I; w.kind = BPPSA_JAC_GRU;
   w.x = x; w.g = grad_h; w.hp = hp; w.r = r; w.z = z; w.n = n; w.M = M;
   w.rows = (long long)T * B;
-  w.rows_per_part = (w.rows + nparts - 1) / nparts;
   w.NA = 4 * H; w.E = I + 1;
+  if (H == SG_H && w.E <= SG_XM + 1 && H + w.E <= SG_UC) nparts = std::min(nparts, (long long)WG_SMALL_PARTS);
+  w.rows_per_part = (w.rows + nparts - 1) / nparts;
   cudaError_t e = run_partials(w, ws, nparts, st);
   if (e != cudaSuccess) return e;
   const int total = 3 * H * H + 3 * H * I + 6 * H;
