@@ -599,7 +599,7 @@ cudaError_t up_lc_impl(const LeafArgs& a, int C, float* agg_out, long long n_out
 // by the block's lanes), then the products with the three W in shared memory.
 // Same arithmetic and order as leaf_up_kernel<GRU> (load_coef; v = r, n, z
 // outer, k inner; then fma(z, c, .)).
-template <int HT>
+template <int HT, int NCH>
 __global__ void __launch_bounds__(128) leaf_up_lc_gru_kernel(LeafArgs a, int C, float* __restrict__ agg_out,
                                                             long long n_out, long long q0, long long nq) {
   __shared__ __align__(16) float Ws[3][HT][HT];    // [v][k][i] = W_hh3[(vrow + k) H + i], vrow = 0, 2H, H
@@ -610,65 +610,83 @@ __global__ void __launch_bounds__(128) leaf_up_lc_gru_kernel(LeafArgs a, int C, 
     Ws[v][k][i] = (k < H && i < H) ? __ldg(a.W + (long long)(vrow + k) * H + i) : 0.f;
   }
   __syncthreads();
-  const long long chain = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (chain >= (long long)B * nq * H) return;
-  const int col = (int)(chain % H);
-  const long long rest = chain / H;
+  // NCH chains per lane (cols jl, jl + L, ..., L = ceil(H / NCH)): the step's
+  // gate coefficients and every W load serve all of them
+  const int L = (H + NCH - 1) / NCH;
+  const long long task = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (task >= (long long)B * nq * L) return;
+  const int jl = (int)(task % L);
+  const long long rest = task / L;
   const long long q = q0 + rest % nq;
   const int b = (int)(rest / nq);
   const bool vec = a.seg.head && q == 0;
-  if (vec && col > 0) return;
+  if (vec && jl > 0) return;
   const long long S = a.seg.S();
   const long long s1 = min(q * C + (long long)C, S);
   long long s = vec ? 1 : q * C;
-  float c[HT];
+  float c[NCH][HT];
 #pragma unroll
-  for (int i = 0; i < HT; ++i)
-    c[i] = vec ? ((i < H) ? __ldg(a.seed + (long long)b * H + i) : 0.f) : (i == col ? 1.f : 0.f);
+  for (int u = 0; u < NCH; ++u)
+#pragma unroll
+    for (int i = 0; i < HT; ++i)
+      c[u][i] = vec ? ((u == 0 && i < H) ? __ldg(a.seed + (long long)b * H + i) : 0.f) : (i == jl + u * L ? 1.f : 0.f);
   const long long rowB = (long long)B * H;
   for (; s < s1; ++s) {
     const long long off = (long long)a.seg.time_of(s) * rowB + (long long)b * H;
-    if (s + kRowPF < s1 && col == 0) {
+    if (s + kRowPF < s1 && jl == 0) {
       const long long offp = (long long)a.seg.time_of(s + kRowPF) * rowB + (long long)b * H;
       prefetch_row_l2(a.r + offp, H), prefetch_row_l2(a.z + offp, H), prefetch_row_l2(a.n + offp, H);
       prefetch_row_l2(a.M + offp, H), prefetch_row_l2(a.hp + offp, H);
     }
-    float x[3][HT], zc[HT];
+    float cf[4][HT];
 #pragma unroll
     for (int k = 0; k < HT; ++k) {
-      const Coef<BPPSA_JAC_GRU> cf = load_coef<BPPSA_JAC_GRU>(a, off + k, k < H);
-      x[0][k] = cf.c[0] * c[k];
-      x[1][k] = cf.c[1] * c[k];
-      x[2][k] = cf.c[2] * c[k];
-      zc[k] = cf.c[3];
+      const Coef<BPPSA_JAC_GRU> co = load_coef<BPPSA_JAC_GRU>(a, off + k, k < H);
+      cf[0][k] = co.c[0], cf[1][k] = co.c[1], cf[2][k] = co.c[2], cf[3][k] = co.c[3];
     }
-    float2 acc[HT / 2];
+    float2 acc[NCH][HT / 2];
 #pragma unroll
-    for (int p2 = 0; p2 < HT / 2; ++p2) acc[p2] = make_float2(0.f, 0.f);
+    for (int u = 0; u < NCH; ++u)
+#pragma unroll
+      for (int p2 = 0; p2 < HT / 2; ++p2) acc[u][p2] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int v = 0; v < 3; ++v)
 #pragma unroll
       for (int k = 0; k < HT; ++k) {
-        const float2 xk = make_float2(x[v][k], x[v][k]);
+        float2 xk[NCH];
+#pragma unroll
+        for (int u = 0; u < NCH; ++u) {
+          const float xv = cf[v][k] * c[u][k];
+          xk[u] = make_float2(xv, xv);
+        }
 #pragma unroll
         for (int p4 = 0; p4 < HT / 4; ++p4) {
           const float4 w4 = *reinterpret_cast<const float4*>(&Ws[v][k][4 * p4]);
-          acc[2 * p4] = __ffma2_rn(xk, make_float2(w4.x, w4.y), acc[2 * p4]);
-          acc[2 * p4 + 1] = __ffma2_rn(xk, make_float2(w4.z, w4.w), acc[2 * p4 + 1]);
+#pragma unroll
+          for (int u = 0; u < NCH; ++u) {
+            acc[u][2 * p4] = __ffma2_rn(xk[u], make_float2(w4.x, w4.y), acc[u][2 * p4]);
+            acc[u][2 * p4 + 1] = __ffma2_rn(xk[u], make_float2(w4.z, w4.w), acc[u][2 * p4 + 1]);
+          }
         }
       }
 #pragma unroll
-    for (int p2 = 0; p2 < HT / 2; ++p2) {
-      c[2 * p2] = fmaf(zc[2 * p2], c[2 * p2], acc[p2].x);
-      c[2 * p2 + 1] = fmaf(zc[2 * p2 + 1], c[2 * p2 + 1], acc[p2].y);
-    }
-  }
-  float* dst = agg_out + ((long long)b * n_out + q) * H * H + (long long)(vec ? 0 : col) * H;
+    for (int u = 0; u < NCH; ++u)
 #pragma unroll
-  for (int i = 0; i < HT; ++i)
-    if (i < H) dst[i] = c[i];
+      for (int p2 = 0; p2 < HT / 2; ++p2) {
+        c[u][2 * p2] = fmaf(cf[3][2 * p2], c[u][2 * p2], acc[u][p2].x);
+        c[u][2 * p2 + 1] = fmaf(cf[3][2 * p2 + 1], c[u][2 * p2 + 1], acc[u][p2].y);
+      }
+  }
+#pragma unroll
+  for (int u = 0; u < NCH; ++u) {
+    const int col = vec ? 0 : jl + u * L;
+    if ((vec && u > 0) || col >= H) continue;
+    float* dst = agg_out + ((long long)b * n_out + q) * H * H + (long long)col * H;
+#pragma unroll
+    for (int i = 0; i < HT; ++i)
+      if (i < H) dst[i] = c[u][i];
+  }
 }
-
 
 template <int CELL, int HT, int NC>
 cudaError_t up_impl(const LeafArgs& a, int C, float* agg_out, long long n_out, long long q0, long long nq,
@@ -828,9 +846,13 @@ cudaError_t launch_leaf_up(const LeafArgs& a, int C, float* agg_out, long long n
   }
 #ifndef BPPSA_LEAF_UP_ROWS
   if (H <= 20) {
-    const long long chains = (long long)a.seg.B * nq * H;
-    if (chains == 0) return cudaSuccess;
-    leaf_up_lc_gru_kernel<20><<<(unsigned)((chains + 127) / 128), 128, 0, st>>>(a, C, agg_out, n_out, q0, nq);
+#ifndef BPPSA_LC_GRU_NCH
+#define BPPSA_LC_GRU_NCH 2
+#endif
+    constexpr int NCH = BPPSA_LC_GRU_NCH;
+    const long long tasks = (long long)a.seg.B * nq * ((H + NCH - 1) / NCH);
+    if (tasks == 0) return cudaSuccess;
+    leaf_up_lc_gru_kernel<20, NCH><<<(unsigned)((tasks + 127) / 128), 128, 0, st>>>(a, C, agg_out, n_out, q0, nq);
     return cudaGetLastError();
   }
 #endif
