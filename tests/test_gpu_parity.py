@@ -466,6 +466,27 @@ def test_weight_grads_rnn_inputs_tc(lib, I):
         assert rel(dWih, r[0]) <= TOL
 
 
+@pytest.mark.parametrize("T,B,H,I", [(30000, 16, 20, 1), (1999, 7, 20, 3), (2500, 70, 20, 0), (3001, 5, 17, 2),
+                                     (777, 3, 8, 1), (1000, 16, 20, 4)])
+def test_weight_grads_rnn_small_h(lib, T, B, H, I):
+    """The staged small-H kernel (H <= 20, I <= 3: wgrad_rnn_small_kernel): 16-byte
+    copies (H = 20) and 4-byte copies (H = 17, 8), B > one 64-row stage (h_prev
+    crossing stages and parts), parts that start mid-stage (x alignment), I = 0;
+    I = 4 takes the tile kernel.  Random tape, with and without h_init."""
+    rng = np.random.default_rng(T + I)
+    h = rng.uniform(-0.95, 0.95, (T, B, H)).astype(np.float32)
+    g = rng.standard_normal((T, B, H)).astype(np.float32)
+    x = rng.standard_normal((T, B, I)).astype(np.float32)
+    h_init = rng.uniform(-1, 1, (B, H)).astype(np.float32)
+    for hi in (None, h_init):
+        dWih, dWhh, db = lib.weight_grads_rnn(cu(x), cu(h), cu(g), h_init=None if hi is None else cu(hi))
+        torch.cuda.synchronize()
+        r = bp.weight_grads_rnn(x, h, g, h_init=hi)
+        assert rel(dWhh, r[1]) <= TOL and rel(db, r[2]) <= TOL
+        if I:
+            assert rel(dWih, r[0]) <= TOL
+
+
 @pytest.mark.parametrize("set_name,B", [("S", 16), ("L", 64)])
 def test_weight_grads_gru(lib, set_name, B):
     gw = W.gru_workload(set_name, B, seed=3)
