@@ -21,7 +21,9 @@ CFG = {"c4": (1 << 20, 16, 64, 128, 32), "c1": (1000, 16, 20, 8, 8), "c2": (3000
        "c4b512c28": (1 << 20, 16, 64, 512, 28), "c4b512c24": (1 << 20, 16, 64, 512, 24),
        "c4b448c32": (1 << 20, 16, 64, 448, 32), "c4b1024c8": (1 << 20, 16, 64, 1024, 8),
        "c4b1024c64": (1 << 20, 16, 64, 1024, 64), "c2b8": (30000, 16, 20, 8, 8), "c2b32": (30000, 16, 20, 32, 16),
-       "c2b64": (30000, 16, 20, 64, 16), "c2b32c32": (30000, 16, 20, 32, 32), "c2b16c8": (30000, 16, 20, 16, 8)}
+       "c2b64": (30000, 16, 20, 64, 16), "c2b32c32": (30000, 16, 20, 32, 32), "c2b16c8": (30000, 16, 20, 16, 8),
+       "c4b886": (1 << 20, 16, 64, 886, 32), "c4b880": (1 << 20, 16, 64, 880, 32), "c4b947": (1 << 20, 16, 64, 947, 32),
+       "c4b840": (1 << 20, 16, 64, 840, 32)}
 
 
 def run(name, reps=5):
