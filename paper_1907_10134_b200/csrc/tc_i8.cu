@@ -1314,8 +1314,14 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
   const uint32_t a_mine = tmem + ((uint32_t)(quad * 32) << 16) + WK_A_COL + 4 * cq;
   const uint32_t ring = su32(smem + WT_OFF_RING);
   const int half = cq >> 1;
-  const uint32_t hrow_off = (uint32_t)(row * 256 + half * 128);         // my half-row in a stage
-  const int swz = (2 * row + half) & 7;                                 // its 128-byte line's swizzle
+  // stage layout [half][row][32 floats] (the tensor maps put the column half
+  // outermost): a warp's 32 rows are 32 consecutive 128-byte lines, so the
+  // SWIZZLE_128B chunk positions of a column chunk cover all eight 16-byte
+  // slots (the [row][half] layout gave four: 2-way bank conflicts)
+  const int GB = G * B;
+  const uint32_t hrow_off = (uint32_t)((half * GB + row) * 128);        // my half-row in a stage
+  const int swz = (half * GB + row) & 7;                                // its 128-byte line's swizzle
+  const bool in_stage = row < GB;
   const int c0 = (cq & 1) * 4;                                           // my first 16-byte chunk of the line
   const uint32_t red0 = su32(smem + WT_OFF_RED) + (uint32_t)(row * 16);
   const uint32_t dbar = su32(&d_full[0]), hbar0 = su32(&h_full[0]);
@@ -1367,7 +1373,7 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
       my_ss = (a.seg.head && qr == 0) ? 1 : qr * C;
       my_len = min(qr * C + C, S) - my_ss;
     }
-    const uint32_t my_dst = (uint32_t)((G - 1 - lane) * B * 256);
+    const uint32_t my_dst = (uint32_t)((G - 1 - lane) * B * 128);     // + half * GB * 128
     auto c5 = [&](int st, int& c3, int& c4) {
       c3 = R_off - st;
       c4 = A_blk - (int)(qb + G - 1);
@@ -1384,7 +1390,7 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
           asm volatile(
               "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
               "%6}], [%7];\n" ::"r"(stage),
-              "l"(reinterpret_cast<uint64_t>(&h5)), "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(bar)
+              "l"(reinterpret_cast<uint64_t>(&h5)), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(0), "r"(bar)
               : "memory");
         }
       } else {
@@ -1397,11 +1403,13 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
         if (lane == 0) mbar_arrive_tx(bar, bytes);
         __syncwarp();
         if (my_on && st < my_len)
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-              "[%5];\n" ::"r"(stage + my_dst),
-              "l"(reinterpret_cast<uint64_t>(&h3)), "r"(0), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(bar)
-              : "memory");
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];\n" ::"r"(stage + my_dst + (uint32_t)(hf * GB * 128)),
+                "l"(reinterpret_cast<uint64_t>(&h3)), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(hf), "r"(bar)
+                : "memory");
       }
     };
     auto issue_stores = [&](int st, uint32_t gstep) {
@@ -1411,13 +1419,15 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
         if (lane == 0)
           asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(
                            reinterpret_cast<uint64_t>(&g5)),
-                       "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(stage)
+                       "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(0), "r"(stage)
                        : "memory");
       } else if (my_on && st < my_len) {
-        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
-                         reinterpret_cast<uint64_t>(&g3)),
-                     "r"(0), "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(stage + my_dst)
-                     : "memory");
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                           reinterpret_cast<uint64_t>(&g3)),
+                       "r"(0), "r"(a.seg.time_of(my_ss + st) * B), "r"(hf), "r"(stage + my_dst + (uint32_t)(hf * GB * 128))
+                       : "memory");
       }
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     };
@@ -1465,8 +1475,9 @@ __global__ void __launch_bounds__(WK_EPI, 1) tc_walk_i8t_kernel(LeafArgs a, cons
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t hp = stg + (uint32_t)(((c0 + c) ^ swz) << 4);
-        const float4 h4 = lds128(hp);
-        sts128(hp, v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
+        // rows >= G B (no chain) would alias the other half plane's first lines
+        const float4 h4 = in_stage ? lds128(hp) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in_stage) sts128(hp, v[2 * c].x, v[2 * c].y, v[2 * c + 1].x, v[2 * c + 1].y);
         const float2 d0 = make_float2(fmaf(-h4.x, h4.x, 1.f), fmaf(-h4.y, h4.y, 1.f));
         const float2 d1 = make_float2(fmaf(-h4.z, h4.z, 1.f), fmaf(-h4.w, h4.w, 1.f));
         y[2 * c] = apply ? __fmul2_rn(d0, v[2 * c]) : make_float2(0.f, 0.f);
@@ -1595,7 +1606,44 @@ cudaError_t launch_tc_fold_i8(const LeafArgs& a, int C, float* agg_out, long lon
 }
 
 // Level-0 walk of an RNN H = 64 segment on the integer tensor cores.
-cudaError_t make_walk_map(const float* base, int T, int B, int C, long long A, bool five, int G, CUtensorMap* map);
+// Tensor maps over h / grad_h with the column half OUTERMOST, so a box lands
+// in shared memory as [half][rows][32 floats] (SWIZZLE_128B): 5D {col 32, b,
+// step-in-block, block, half} with box {32, B, 1, G, 2}; 3D {col 32, t B + b,
+// half} with box {32, B, 1} (one per half, per group).
+static cudaError_t make_walk_map_split(const float* base, int T, int B, int C, long long A, bool five, int G,
+                                       CUtensorMap* map) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  const cuuint64_t row = (cuuint64_t)TH * sizeof(float);
+  const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+  CUresult r;
+  if (!five) {
+    const cuuint64_t dims[3] = {32, (cuuint64_t)T * B, 2};
+    const cuuint64_t strides[2] = {row, 128};
+    const cuuint32_t box[3] = {32u, (cuuint32_t)B, 1u};
+    r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    if (A < 1) A = 1;
+    const cuuint64_t dims[5] = {32, (cuuint64_t)B, (cuuint64_t)C, (cuuint64_t)A, 2};
+    const cuuint64_t strides[4] = {row, row * B, row * B * C, 128};
+    const cuuint32_t box[5] = {32u, (cuuint32_t)B, 1u, (cuuint32_t)G, 2u};
+    r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 cudaError_t launch_tc_walk_i8(const LeafArgs& a, int C, const float* carry, long long nblk, float* grad_h,
                               float* grad_init, int num_sms, cudaStream_t st) {
@@ -1607,7 +1655,7 @@ cudaError_t launch_tc_walk_i8(const LeafArgs& a, int C, const float* carry, long
     CUtensorMap maps[4];
     cudaError_t e = cudaSuccess;
     for (int m = 0; m < 4 && e == cudaSuccess; ++m)
-      e = make_walk_map(m < 2 ? a.h : grad_h, a.seg.T, B, C, Tm / C, m % 2 == 1, G, &maps[m]);
+      e = make_walk_map_split(m < 2 ? a.h : grad_h, a.seg.T, B, C, Tm / C, m % 2 == 1, G, &maps[m]);
     if (e != cudaSuccess) return e;
     const long long A = Tm / C, nfull = A > 1 ? (A - 1) / G : 0, rem0 = 1 + nfull * G;
     const long long nt = 1 + nfull + (nblk > rem0 ? (nblk - rem0 + 1) / 2 : 0);
