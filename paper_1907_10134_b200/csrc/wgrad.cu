@@ -527,8 +527,7 @@ cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream
   if (w.kind == BPPSA_JAC_GRU && w.H == SG_H && w.E <= SG_XM + 1 && w.I <= SG_XM && w.H + w.E <= SG_UC) {
     const size_t smem = (size_t)(SG_NS * SG_STAGE + SG_RS * (4 * SG_H + SG_UC)) * sizeof(float);
     static_assert((size_t)SG_G * SG_TILES * 16 <= (size_t)SG_NS * SG_STAGE, "reduction fits");
-    cudaError_t e = cudaFuncSetAttribute(wgrad_gru_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(wgrad_gru_small_kernel), (int)smem);
     if (e != cudaSuccess) return e;
     wgrad_gru_small_kernel<<<(unsigned)nparts, SG_NT, smem, st>>>(w, ws);
     return cudaGetLastError();
@@ -536,8 +535,7 @@ cudaError_t run_partials(const WArgs& w, float* ws, long long nparts, cudaStream
   if (w.kind == BPPSA_JAC_RNN_TANH && w.H <= SM_H && w.E <= SM_EMAX) {
     const size_t smem = (size_t)SM_NS * SM_STAGE * sizeof(float);
     static_assert((size_t)SM_SG * SM_TILES * (16 + 4 * SM_EMAX) <= (size_t)SM_NS * SM_STAGE, "reduction fits");
-    cudaError_t e = cudaFuncSetAttribute(wgrad_rnn_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(wgrad_rnn_small_kernel), (int)smem);
     if (e != cudaSuccess) return e;
     wgrad_rnn_small_kernel<<<(unsigned)nparts, SM_NT, smem, st>>>(w, ws);
     return cudaGetLastError();
