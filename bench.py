@@ -257,6 +257,9 @@ def run_ours(args):
     torch.backends.cudnn.allow_tf32 = False
     if world > 1:
         if backend == "nccl":
+            # the communicator-init lines on stderr let the driver count the ranks
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
